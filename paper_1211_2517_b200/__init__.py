@@ -1,0 +1,231 @@
+"""B200-native SVD-compressed KIFMM matvec (arXiv 1211.2517) — Python binding.
+
+Thin ctypes marshalling over the C-ABI of include/kifmm.h; every step of the
+matvec runs in the CUDA kernels of libkifmm_b200.so (csrc/).  PyTorch is used
+only for device memory and streams.  There is no CPU fallback: importing this
+package fails loudly if the library has not been built
+(`python -m paper_1211_2517_b200.build`).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkifmm_b200.so")
+
+FMM_OK, FMM_EINVAL, FMM_ECONFIG, FMM_ECUDA, FMM_ENOMEM = 0, -1, -2, -3, -4
+
+
+class FmmError(RuntimeError):
+    pass
+
+
+class TablesView(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_int), ("n", ctypes.c_int), ("k", ctypes.c_int), ("d", ctypes.c_double),
+                ("U", ctypes.c_void_p), ("C", ctypes.c_void_p), ("S", ctypes.c_void_p), ("T", ctypes.c_void_p),
+                ("M", ctypes.c_void_p), ("L", ctypes.c_void_p)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_int), ("k", ctypes.c_int), ("leaf_size", ctypes.c_int), ("d", ctypes.c_double),
+                ("pinv_rcond", ctypes.c_double), ("wx_direct_max", ctypes.c_int),
+                ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("p", ctypes.c_int), ("n", ctypes.c_int), ("k", ctypes.c_int),
+                ("kp", ctypes.c_int), ("nboxes", ctypes.c_int), ("nleaves", ctypes.c_int), ("nlevels", ctypes.c_int),
+                ("nU", ctypes.c_int64), ("nV", ctypes.c_int64), ("nW", ctypes.c_int64), ("nX", ctypes.c_int64),
+                ("n_s2m", ctypes.c_int64), ("n_xnd", ctypes.c_int64), ("n_l2t", ctypes.c_int64),
+                ("n_wnd", ctypes.c_int64), ("m2l_tiles", ctypes.c_int64), ("m2l_pairs", ctypes.c_int64),
+                ("r0", ctypes.c_double), ("lo_root", ctypes.c_double * 3), ("precompute_ms", ctypes.c_double),
+                ("tree_ms", ctypes.c_double), ("lists_ms", ctypes.c_double), ("schedule_ms", ctypes.c_double),
+                ("phase_ms", ctypes.c_float * 8)]
+
+
+PHASES = ("p2p", "s2m", "m2m", "m2l", "x", "l2l", "l2t_w", "output")
+
+# every symbol declared in include/kifmm.h
+EXPORTS = ("fmm_default_options", "fmm_setup", "fmm_setup_ex", "fmm_matvec", "fmm_matvec_host", "fmm_free",
+           "fmm_info", "fmm_export_tree", "fmm_export_lists", "fmm_export_phase", "fmm_tables_build",
+           "fmm_tables_view_get", "fmm_tables_free", "fmm_last_error")
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: the CUDA library has not been built "
+                              "(python -m paper_1211_2517_b200.build); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.fmm_default_options.argtypes = [ctypes.POINTER(Options)]
+        L.fmm_default_options.restype = None
+        L.fmm_setup.argtypes = [vp, vp, i64, ci, ci, ci, ctypes.POINTER(vp)]
+        L.fmm_setup_ex.argtypes = [vp, vp, i64, ctypes.POINTER(Options), vp, ctypes.POINTER(vp)]
+        L.fmm_matvec.argtypes = [vp, vp, vp, vp]
+        L.fmm_matvec_host.argtypes = [vp, vp, vp, vp]
+        L.fmm_free.argtypes = [vp]
+        L.fmm_free.restype = None
+        L.fmm_info.argtypes = [vp, ctypes.POINTER(Info)]
+        L.fmm_export_tree.argtypes = [vp] + [vp] * 8
+        L.fmm_export_lists.argtypes = [vp] + [vp] * 4
+        L.fmm_export_phase.argtypes = [vp, ci, vp]
+        L.fmm_tables_build.argtypes = [ci, ci, ctypes.c_double, ctypes.c_double, ctypes.POINTER(vp)]
+        L.fmm_tables_view_get.argtypes = [vp, ctypes.POINTER(TablesView), ctypes.POINTER(ctypes.POINTER(ctypes.c_double))]
+        L.fmm_tables_free.argtypes = [vp]
+        L.fmm_tables_free.restype = None
+        L.fmm_last_error.argtypes = []
+        L.fmm_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != FMM_OK:
+        raise FmmError(f"{what} failed ({rc}): {lib().fmm_last_error().decode()}")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def fmm_tables_build(p: int, k: int, d: float = 0.1, rcond: float = 1e-10) -> dict:
+    """Host precompute of the operator tables (no GPU needed)."""
+    h = ctypes.c_void_p()
+    _check(lib().fmm_tables_build(p, k, d, rcond, ctypes.byref(h)), "fmm_tables_build")
+    try:
+        v = TablesView()
+        sig = ctypes.POINTER(ctypes.c_double)()
+        _check(lib().fmm_tables_view_get(h, ctypes.byref(v), ctypes.byref(sig)), "fmm_tables_view_get")
+        n, k_ = v.n, v.k
+
+        def arr(ptr, shape):
+            cnt = int(np.prod(shape))
+            return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_double)), shape=(cnt,)).reshape(shape).copy()
+
+        return dict(p=v.p, n=n, k=k_, d=v.d, rcond=rcond, U=arr(v.U, (n, k_)), C=arr(v.C, (316, k_, k_)),
+                    S=arr(v.S, (k_, n)), T=arr(v.T, (n, k_)), M=arr(v.M, (8, k_, k_)), L=arr(v.L, (8, k_, k_)),
+                    sigma=np.ctypeslib.as_array(sig, shape=(n,)).copy())
+    finally:
+        lib().fmm_tables_free(h)
+
+
+class Plan:
+    """An immutable FMM plan (tree, lists, operator tables) on the current device."""
+
+    def __init__(self, points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, d: float = 0.1,
+                 rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
+                 stream=None):
+        import torch
+        if not (isinstance(points, torch.Tensor) and points.is_cuda):
+            raise TypeError("points must be a CUDA tensor [N, 3] float64")
+        self.points = points.contiguous().to(torch.float64)
+        self.N = self.points.shape[0]
+        opt = Options()
+        lib().fmm_default_options(ctypes.byref(opt))
+        opt.p, opt.k, opt.leaf_size, opt.d, opt.pinv_rcond = p, k, leaf_size, d, rcond
+        opt.wx_direct_max, opt.profile = wx_direct_max, int(profile)
+        self._keep = []
+        if tables is not None:
+            arrs = {x: np.ascontiguousarray(tables[x], dtype=np.float64) for x in "UCSTML"}
+            self._keep.append(arrs)
+            tv = TablesView(tables["p"], tables["n"], tables["k"], tables["d"], *(arrs[x].ctypes.data for x in "UCSTML"))
+            self._keep.append(tv)
+            opt.tables = ctypes.pointer(tv)
+        dens = None
+        if densities is not None:
+            dens = densities.contiguous().to(torch.float64)
+        h = ctypes.c_void_p()
+        _check(lib().fmm_setup_ex(ctypes.c_void_p(self.points.data_ptr()),
+                                  ctypes.c_void_p(dens.data_ptr()) if dens is not None else None,
+                                  self.N, ctypes.byref(opt), _stream_ptr(stream), ctypes.byref(h)), "fmm_setup")
+        self._h = h
+        self.info = self.get_info()
+
+    def __del__(self):
+        self.free()
+
+    def free(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.fmm_free(self._h)
+            self._h = None
+
+    def get_info(self) -> dict:
+        inf = Info()
+        _check(lib().fmm_info(self._h, ctypes.byref(inf)), "fmm_info")
+        out = {name: getattr(inf, name) for name, _ in Info._fields_ if name not in ("lo_root", "phase_ms")}
+        out["lo_root"] = list(inf.lo_root)
+        out["phase_ms"] = dict(zip(PHASES, list(inf.phase_ms)))
+        return out
+
+    def matvec(self, density=None, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.N, dtype=torch.float64, device=self.points.device)
+        dptr = None
+        if density is not None:
+            if not (density.is_cuda and density.dtype == torch.float64 and density.is_contiguous()):
+                raise TypeError("density must be a contiguous CUDA float64 tensor")
+            dptr = ctypes.c_void_p(density.data_ptr())
+        _check(lib().fmm_matvec(self._h, dptr, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)), "fmm_matvec")
+        return out
+
+    def matvec_host(self, density: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
+        density = np.ascontiguousarray(density, dtype=np.float64)
+        if out is None:
+            out = np.empty(self.N, dtype=np.float64)
+        _check(lib().fmm_matvec_host(self._h, density.ctypes.data, out.ctypes.data, _stream_ptr(stream)),
+               "fmm_matvec_host")
+        return out
+
+    def export_tree(self) -> dict:
+        nb = self.info["nboxes"]
+        t = dict(level=np.zeros(nb, np.int32), key=np.zeros(nb, np.uint64), parent=np.zeros(nb, np.int32),
+                 pbeg=np.zeros(nb, np.int32), pend=np.zeros(nb, np.int32), leaf=np.zeros(nb, np.uint8),
+                 perm=np.zeros(self.N, np.int32), geom=np.zeros(5))
+        _check(lib().fmm_export_tree(self._h, *(t[x].ctypes.data for x in
+                                               ("level", "key", "parent", "pbeg", "pend", "leaf", "perm", "geom"))),
+               "fmm_export_tree")
+        return t
+
+    def export_lists(self) -> dict:
+        i = self.info
+        out = dict(U=np.zeros((i["nU"], 2), np.int32), V=np.zeros((i["nV"], 3), np.int32),
+                   W=np.zeros((i["nW"], 3), np.int32), X=np.zeros((i["nX"], 3), np.int32))
+        _check(lib().fmm_export_lists(self._h, *(out[x].ctypes.data for x in "UVWX")), "fmm_export_lists")
+        return out
+
+    def export_phase(self, which: str) -> np.ndarray:
+        idx = {"qhat": 0, "lhat": 1, "near": 2, "far": 3}[which]
+        if idx < 2:
+            out = np.zeros((self.info["nboxes"], self.info["k"]))
+        else:
+            out = np.zeros(self.N)
+        _check(lib().fmm_export_phase(self._h, idx, out.ctypes.data), "fmm_export_phase")
+        return out
+
+
+# C-ABI-named entry points (same names as include/kifmm.h)
+def fmm_setup(points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, **kw) -> Plan:
+    return Plan(points, densities, p=p, k=k, leaf_size=leaf_size, **kw)
+
+
+def fmm_matvec(plan: Plan, density=None, potential=None, stream=None):
+    return plan.matvec(density, potential, stream)
+
+
+def fmm_matvec_host(plan: Plan, density: np.ndarray, potential: np.ndarray | None = None, stream=None):
+    return plan.matvec_host(density, potential, stream)
+
+
+def fmm_free(plan: Plan) -> None:
+    plan.free()

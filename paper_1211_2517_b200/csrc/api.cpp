@@ -1,0 +1,319 @@
+// C-ABI of the B200 KIFMM library (include/kifmm.h).
+#include "../../include/kifmm.h"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "fmm_internal.h"
+
+struct fmm_plan {
+  kifmm::Plan P;
+  double* d_default_density = nullptr;
+  double precompute_ms = 0, tree_ms = 0, lists_ms = 0, schedule_ms = 0;
+};
+
+struct fmm_tables {
+  kifmm::HostTables H;
+};
+
+namespace kifmm {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+}  // namespace kifmm
+
+using kifmm::set_error;
+
+namespace {
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void free_plan_memory(fmm_plan* h) {
+  kifmm::Plan& P = h->P;
+  for (void* p : P.allocations) cudaFree(p);
+  P.allocations.clear();
+  kifmm::Tree& T = P.tree;
+  void* tp[] = {T.d_key, T.d_level, T.d_parent, T.d_pbeg, T.d_pend, T.d_child_begin, T.d_nchild, T.d_leaf, T.d_geom,
+                T.d_perm, T.d_pts, P.lists.d_U, P.lists.d_V, P.lists.d_W, P.lists.d_X, h->d_default_density};
+  for (void* p : tp)
+    if (p) cudaFree(p);
+  for (auto e : P.ev_phase) cudaEventDestroy(e);
+  P.ev_phase.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+void fmm_default_options(fmm_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->p = 6;
+  o->k = 60;
+  o->leaf_size = 128;
+  o->d = 0.1;
+  o->pinv_rcond = 1e-10;
+  o->wx_direct_max = -1;
+  o->tables = nullptr;
+  o->profile = 0;
+}
+
+const char* fmm_last_error(void) { return kifmm::last_error(); }
+
+int fmm_tables_build(int p, int k, double d, double rcond, fmm_tables** out) {
+  if (!out || p < 2 || k < 1 || !(d >= 0 && d < 2.0 / 3.0) || !(rcond >= 0)) {
+    set_error("fmm_tables_build: invalid argument");
+    return FMM_EINVAL;
+  }
+  *out = nullptr;
+  fmm_tables* t = new (std::nothrow) fmm_tables();
+  if (!t) { set_error("fmm_tables_build: out of host memory"); return FMM_ENOMEM; }
+  int rc = kifmm::build_tables(p, k, d, rcond, &t->H);
+  if (rc) { delete t; return rc; }
+  *out = t;
+  return FMM_OK;
+}
+
+int fmm_tables_view_get(const fmm_tables* t, fmm_tables_view* v, const double** sigma) {
+  if (!t || !v) { set_error("fmm_tables_view_get: null argument"); return FMM_EINVAL; }
+  const kifmm::HostTables& H = t->H;
+  v->p = H.p; v->n = H.n; v->k = H.k; v->d = H.d;
+  v->U = H.U.data(); v->C = H.C.data(); v->S = H.S.data(); v->T = H.T.data(); v->M = H.M.data(); v->L = H.L.data();
+  if (sigma) *sigma = H.sigma.data();
+  return FMM_OK;
+}
+
+void fmm_tables_free(fmm_tables* t) { delete t; }
+
+int fmm_setup(const double* points, const double* densities, int64_t N, int p, int k, int leaf_size, fmm_plan** out) {
+  fmm_options o;
+  fmm_default_options(&o);
+  o.p = p; o.k = k; o.leaf_size = leaf_size;
+  return fmm_setup_ex(points, densities, N, &o, nullptr, out);
+}
+
+int fmm_setup_ex(const double* points, const double* densities, int64_t N, const fmm_options* opt, void* stream,
+                 fmm_plan** out) {
+  if (!out) { set_error("fmm_setup: out is NULL"); return FMM_EINVAL; }
+  *out = nullptr;
+  if (!opt || !points || N < 1 || N > INT32_MAX || opt->p < 2 || opt->k < 1 || opt->leaf_size < 1 ||
+      !(opt->d >= 0 && opt->d < 2.0 / 3.0) || !(opt->pinv_rcond >= 0)) {
+    set_error("fmm_setup: invalid argument (points, N in [1, 2^31), p >= 2, k >= 1, leaf_size >= 1, 0 <= d < 2/3)");
+    return FMM_EINVAL;
+  }
+  const int n_expect = 6 * (opt->p - 1) * (opt->p - 1) + 2;
+  if (opt->p * 1 > 0 && n_expect > 296) { set_error("fmm_setup: p > 8 is not supported (n <= 296)"); return FMM_EINVAL; }
+  fmm_plan* h = new (std::nothrow) fmm_plan();
+  if (!h) { set_error("fmm_setup: out of host memory"); return FMM_ENOMEM; }
+  kifmm::Plan& P = h->P;
+  cudaStream_t st = (cudaStream_t)stream;
+  P.stream = st;
+  cudaGetDevice(&P.device);
+  P.leaf_size = opt->leaf_size;
+  P.d = opt->d;
+  P.rcond = opt->pinv_rcond;
+  P.profile = opt->profile != 0;
+  auto fail = [&](int rc) { free_plan_memory(h); delete h; return rc; };
+  if (kifmm::kernels_init()) return fail(FMM_ECUDA);
+  // ---- operator tables
+  auto t0 = std::chrono::steady_clock::now();
+  if (opt->tables) {
+    const fmm_tables_view* v = opt->tables;
+    if (v->p != opt->p || v->n != n_expect || v->k < 1 || v->k > v->n || !v->U || !v->C || !v->S || !v->T || !v->M ||
+        !v->L || std::fabs(v->d - opt->d) > 1e-15) {
+      set_error("fmm_setup: operator tables do not match (p, n, k, d)");
+      return fail(FMM_ECONFIG);
+    }
+    kifmm::HostTables& H = P.tables;
+    H.p = v->p; H.n = v->n; H.k = v->k; H.d = v->d; H.rcond = opt->pinv_rcond;
+    const size_t n = v->n, k = v->k;
+    H.U.assign(v->U, v->U + n * k);
+    H.C.assign(v->C, v->C + 316 * k * k);
+    H.S.assign(v->S, v->S + k * n);
+    H.T.assign(v->T, v->T + n * k);
+    H.M.assign(v->M, v->M + 8 * k * k);
+    H.L.assign(v->L, v->L + 8 * k * k);
+    // surface grid (same enumeration as the precompute)
+    H.surf.clear();
+    const int pp = v->p;
+    for (int i = 0; i < pp; ++i)
+      for (int j = 0; j < pp; ++j)
+        for (int l = 0; l < pp; ++l)
+          if (i == 0 || j == 0 || l == 0 || i == pp - 1 || j == pp - 1 || l == pp - 1) {
+            H.surf.push_back(-1.0 + 2.0 / (pp - 1) * i);
+            H.surf.push_back(-1.0 + 2.0 / (pp - 1) * j);
+            H.surf.push_back(-1.0 + 2.0 / (pp - 1) * l);
+          }
+  } else {
+    int rc = kifmm::build_tables(opt->p, opt->k, opt->d, opt->pinv_rcond, &P.tables);
+    if (rc) return fail(rc);
+  }
+  h->precompute_ms = ms_since(t0);
+  P.p = P.tables.p;
+  P.n = P.tables.n;
+  P.k = P.tables.k;
+  P.kp = (P.k + 7) / 8 * 8;
+  P.np = (P.n + 7) / 8 * 8;
+  P.wx = opt->wx_direct_max < 0 ? P.n : opt->wx_direct_max;
+  if (kifmm::upload_tables(P)) return fail(FMM_ECUDA);
+  // ---- device tree + lists
+  P.tree.N = N;
+  t0 = std::chrono::steady_clock::now();
+  if (kifmm::build_tree_device(P, points, st)) return fail(FMM_ECUDA);
+  h->tree_ms = ms_since(t0);
+  t0 = std::chrono::steady_clock::now();
+  if (kifmm::build_lists_device(P, st)) return fail(FMM_ECUDA);
+  h->lists_ms = ms_since(t0);
+  t0 = std::chrono::steady_clock::now();
+  if (kifmm::build_schedules(P, st)) return fail(FMM_ECUDA);
+  h->schedule_ms = ms_since(t0);
+  if (densities) {
+    if (cudaMalloc(&h->d_default_density, sizeof(double) * N) != cudaSuccess ||
+        cudaMemcpyAsync(h->d_default_density, densities, sizeof(double) * N, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      set_error("fmm_setup: copying the default densities failed");
+      return fail(FMM_ECUDA);
+    }
+  }
+  P.ev_phase.resize(9);
+  for (auto& e : P.ev_phase) cudaEventCreate(&e);
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    set_error("fmm_setup: CUDA error during setup");
+    return fail(FMM_ECUDA);
+  }
+  *out = h;
+  return FMM_OK;
+}
+
+int fmm_matvec(fmm_plan* h, const double* density, double* potential, void* stream) {
+  if (!h || !potential) { set_error("fmm_matvec: null plan or potential"); return FMM_EINVAL; }
+  const double* q = density ? density : h->d_default_density;
+  if (!q) { set_error("fmm_matvec: no density given and none at setup"); return FMM_EINVAL; }
+  int rc = kifmm::matvec_device(h->P, q, potential, (cudaStream_t)stream);
+  return rc ? FMM_ECUDA : FMM_OK;
+}
+
+int fmm_matvec_host(fmm_plan* h, const double* h_density, double* h_potential, void* stream) {
+  if (!h || !h_density || !h_potential) { set_error("fmm_matvec_host: null argument"); return FMM_EINVAL; }
+  kifmm::Plan& P = h->P;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t N = P.tree.N;
+  double* d_q = P.d_io;
+  double* d_p = P.d_io + N;
+  if (cudaMemcpyAsync(d_q, h_density, sizeof(double) * N, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    set_error("fmm_matvec_host: H2D copy failed");
+    return FMM_ECUDA;
+  }
+  int rc = kifmm::matvec_device(P, d_q, d_p, st);
+  if (rc) return FMM_ECUDA;
+  if (cudaMemcpyAsync(h_potential, d_p, sizeof(double) * N, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("fmm_matvec_host: D2H copy failed");
+    return FMM_ECUDA;
+  }
+  return FMM_OK;
+}
+
+void fmm_free(fmm_plan* h) {
+  if (!h) return;
+  free_plan_memory(h);
+  delete h;
+}
+
+int fmm_info(const fmm_plan* h, fmm_info_t* info) {
+  if (!h || !info) { set_error("fmm_info: null argument"); return FMM_EINVAL; }
+  const kifmm::Plan& P = h->P;
+  std::memset(info, 0, sizeof(*info));
+  info->N = P.tree.N;
+  info->p = P.p; info->n = P.n; info->k = P.k; info->kp = P.kp;
+  info->nboxes = P.tree.nboxes; info->nleaves = P.tree.nleaves; info->nlevels = P.tree.nlevels;
+  info->nU = P.lists.nU; info->nV = P.lists.nV; info->nW = P.lists.nW; info->nX = P.lists.nX;
+  info->n_s2m = P.n_s2m; info->n_xnd = P.n_xnd; info->n_l2t = P.n_l2t; info->n_wnd = P.n_wnd;
+  info->m2l_tiles = P.g_m2l.ntiles; info->m2l_pairs = P.g_m2l.npairs;
+  info->r0 = P.tree.r0;
+  for (int d = 0; d < 3; ++d) info->lo_root[d] = P.tree.lo_root[d];
+  info->precompute_ms = h->precompute_ms; info->tree_ms = h->tree_ms; info->lists_ms = h->lists_ms;
+  info->schedule_ms = h->schedule_ms;
+  if (P.profile && P.profiled && P.ev_phase.size() == 9 && cudaEventSynchronize(P.ev_phase[8]) == cudaSuccess)
+    for (int i = 0; i < 8; ++i) cudaEventElapsedTime(&info->phase_ms[i], P.ev_phase[i], P.ev_phase[i + 1]);
+  return FMM_OK;
+}
+
+int fmm_export_tree(const fmm_plan* h, int32_t* level, uint64_t* key, int32_t* parent, int32_t* pbeg, int32_t* pend,
+                    uint8_t* leaf, int32_t* perm, double* geom) {
+  if (!h) { set_error("fmm_export_tree: null plan"); return FMM_EINVAL; }
+  const kifmm::Tree& T = h->P.tree;
+  const size_t nb = T.nboxes;
+  for (size_t b = 0; b < nb; ++b) {
+    if (level) level[b] = T.level[b];
+    if (key) key[b] = T.key[b];
+    if (parent) parent[b] = T.parent[b];
+    if (pbeg) pbeg[b] = T.pbeg[b];
+    if (pend) pend[b] = T.pend[b];
+    if (leaf) leaf[b] = T.leaf[b];
+  }
+  if (perm && cudaMemcpy(perm, T.d_perm, sizeof(int32_t) * T.N, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    set_error("fmm_export_tree: copy failed");
+    return FMM_ECUDA;
+  }
+  if (geom) {
+    for (int d = 0; d < 3; ++d) geom[d] = T.lo_root[d];
+    geom[3] = T.r0;
+    geom[4] = T.scale;
+  }
+  return FMM_OK;
+}
+
+int fmm_export_lists(const fmm_plan* h, int32_t* U, int32_t* V, int32_t* W, int32_t* X) {
+  if (!h) { set_error("fmm_export_lists: null plan"); return FMM_EINVAL; }
+  const kifmm::Lists& L = h->P.lists;
+  std::vector<int4> tmp;
+  if (U && L.nU && cudaMemcpy(U, L.d_U, sizeof(int2) * L.nU, cudaMemcpyDeviceToHost) != cudaSuccess) goto err;
+  if (V && L.nV) {
+    tmp.resize(L.nV);
+    if (cudaMemcpy(tmp.data(), L.d_V, sizeof(int4) * L.nV, cudaMemcpyDeviceToHost) != cudaSuccess) goto err;
+    for (int i = 0; i < L.nV; ++i) { V[3 * i] = tmp[i].x; V[3 * i + 1] = tmp[i].y; V[3 * i + 2] = tmp[i].z; }
+  }
+  if (W && L.nW) {
+    tmp.resize(L.nW);
+    if (cudaMemcpy(tmp.data(), L.d_W, sizeof(int4) * L.nW, cudaMemcpyDeviceToHost) != cudaSuccess) goto err;
+    for (int i = 0; i < L.nW; ++i) { W[3 * i] = tmp[i].x; W[3 * i + 1] = tmp[i].y; W[3 * i + 2] = tmp[i].z; }
+  }
+  if (X && L.nX) {
+    tmp.resize(L.nX);
+    if (cudaMemcpy(tmp.data(), L.d_X, sizeof(int4) * L.nX, cudaMemcpyDeviceToHost) != cudaSuccess) goto err;
+    for (int i = 0; i < L.nX; ++i) { X[3 * i] = tmp[i].x; X[3 * i + 1] = tmp[i].y; X[3 * i + 2] = tmp[i].z; }
+  }
+  return FMM_OK;
+err:
+  set_error("fmm_export_lists: copy failed");
+  return FMM_ECUDA;
+}
+
+int fmm_export_phase(const fmm_plan* h, int which, double* out) {
+  if (!h || !out || which < 0 || which > 3) { set_error("fmm_export_phase: invalid argument"); return FMM_EINVAL; }
+  const kifmm::Plan& P = h->P;
+  if (cudaDeviceSynchronize() != cudaSuccess) { set_error("fmm_export_phase: device error"); return FMM_ECUDA; }
+  if (which >= 2) {
+    const double* src = which == 2 ? P.d_pot_near : P.d_pot_far;
+    if (cudaMemcpy(out, src, sizeof(double) * P.tree.N, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      set_error("fmm_export_phase: copy failed");
+      return FMM_ECUDA;
+    }
+    return FMM_OK;
+  }
+  const double* src = which == 0 ? P.d_qhat : P.d_lhat;
+  const size_t nb = P.tree.nboxes;
+  std::vector<double> tmp(nb * P.kp);
+  if (cudaMemcpy(tmp.data(), src, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    set_error("fmm_export_phase: copy failed");
+    return FMM_ECUDA;
+  }
+  for (size_t b = 0; b < nb; ++b)
+    for (int a = 0; a < P.k; ++a) out[b * P.k + a] = tmp[b * P.kp + a];
+  return FMM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// Internal structures of the B200 KIFMM library (not part of the C-ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace kifmm {
+
+constexpr int kNumOffsets = 316;  // M2L offsets per level
+
+struct HostTables {
+  int p = 0, n = 0, k = 0;
+  double d = 0.1, rcond = 1e-10;
+  std::vector<double> sigma;   // singular values of K_fat (n)
+  std::vector<double> surf;    // unit surface grid (n x 3)
+  std::vector<double> U;       // n x k
+  std::vector<double> C;       // 316 x k x k
+  std::vector<double> S;       // k x n
+  std::vector<double> T;       // n x k
+  std::vector<double> M;       // 8 x k x k
+  std::vector<double> L;       // 8 x k x k
+};
+
+int build_tables(int p, int k, double d, double rcond, HostTables* out);
+
+// One launch of the grouped gather-GEMM-scatter kernel: Y[tgt] (+)= scale * Op * X[src].
+struct GemmTile {
+  int op;        // operator index within the op array
+  int begin;     // first pair
+  int count;     // pairs in this tile (<= tile width)
+  int pad;
+  double scale;  // level factor applied to the product
+};
+
+struct GemmLaunch {
+  int ntiles = 0;
+  GemmTile* d_tiles = nullptr;
+  int2* d_pairs = nullptr;  // (src row, tgt row)
+  int npairs = 0;
+};
+
+struct Tree {
+  int64_t N = 0;
+  int nboxes = 0, nleaves = 0, nlevels = 0;
+  double lo_root[3] = {0, 0, 0}, r0 = 1, scale = 1;
+  std::vector<int> level_begin;       // nlevels + 1
+  // device
+  uint64_t* d_key = nullptr;          // per box: Morton prefix at its level
+  int* d_level = nullptr;
+  int* d_parent = nullptr;
+  int* d_pbeg = nullptr;
+  int* d_pend = nullptr;
+  int* d_child_begin = nullptr;       // first child (children contiguous), -1 for leaves
+  int* d_nchild = nullptr;
+  uint8_t* d_leaf = nullptr;
+  double4* d_geom = nullptr;          // (cx, cy, cz, r)
+  int32_t* d_perm = nullptr;          // sorted -> caller
+  double4* d_pts = nullptr;           // sorted points (x, y, z, q)
+  // host mirrors (setup-time copies)
+  std::vector<uint64_t> key;
+  std::vector<int> level, parent, pbeg, pend, child_begin, nchild;
+  std::vector<uint8_t> leaf;
+};
+
+struct Lists {
+  // canonical device lists
+  int nU = 0, nV = 0, nW = 0, nX = 0;
+  int2* d_U = nullptr;     // (tgt, src) by (tgt, src)
+  int4* d_V = nullptr;     // (tgt, src, off, 0) by (off, tgt)
+  int4* d_W = nullptr;     // (tgt, src, direct, 0) by (tgt, src)
+  int4* d_X = nullptr;     // (tgt, src, direct, 0) by (tgt, src)
+};
+
+struct Plan {
+  int device = 0;
+  int p = 0, k = 0, kp = 0, n = 0, leaf_size = 0, wx = 0;
+  double d = 0.1, rcond = 1e-10;
+  Tree tree;
+  Lists lists;
+  HostTables tables;   // host copy (unpadded)
+  // device operator tables, zero-padded to kp
+  double* d_C = nullptr;    // 316 x kp x kp
+  double* d_M = nullptr;    // 8 x kp x kp
+  double* d_L = nullptr;    // 8 x kp x kp
+  double* d_S = nullptr;    // kp x n    (S')
+  double* d_Ut = nullptr;   // kp x n    (U^T)
+  double* d_T = nullptr;    // n x kp    (T')
+  double* d_Ue = nullptr;   // n x kp    (U)
+  double* d_surf = nullptr; // n x 3 unit surface grid
+  // work buffers
+  double* d_qhat = nullptr;     // nboxes x kp (level-normalised q^')
+  double* d_lhat = nullptr;     // nboxes x kp
+  double* d_chk_s2m = nullptr;  // n_s2m x n  check potentials of leaves (S2M stage 1)
+  double* d_chk_x = nullptr;    // n_xnd x n  check potentials of non-direct X pairs
+  double* d_eqd_l2t = nullptr;  // n_l2t x n  downward equivalent densities
+  double* d_eqd_w = nullptr;    // n_wnd x n  upward equivalent densities of W sources
+  double* d_pot_near = nullptr; // N (sorted)
+  double* d_pot_far = nullptr;  // N (sorted)
+  double* d_io = nullptr;       // N staging for host-buffer matvec
+  // evaluation work lists (k_eval items: (box, out row, 0, 0); CSR of segments (kind, a, b, len))
+  int np = 0;                                  // n rounded up to a multiple of 8
+  int n_tleaf = 0; int4* d_tleaf_items = nullptr;
+  int* d_near_off = nullptr; int4* d_near_seg = nullptr; int n_near_seg = 0;
+  int* d_far_off = nullptr;  int4* d_far_seg = nullptr;  int n_far_seg = 0;
+  int n_s2m = 0; int4* d_s2m_items = nullptr; int* d_s2m_off = nullptr; int4* d_s2m_seg = nullptr;
+  int n_xnd = 0; int4* d_x_items = nullptr;   int* d_x_off = nullptr;   int4* d_x_seg = nullptr;
+  int n_l2t = 0, n_wnd = 0;
+  std::vector<void*> allocations;              // everything cudaMalloc'ed for the plan
+  // dense-algebra launches
+  GemmLaunch g_s2m, g_m2l, g_x, g_l2t, g_w;
+  std::vector<GemmLaunch> g_m2m;   // per child level (descending)
+  std::vector<GemmLaunch> g_l2l;   // per parent level (ascending)
+  // timing of the last matvec (ms per phase), filled when profiling is on
+  std::vector<float> phase_ms;
+  cudaStream_t stream = nullptr;
+  cudaStream_t stream_near = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::vector<cudaEvent_t> ev_phase;
+  bool profile = false;
+  bool profiled = false;  // a profiled matvec has recorded the phase events
+};
+
+// error helpers (thread-local last error)
+void set_error(const std::string& msg);
+const char* last_error();
+
+#define KIFMM_CUDA(call)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      ::kifmm::set_error(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + \
+                         ":" + std::to_string(__LINE__));                                   \
+      return -3;                                                                            \
+    }                                                                                       \
+  } while (0)
+
+// setup stages (tree.cu, lists.cu) and matvec launches (kernels.cu)
+int build_tree_device(Plan& P, const double* d_points_caller, cudaStream_t st);
+int build_lists_device(Plan& P, cudaStream_t st);
+int build_schedules(Plan& P, cudaStream_t st);
+int upload_tables(Plan& P);
+int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t st);
+int kernels_init();
+int ggs_tile_width(int M, int K);
+
+}  // namespace kifmm

@@ -1,0 +1,269 @@
+// Host precompute of the SVD-compressed KIFMM operator tables (runs once per
+// (p, k, d); timed separately from the matvec, as the north_star asks).
+//
+// All operators at unit halfwidth (homogeneous kernel of degree -1);
+// the level factors live in the matvec (reading Q15).
+//   surfaces  P:109-113  UE, DC at (1+d); UC, DE at (3-2d); p points per edge
+//   E_u, E_d  P:126-154  equivalent-density solves, pinv by one-sided Jacobi SVD
+//   K_delta   P:136-144  K_ij = G(x_i, y_j), x = DC(target @ 0), y = UE(source @ 2 delta)
+//   basis U   P:172-203  leading left singular vectors of K_fat (= those of K_thin,
+//                        P:199-203) from a cyclic-Jacobi eigensolve of K_fat K_fat^T
+//   C_delta   P:216-223  U^T K_delta U
+//   S', T'    P:341, P:351   S' = U^T pinv(E_u), T' = pinv(E_d) U (fused, reading Q17)
+//   M~_o, L~_o P:337, P:347  U^T pinv(E_u) G(UC, UE_child) U,  U^T G(DC_child, DE) pinv(E_d) U
+// Own dense linear algebra (no LAPACK in this image); shares no code with oracle/.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "fmm_internal.h"
+
+namespace kifmm {
+
+namespace {
+
+using Mat = std::vector<double>;  // row-major
+
+std::vector<double> unit_surface(int p) {
+  std::vector<double> g;
+  const double h = 2.0 / (p - 1);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      for (int k = 0; k < p; ++k) {
+        bool on = i == 0 || j == 0 || k == 0 || i == p - 1 || j == p - 1 || k == p - 1;
+        if (!on) continue;
+        g.push_back(-1.0 + h * i);
+        g.push_back(-1.0 + h * j);
+        g.push_back(-1.0 + h * k);
+      }
+  return g;
+}
+
+// G(x_i, y_j) = 1/(4 pi |x_i - y_j|) for x = a*g + ca, y = b*g + cb
+Mat kmat(const std::vector<double>& g, int n, double a, const double ca[3], double b, const double cb[3]) {
+  Mat K((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double r2 = 0;
+      for (int d = 0; d < 3; ++d) {
+        double t = (a * g[3 * i + d] + ca[d]) - (b * g[3 * j + d] + cb[d]);
+        r2 += t * t;
+      }
+      K[(size_t)i * n + j] = 1.0 / (4.0 * M_PI * std::sqrt(r2));
+    }
+  return K;
+}
+
+// C = A (m x k) * B (k x n)
+Mat matmul(const Mat& A, const Mat& B, int m, int k, int n) {
+  Mat C((size_t)m * n, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < m; ++i)
+    for (int l = 0; l < k; ++l) {
+      double a = A[(size_t)i * k + l];
+      if (a == 0.0) continue;
+      const double* b = &B[(size_t)l * n];
+      double* c = &C[(size_t)i * n];
+      for (int j = 0; j < n; ++j) c[j] += a * b[j];
+    }
+  return C;
+}
+
+Mat transpose(const Mat& A, int m, int n) {
+  Mat T((size_t)n * m);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < n; ++j) T[(size_t)j * m + i] = A[(size_t)i * n + j];
+  return T;
+}
+
+// Moore-Penrose pseudo-inverse by one-sided (Hestenes) Jacobi SVD of a square A;
+// singular values <= rcond * sigma_max are dropped (reading Q11).
+Mat pinv_jacobi(const Mat& A, int n, double rcond) {
+  // work on columns: W = A (n x n, column j = W[:, j]); V accumulates rotations
+  Mat W = transpose(A, n, n);  // row c of W = column c of A
+  Mat V((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0;
+    for (int i = 0; i < n - 1; ++i)
+      for (int j = i + 1; j < n; ++j) {
+        double* wi = &W[(size_t)i * n];
+        double* wj = &W[(size_t)j * n];
+        double al = 0, be = 0, ga = 0;
+        for (int r = 0; r < n; ++r) { al += wi[r] * wi[r]; be += wj[r] * wj[r]; ga += wi[r] * wj[r]; }
+        if (ga == 0.0) continue;
+        double rel = std::fabs(ga) / std::sqrt(al * be);
+        off = std::max(off, rel);
+        if (rel < 1e-15) continue;
+        double zeta = (be - al) / (2.0 * ga);
+        double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+        for (int r = 0; r < n; ++r) {
+          double x = wi[r], y = wj[r];
+          wi[r] = c * x - s * y;
+          wj[r] = s * x + c * y;
+        }
+        double* vi = &V[(size_t)i * n];
+        double* vj = &V[(size_t)j * n];
+        for (int r = 0; r < n; ++r) {
+          double x = vi[r], y = vj[r];
+          vi[r] = c * x - s * y;
+          vj[r] = s * x + c * y;
+        }
+      }
+    if (off < 1e-15) break;
+  }
+  // sigma_c = |W_c|, u_c = W_c / sigma_c; A = sum_c sigma_c u_c v_c^T with v_c = row c of V
+  std::vector<double> sig(n);
+  double smax = 0;
+  for (int c = 0; c < n; ++c) {
+    double s2 = 0;
+    for (int r = 0; r < n; ++r) s2 += W[(size_t)c * n + r] * W[(size_t)c * n + r];
+    sig[c] = std::sqrt(s2);
+    smax = std::max(smax, sig[c]);
+  }
+  // pinv = sum_c v_c u_c^T / sigma_c = sum_c v_c W_c^T / sigma_c^2
+  Mat P((size_t)n * n, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < n; ++c) {
+      if (!(sig[c] > rcond * smax)) continue;
+      double f = V[(size_t)c * n + i] / (sig[c] * sig[c]);
+      const double* w = &W[(size_t)c * n];
+      double* pr = &P[(size_t)i * n];
+      for (int j = 0; j < n; ++j) pr[j] += f * w[j];
+    }
+  return P;
+}
+
+// Cyclic Jacobi eigendecomposition of a symmetric n x n matrix. Returns
+// eigenvalues descending; column c of `vec` (row-major n x n) is eigenvector c.
+void jacobi_eig(Mat A, int n, std::vector<double>& val, Mat& vec) {
+  Mat V((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+  double scale = 0;
+  for (int i = 0; i < n; ++i) scale = std::max(scale, std::fabs(A[(size_t)i * n + i]));
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) off = std::max(off, std::fabs(A[(size_t)p * n + q]));
+    if (off <= 1e-18 * scale) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        double apq = A[(size_t)p * n + q];
+        if (std::fabs(apq) <= 1e-300) continue;
+        double app = A[(size_t)p * n + p], aqq = A[(size_t)q * n + q];
+        double theta = (aqq - app) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int r = 0; r < n; ++r) {  // columns p, q
+          double arp = A[(size_t)r * n + p], arq = A[(size_t)r * n + q];
+          A[(size_t)r * n + p] = c * arp - s * arq;
+          A[(size_t)r * n + q] = s * arp + c * arq;
+        }
+        for (int r = 0; r < n; ++r) {  // rows p, q
+          double apr = A[(size_t)p * n + r], aqr = A[(size_t)q * n + r];
+          A[(size_t)p * n + r] = c * apr - s * aqr;
+          A[(size_t)q * n + r] = s * apr + c * aqr;
+        }
+        for (int r = 0; r < n; ++r) {
+          double vrp = V[(size_t)r * n + p], vrq = V[(size_t)r * n + q];
+          V[(size_t)r * n + p] = c * vrp - s * vrq;
+          V[(size_t)r * n + q] = s * vrp + c * vrq;
+        }
+      }
+  }
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return A[(size_t)a * n + a] > A[(size_t)b * n + b]; });
+  val.resize(n);
+  vec.assign((size_t)n * n, 0.0);
+  for (int c = 0; c < n; ++c) {
+    val[c] = A[(size_t)idx[c] * n + idx[c]];
+    for (int r = 0; r < n; ++r) vec[(size_t)r * n + c] = V[(size_t)r * n + idx[c]];
+  }
+}
+
+}  // namespace
+
+int build_tables(int p, int k, double d, double rcond, HostTables* out) {
+  const std::vector<double> g = unit_surface(p);
+  const int n = (int)g.size() / 3;
+  const double fin = 1.0 + d, fout = 3.0 - 2.0 * d;
+  const double zero[3] = {0, 0, 0};
+  // equivalent-density solves
+  Mat Eu = kmat(g, n, fout, zero, fin, zero);   // G(UC, UE)
+  Mat Ed = kmat(g, n, fin, zero, fout, zero);   // G(DC, DE)
+  Mat Eui = pinv_jacobi(Eu, n, rcond);
+  Mat Edi = pinv_jacobi(Ed, n, rcond);
+  // the 316 M2L matrices and the Gram matrix of K_fat
+  std::vector<Mat> K(kNumOffsets);
+  int id = 0;
+  for (int i = -3; i <= 3; ++i)
+    for (int j = -3; j <= 3; ++j)
+      for (int l = -3; l <= 3; ++l) {
+        if (std::max(std::abs(i), std::max(std::abs(j), std::abs(l))) <= 1) continue;
+        const double cb[3] = {2.0 * i, 2.0 * j, 2.0 * l};
+        K[id++] = kmat(g, n, fin, zero, fin, cb);
+      }
+  Mat gram((size_t)n * n, 0.0);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b <= a; ++b) {
+      double s = 0;
+      for (int o = 0; o < kNumOffsets; ++o) {
+        const double* ra = &K[o][(size_t)a * n];
+        const double* rb = &K[o][(size_t)b * n];
+        for (int c = 0; c < n; ++c) s += ra[c] * rb[c];
+      }
+      gram[(size_t)a * n + b] = s;
+      gram[(size_t)b * n + a] = s;
+    }
+  std::vector<double> lam;
+  Mat vec;
+  jacobi_eig(gram, n, lam, vec);
+  std::vector<double> sigma(n);
+  for (int i = 0; i < n; ++i) sigma[i] = std::sqrt(std::max(lam[i], 0.0));
+  // k_eff: smallest k' >= k with sigma_k' - sigma_k'+1 > 1e-8 sigma_1 (reading Q12)
+  int kk = std::min(k, n);
+  while (kk < n && !(sigma[kk - 1] - sigma[kk] > 1e-8 * sigma[0])) ++kk;
+  Mat U((size_t)n * kk);
+  for (int c = 0; c < kk; ++c) {
+    int arg = 0;
+    for (int r = 0; r < n; ++r)
+      if (std::fabs(vec[(size_t)r * n + c]) > std::fabs(vec[(size_t)arg * n + c])) arg = r;
+    double sgn = vec[(size_t)arg * n + c] < 0 ? -1.0 : 1.0;
+    for (int r = 0; r < n; ++r) U[(size_t)r * kk + c] = sgn * vec[(size_t)r * n + c];
+  }
+  Mat Ut = transpose(U, n, kk);
+  out->p = p; out->n = n; out->k = kk; out->d = d; out->rcond = rcond;
+  out->sigma = sigma;
+  out->U = U;
+  out->C.assign((size_t)kNumOffsets * kk * kk, 0.0);
+  for (int o = 0; o < kNumOffsets; ++o) {
+    Mat KU = matmul(K[o], U, n, n, kk);
+    Mat c = matmul(Ut, KU, kk, n, kk);
+    std::memcpy(&out->C[(size_t)o * kk * kk], c.data(), sizeof(double) * kk * kk);
+  }
+  out->S = matmul(Ut, Eui, kk, n, n);
+  out->T = matmul(Edi, U, n, n, kk);
+  out->M.assign((size_t)8 * kk * kk, 0.0);
+  out->L.assign((size_t)8 * kk * kk, 0.0);
+  for (int o = 0; o < 8; ++o) {
+    const double cc[3] = {(o >> 2) & 1 ? 0.5 : -0.5, (o >> 1) & 1 ? 0.5 : -0.5, o & 1 ? 0.5 : -0.5};
+    Mat Gu = kmat(g, n, fout, zero, 0.5 * fin, cc);   // G(UC_parent, UE_child)
+    Mat m1 = matmul(out->S, Gu, kk, n, n);            // U^T pinv(E_u) G
+    Mat Mo = matmul(m1, U, kk, n, kk);
+    std::memcpy(&out->M[(size_t)o * kk * kk], Mo.data(), sizeof(double) * kk * kk);
+    Mat Gd = kmat(g, n, 0.5 * fin, cc, fout, zero);   // G(DC_child, DE_parent)
+    Mat l1 = matmul(Ut, Gd, kk, n, n);
+    Mat Lo = matmul(l1, out->T, kk, n, kk);            // U^T G pinv(E_d) U
+    std::memcpy(&out->L[(size_t)o * kk * kk], Lo.data(), sizeof(double) * kk * kk);
+  }
+  out->surf = g;
+  return 0;
+}
+
+}  // namespace kifmm

@@ -1,0 +1,255 @@
+// Launch schedules of the matvec, derived once at setup from the device tree and
+// lists: pair lists + tiles for the grouped GEMM kernel, and segment CSRs for the
+// evaluation kernel.  Applies the W/X "direct" shortcut of reading O5.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <map>
+
+#include "fmm_internal.h"
+
+namespace kifmm {
+
+namespace {
+
+template <typename T>
+int upload(Plan& P, T** dst, const std::vector<T>& v, cudaStream_t st) {
+  KIFMM_CUDA(cudaMalloc((void**)dst, sizeof(T) * std::max<size_t>(v.size(), 1)));
+  P.allocations.push_back(*dst);
+  if (!v.empty()) KIFMM_CUDA(cudaMemcpyAsync(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+struct PairGroup {
+  int op;
+  double scale;
+  std::vector<int2> pairs;
+};
+
+// tiles of <= width pairs that never straddle a group
+int make_launch(Plan& P, GemmLaunch& L, const std::vector<PairGroup>& groups, int width, cudaStream_t st) {
+  std::vector<int2> pairs;
+  std::vector<GemmTile> tiles;
+  for (const auto& g : groups) {
+    int base = (int)pairs.size();
+    pairs.insert(pairs.end(), g.pairs.begin(), g.pairs.end());
+    for (int b = 0; b < (int)g.pairs.size(); b += width)
+      tiles.push_back(GemmTile{g.op, base + b, std::min(width, (int)g.pairs.size() - b), 0, g.scale});
+  }
+  L.npairs = (int)pairs.size();
+  L.ntiles = (int)tiles.size();
+  if (upload(P, &L.d_pairs, pairs, st) || upload(P, &L.d_tiles, tiles, st)) return -3;
+  return 0;
+}
+
+}  // namespace
+
+int build_schedules(Plan& P, cudaStream_t st) {
+  Tree& T = P.tree;
+  Lists& Ls = P.lists;
+  const int nb = T.nboxes, n = P.n, np = P.np, kp = P.kp;
+  // lists back to the host (setup only)
+  std::vector<int2> U(Ls.nU);
+  std::vector<int4> V(Ls.nV), W(Ls.nW), X(Ls.nX);
+  if (Ls.nU) KIFMM_CUDA(cudaMemcpyAsync(U.data(), Ls.d_U, sizeof(int2) * Ls.nU, cudaMemcpyDeviceToHost, st));
+  if (Ls.nV) KIFMM_CUDA(cudaMemcpyAsync(V.data(), Ls.d_V, sizeof(int4) * Ls.nV, cudaMemcpyDeviceToHost, st));
+  if (Ls.nW) KIFMM_CUDA(cudaMemcpyAsync(W.data(), Ls.d_W, sizeof(int4) * Ls.nW, cudaMemcpyDeviceToHost, st));
+  if (Ls.nX) KIFMM_CUDA(cudaMemcpyAsync(X.data(), Ls.d_X, sizeof(int4) * Ls.nX, cudaMemcpyDeviceToHost, st));
+  KIFMM_CUDA(cudaStreamSynchronize(st));
+  if (const char* dir = std::getenv("KIFMM_DUMP")) {  // debugging aid: raw tree + lists
+    auto dump = [&](const char* name, const void* p, size_t bytes) {
+      std::string path = std::string(dir) + "/" + name;
+      if (FILE* f = std::fopen(path.c_str(), "wb")) { std::fwrite(p, 1, bytes, f); std::fclose(f); }
+    };
+    dump("key.bin", T.key.data(), T.key.size() * 8);
+    dump("level.bin", T.level.data(), T.level.size() * 4);
+    dump("parent.bin", T.parent.data(), T.parent.size() * 4);
+    dump("pbeg.bin", T.pbeg.data(), T.pbeg.size() * 4);
+    dump("pend.bin", T.pend.data(), T.pend.size() * 4);
+    dump("leaf.bin", T.leaf.data(), T.leaf.size());
+    dump("child_begin.bin", T.child_begin.data(), T.child_begin.size() * 4);
+    dump("nchild.bin", T.nchild.data(), T.nchild.size() * 4);
+    dump("U.bin", U.data(), U.size() * 8);
+    dump("V.bin", V.data(), V.size() * 16);
+    dump("W.bin", W.data(), W.size() * 16);
+    dump("X.bin", X.data(), X.size() * 16);
+  }
+  // validate the device lists before indexing host arrays with them
+  auto bad = [&](int b) { return b < 0 || b >= nb; };
+  for (auto& u : U)
+    if (bad(u.x) || bad(u.y) || !T.leaf[u.x] || !T.leaf[u.y]) { set_error("build_schedules: corrupt U list"); return -3; }
+  for (auto& v : V)
+    if (bad(v.x) || bad(v.y) || v.z < 0 || v.z >= kNumOffsets) { set_error("build_schedules: corrupt V list"); return -3; }
+  for (auto& w : W)
+    if (bad(w.x) || bad(w.y) || !T.leaf[w.x]) { set_error("build_schedules: corrupt W list"); return -3; }
+  for (auto& x : X)
+    if (bad(x.x) || bad(x.y) || !T.leaf[x.y] || (x.z && !T.leaf[x.x])) { set_error("build_schedules: corrupt X list"); return -3; }
+  auto npts = [&](int b) { return T.pend[b] - T.pbeg[b]; };
+  auto rl = [&](int b) { return std::ldexp(T.r0, -T.level[b]); };
+
+  // ---- target leaves, near (P2P) and far (L2T + W) segment CSRs
+  std::vector<int> leaf_row(nb, -1);
+  std::vector<int4> titems;
+  for (int b = 0; b < nb; ++b)
+    if (T.leaf[b]) { leaf_row[b] = (int)titems.size(); titems.push_back(make_int4(b, (int)titems.size(), 0, 0)); }
+  const int nt = (int)titems.size();
+  std::vector<std::vector<int4>> near(nt), far(nt);
+  for (auto& u : U) near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
+  // W pairs: direct -> P2P over the source subtree; else M2T through the source's equivalent density
+  std::vector<PairGroup> wgroups;  // grouped by source level (scale r_A)
+  std::map<int, int> wlevel;
+  int n_wnd = 0;
+  for (auto& w : W) {
+    if (w.z) {
+      near[leaf_row[w.x]].push_back(make_int4(0, T.pbeg[w.y], 0, npts(w.y)));
+    } else {
+      int lv = T.level[w.y];
+      if (!wlevel.count(lv)) { wlevel[lv] = (int)wgroups.size(); wgroups.push_back(PairGroup{0, rl(w.y), {}}); }
+      wgroups[wlevel[lv]].pairs.push_back(make_int2(w.y, n_wnd));
+      far[leaf_row[w.x]].push_back(make_int4(2, n_wnd, w.y, n));
+      ++n_wnd;
+    }
+  }
+  // X pairs: direct (target leaf small) -> P2P; else S2L through the target's check potential
+  std::vector<int4> xitems, xsegs;
+  std::vector<int> xoff{0};
+  std::vector<PairGroup> xgroup{PairGroup{0, 1.0, {}}};
+  for (auto& x : X) {
+    if (x.z) {
+      near[leaf_row[x.x]].push_back(make_int4(0, T.pbeg[x.y], 0, npts(x.y)));
+    } else {
+      int row = (int)xitems.size();
+      xitems.push_back(make_int4(x.x, row, 0, 0));
+      xsegs.push_back(make_int4(0, T.pbeg[x.y], 0, npts(x.y)));
+      xoff.push_back((int)xsegs.size());
+      xgroup[0].pairs.push_back(make_int2(row, x.x));
+    }
+  }
+  // L2T for leaves at level >= 2 (grouped by level for the r_l factor)
+  std::vector<PairGroup> lgroups;
+  std::map<int, int> llevel;
+  int n_l2t = 0;
+  for (int i = 0; i < nt; ++i) {
+    int b = titems[i].x;
+    if (T.level[b] < 2) continue;
+    int lv = T.level[b];
+    if (!llevel.count(lv)) { llevel[lv] = (int)lgroups.size(); lgroups.push_back(PairGroup{0, rl(b), {}}); }
+    lgroups[llevel[lv]].pairs.push_back(make_int2(b, n_l2t));
+    far[i].insert(far[i].begin(), make_int4(1, n_l2t, b, n));
+    ++n_l2t;
+  }
+  std::vector<int> near_off{0}, far_off{0};
+  std::vector<int4> near_seg, far_seg;
+  for (int i = 0; i < nt; ++i) {
+    near_seg.insert(near_seg.end(), near[i].begin(), near[i].end());
+    near_off.push_back((int)near_seg.size());
+    far_seg.insert(far_seg.end(), far[i].begin(), far[i].end());
+    far_off.push_back((int)far_seg.size());
+  }
+  P.n_tleaf = nt;
+  P.n_near_seg = (int)near_seg.size();
+  P.n_far_seg = (int)far_seg.size();
+  if (upload(P, &P.d_tleaf_items, titems, st) || upload(P, &P.d_near_off, near_off, st) ||
+      upload(P, &P.d_near_seg, near_seg, st) || upload(P, &P.d_far_off, far_off, st) ||
+      upload(P, &P.d_far_seg, far_seg, st))
+    return -3;
+  // ---- S2M: leaves at level >= 2
+  std::vector<int4> sitems, ssegs;
+  std::vector<int> soff{0};
+  std::vector<PairGroup> sgroup{PairGroup{0, 1.0, {}}};
+  for (int b = 0; b < nb; ++b) {
+    if (!T.leaf[b] || T.level[b] < 2) continue;
+    int row = (int)sitems.size();
+    sitems.push_back(make_int4(b, row, 0, 0));
+    ssegs.push_back(make_int4(0, T.pbeg[b], 0, npts(b)));
+    soff.push_back((int)ssegs.size());
+    sgroup[0].pairs.push_back(make_int2(row, b));
+  }
+  P.n_s2m = (int)sitems.size();
+  P.n_xnd = (int)xitems.size();
+  P.n_l2t = n_l2t;
+  P.n_wnd = n_wnd;
+  if (upload(P, &P.d_s2m_items, sitems, st) || upload(P, &P.d_s2m_off, soff, st) || upload(P, &P.d_s2m_seg, ssegs, st) ||
+      upload(P, &P.d_x_items, xitems, st) || upload(P, &P.d_x_off, xoff, st) || upload(P, &P.d_x_seg, xsegs, st))
+    return -3;
+  // ---- dense-algebra launches
+  const int w_sq = ggs_tile_width(kp, kp), w_kn = ggs_tile_width(kp, np), w_nk = ggs_tile_width(np, kp);
+  if (make_launch(P, P.g_s2m, sgroup, w_kn, st) || make_launch(P, P.g_x, xgroup, w_kn, st) ||
+      make_launch(P, P.g_l2t, lgroups, w_nk, st) || make_launch(P, P.g_w, wgroups, w_nk, st))
+    return -3;
+  // M2L: V is in (offset, target) order -> one group per offset
+  {
+    std::vector<PairGroup> groups;
+    for (auto& v : V) {
+      if (groups.empty() || groups.back().op != v.z) groups.push_back(PairGroup{v.z, 1.0, {}});
+      groups.back().pairs.push_back(make_int2(v.y, v.x));
+    }
+    if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
+  }
+  // M2M per child level (finest first) and L2L per parent level (coarsest first), by octant
+  P.g_m2m.clear();
+  P.g_l2l.clear();
+  for (int l = T.nlevels - 1; l >= 3; --l) {
+    std::vector<PairGroup> groups(8);
+    for (int o = 0; o < 8; ++o) groups[o] = PairGroup{o, 0.5, {}};
+    for (int b = T.level_begin[l]; b < T.level_begin[l + 1]; ++b) groups[T.key[b] & 7].pairs.push_back(make_int2(b, T.parent[b]));
+    P.g_m2m.emplace_back();
+    if (make_launch(P, P.g_m2m.back(), groups, w_sq, st)) return -3;
+  }
+  for (int l = 2; l + 1 < T.nlevels; ++l) {
+    std::vector<PairGroup> groups(8);
+    for (int o = 0; o < 8; ++o) groups[o] = PairGroup{o, 1.0, {}};
+    for (int b = T.level_begin[l + 1]; b < T.level_begin[l + 2]; ++b) groups[T.key[b] & 7].pairs.push_back(make_int2(T.parent[b], b));
+    P.g_l2l.emplace_back();
+    if (make_launch(P, P.g_l2l.back(), groups, w_sq, st)) return -3;
+  }
+  // ---- work buffers (padding columns stay zero)
+  auto zalloc = [&](double** p, size_t cnt) -> int {
+    KIFMM_CUDA(cudaMalloc((void**)p, sizeof(double) * std::max<size_t>(cnt, 1)));
+    P.allocations.push_back(*p);
+    KIFMM_CUDA(cudaMemsetAsync(*p, 0, sizeof(double) * std::max<size_t>(cnt, 1), st));
+    return 0;
+  };
+  if (zalloc(&P.d_qhat, (size_t)nb * kp) || zalloc(&P.d_lhat, (size_t)nb * kp) ||
+      zalloc(&P.d_chk_s2m, (size_t)P.n_s2m * np) || zalloc(&P.d_chk_x, (size_t)P.n_xnd * np) ||
+      zalloc(&P.d_eqd_l2t, (size_t)n_l2t * np) || zalloc(&P.d_eqd_w, (size_t)n_wnd * np) ||
+      zalloc(&P.d_pot_near, T.N) || zalloc(&P.d_pot_far, T.N) || zalloc(&P.d_io, 2 * T.N))
+    return -3;
+  KIFMM_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int upload_tables(Plan& P) {
+  const HostTables& H = P.tables;
+  const int k = H.k, n = H.n, kp = P.kp, np = P.np;
+  std::vector<double> C((size_t)316 * kp * kp, 0.0), M((size_t)8 * kp * kp, 0.0), L((size_t)8 * kp * kp, 0.0);
+  std::vector<double> S((size_t)kp * np, 0.0), Ut((size_t)kp * np, 0.0), Tt((size_t)np * kp, 0.0), Ue((size_t)np * kp, 0.0);
+  for (int o = 0; o < 316; ++o)
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) C[((size_t)o * kp + a) * kp + b] = H.C[((size_t)o * k + a) * k + b];
+  for (int o = 0; o < 8; ++o)
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) {
+        M[((size_t)o * kp + a) * kp + b] = H.M[((size_t)o * k + a) * k + b];
+        L[((size_t)o * kp + a) * kp + b] = H.L[((size_t)o * k + a) * k + b];
+      }
+  for (int a = 0; a < k; ++a)
+    for (int i = 0; i < n; ++i) {
+      S[(size_t)a * np + i] = H.S[(size_t)a * n + i];
+      Ut[(size_t)a * np + i] = H.U[(size_t)i * k + a];
+      Tt[(size_t)i * kp + a] = H.T[(size_t)i * k + a];
+      Ue[(size_t)i * kp + a] = H.U[(size_t)i * k + a];
+    }
+  cudaStream_t st = P.stream;
+  if (upload(P, &P.d_C, C, st) || upload(P, &P.d_M, M, st) || upload(P, &P.d_L, L, st) || upload(P, &P.d_S, S, st) ||
+      upload(P, &P.d_Ut, Ut, st) || upload(P, &P.d_T, Tt, st) || upload(P, &P.d_Ue, Ue, st))
+    return -3;
+  if (upload(P, &P.d_surf, H.surf, st)) return -3;
+  KIFMM_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+}  // namespace kifmm

@@ -1,0 +1,60 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol declared in
+include/kifmm.h, validates arguments without touching a GPU, and its host
+precompute agrees with the oracle's tables on what is basis-independent."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1211_2517_b200 as K
+from oracle import precompute as pc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "kifmm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fmm_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = K.lib()
+    syms = header_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(K.EXPORTS) == syms
+
+
+def test_invalid_arguments_are_rejected_without_gpu():
+    L = K.lib()
+    out = ctypes.c_void_p()
+    for N, p, k, s in [(0, 6, 60, 128), (10, 1, 60, 128), (10, 6, 0, 128), (10, 6, 60, 0)]:
+        rc = L.fmm_setup(ctypes.c_void_p(8), None, N, p, k, s, ctypes.byref(out))
+        assert rc == K.FMM_EINVAL and out.value is None
+        assert b"invalid" in L.fmm_last_error()
+    assert L.fmm_setup(None, None, 10, 6, 60, 128, ctypes.byref(out)) == K.FMM_EINVAL
+    assert L.fmm_matvec(None, None, None, None) == K.FMM_EINVAL
+    L.fmm_free(None)
+    assert L.fmm_tables_build(4, 24, 0.7, 1e-10, ctypes.byref(out)) == K.FMM_EINVAL
+
+
+@pytest.mark.parametrize("p,k,keff,sub_tol", [(4, 24, 25, 1e-9), (6, 60, 61, 1e-6)])
+def test_host_precompute_matches_oracle_tables(p, k, keff, sub_tol):
+    a = K.fmm_tables_build(p, k)
+    b = pc.build_tables(p, k)
+    assert a["k"] == b["k"] == keff and a["n"] == b["n"]
+    np.testing.assert_allclose(a["sigma"][:keff + 1], b["sigma"][:keff + 1], rtol=1e-6)
+    # basis-independent quantities: projector, U C U^T, U S', T' U^T, U M U^T, U L U^T
+    Pa, Pb = a["U"] @ a["U"].T, b["U"] @ b["U"].T
+    assert np.abs(Pa - Pb).max() < sub_tol
+    for d in (0, 100, 315):
+        x, y = a["U"] @ a["C"][d] @ a["U"].T, b["U"] @ b["C"][d] @ b["U"].T
+        assert np.abs(x - y).max() <= 1e3 * sub_tol * np.abs(y).max()
+    for o in (0, 7):
+        x, y = a["U"] @ a["M"][o] @ a["U"].T, b["U"] @ b["M"][o] @ b["U"].T
+        assert np.abs(x - y).max() <= 1e3 * sub_tol * np.abs(y).max()
+    assert np.abs(a["U"].T @ a["U"] - np.eye(keff)).max() < 1e-12

@@ -1,0 +1,170 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+* tree and lists: bit-exact (canonical dumps compared element by element)
+* matvec on the oracle's operator tables: rel L2 <= 1e-11 (north_star), per phase too
+* accuracy vs the direct sum: GPU error <= oracle error + 1e-12
+* own host precompute: within the intrinsic table-sensitivity bound
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth_inputs
+from oracle import precompute as pc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def K():
+    import paper_1211_2517_b200 as K
+    return K
+
+
+def sphere(n, seed):
+    rng = np.random.default_rng(seed)
+    g = rng.normal(size=(n, 3))
+    return g / np.linalg.norm(g, axis=1, keepdims=True), rng.uniform(-1, 1, n)
+
+
+def clustered(n, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.random((n // 2, 3))
+    b = 0.5 + 0.01 * rng.normal(size=(n - n // 2, 3))
+    return np.vstack([a, b]), rng.uniform(-1, 1, n)
+
+
+_TABLES = {}
+
+
+def tables(p, k):
+    if (p, k) not in _TABLES:
+        _TABLES[(p, k)] = pc.build_tables(p, k)
+    return _TABLES[(p, k)]
+
+
+def gpu_plan(pts, p, k, s, wx=-1, tb=None, q=None, **kw):
+    dev = torch.device("cuda:0")
+    P = torch.from_numpy(pts).to(dev)
+    Q = None if q is None else torch.from_numpy(q).to(dev)
+    return K().Plan(P, Q, p=p, k=k, leaf_size=s, wx_direct_max=wx, tables=tb, **kw)
+
+
+CASES = {
+    "C1": lambda: synth_inputs.make("C1")[:2] + (4, 24, 64),
+    "sphere6k_s16": lambda: sphere(6000, 1) + (6, 60, 16),
+    "clustered4k_s8": lambda: clustered(4000, 2) + (4, 24, 8),
+    "octa_sphere32k": lambda: synth_inputs.sphere_octa(6)[:2] + (8, 100, 128),
+    "torus50k": lambda: synth_inputs.torus(50000) + (6, 60, 128),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_tree_and_lists_bit_exact(case):
+    pts, q, p, k, s = CASES[case]()
+    tb = tables(p, k)
+    op = oracle.Plan(pts, s, tb["n"])
+    gp = gpu_plan(pts, p, k, s, tb=tb)
+    to, tg = op.tree(), gp.export_tree()
+    for f in ("level", "key", "parent", "pbeg", "pend", "leaf", "perm"):
+        assert np.array_equal(to[f], tg[f]), f
+    assert np.array_equal(to["geom"], tg["geom"])
+    lo, lg = op.lists(), gp.export_lists()
+    for f in "UVWX":
+        assert lo[f].shape == lg[f].shape, f
+        assert np.array_equal(lo[f], lg[f]), f
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("wx", [-1, 0])
+def test_matvec_parity_shared_tables(case, wx):
+    pts, q, p, k, s = CASES[case]()
+    tb = tables(p, k)
+    op = oracle.Plan(pts, s, tb["n"] if wx < 0 else wx)
+    ref, ph = op.matvec(tb, q, phases=True)
+    gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb)
+    out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel(out, ref) <= TOL
+    # per-phase parity localises failures.  q^' and l^ are intermediate: S' = U^T pinv(E_u)
+    # has entries ~1e3-1e8 x those of q^ at p = 8 (cond E_u 4e11), so summation-order
+    # rounding in them is amplified in directions the later steps annihilate; the
+    # phase tolerance scales with that amplification.
+    amp = {4: 1.0, 6: 1.0, 8: 30.0}[p]
+    for name in ("qhat", "lhat"):
+        a, b = gp.export_phase(name), ph[name]
+        if np.linalg.norm(b) > 0:
+            assert rel(a, b) <= amp * TOL, name
+    assert rel(gp.export_phase("near"), ph["near"]) <= TOL
+    if np.linalg.norm(ph["far"]) > 0:
+        assert rel(gp.export_phase("far"), ph["far"]) <= TOL
+
+
+def test_c2_full_size_parity():
+    # BASELINE configs[1] at full size, in the launch configuration bench.py times
+    pts, q, cfg = synth_inputs.make("C2")
+    tb = tables(cfg["p"], cfg["k"])
+    op = oracle.Plan(pts, cfg["leaf"], tb["n"])
+    ref = op.matvec(tb, q)
+    gp = gpu_plan(pts, cfg["p"], cfg["k"], cfg["leaf"], tb=tb)
+    out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert gp.info["nlevels"] == 6 and gp.info["nleaves"] == 32768
+    assert rel(out, ref) <= TOL
+    # accuracy vs the direct sum on a seeded sample of targets
+    idx = np.random.default_rng(0).choice(pts.shape[0], 2048, replace=False)
+    d = oracle.direct(pts, q, idx)
+    assert rel(out[idx], d) <= rel(ref[idx], d) + 1e-12
+
+
+def test_accuracy_vs_direct_within_oracle_error():
+    pts, q, cfg = synth_inputs.make("C1")
+    d = oracle.direct(pts, q)
+    for p, k in [(4, 24), (6, 60), (8, 100)]:
+        tb = tables(p, k)
+        ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
+        out = gpu_plan(pts, p, k, 64, tb=tb).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+        assert rel(out, d) <= rel(ref, d) + 1e-12
+
+
+@pytest.mark.parametrize("p,k,bound", [(4, 24, 1e-10), (6, 60, 1e-7), (8, 100, 1e-5)])
+def test_own_precompute_within_intrinsic_bound(p, k, bound):
+    # independent precomputes differ by the basis sensitivity
+    pts, q, _ = synth_inputs.make("C1")
+    tb = tables(p, k)
+    ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
+    out = gpu_plan(pts, p, k, 64).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel(out, ref) <= bound
+    d = oracle.direct(pts, q)
+    assert rel(out, d) <= 2 * rel(ref, d) + 1e-12
+
+
+def test_edge_cases():
+    dev = torch.device("cuda:0")
+    tb = tables(4, 24)
+    # N = 1, N <= leaf size (root leaf, pure near field), exact duplicates
+    for pts, q in [(np.array([[0.3, 0.2, 0.1]]), np.array([2.0])),
+                   (np.random.default_rng(1).random((50, 3)), np.random.default_rng(2).uniform(-1, 1, 50)),
+                   (np.array([[0.0, 0, 0], [0.0, 0, 0], [0.0, 3.0, 4.0]]), np.array([1.0, 2.0, 5.0]))]:
+        out = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
+        np.testing.assert_allclose(out, oracle.direct(pts, q), rtol=1e-14, atol=1e-300)
+    # zero density, linearity, default density, host-buffer path
+    pts, q, _ = synth_inputs.make("C1")
+    gp = gpu_plan(pts, 4, 24, 64, tb=tb, q=q)
+    assert torch.all(gp.matvec(torch.zeros(pts.shape[0], dtype=torch.float64, device=dev)) == 0)
+    q2 = np.random.default_rng(3).uniform(-1, 1, q.size)
+    a = gp.matvec(torch.from_numpy(0.5 * q - 2 * q2).to(dev)).cpu().numpy()
+    b = 0.5 * gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy() - 2 * gp.matvec(torch.from_numpy(q2).to(dev)).cpu().numpy()
+    assert rel(a, b) < 1e-13
+    # default density == explicit density (atomic scatter-adds reorder sums: not bitwise)
+    assert rel(gp.matvec().cpu().numpy(), gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
+    host = gp.matvec_host(q)
+    assert rel(host, gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
+    # exact 2x scaling (up to atomic reduction order)
+    s1 = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
+    s2 = gpu_plan(2 * pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
+    assert rel(s2, 0.5 * s1) < 1e-14
