@@ -1,0 +1,260 @@
+"""Benchmark: one FP64 KIFMM matvec per step (BASELINE.json metric: FMM matvec
+points/sec and M2L FP64 tensor-pipe fraction of peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Workload (N=1): BASELINE.json configs[1] = "C2": 1,048,576 points uniform in the
+unit cube (seed 0), densities U[-1,1], p = 6 (n = 152), k = 60 (k_eff 61), leaf
+128.  A step is one whole fmm_matvec (permute, S2M, M2M, M2L, X, L2L, L2T, W,
+P2P, unpermute) with the inputs resident in HBM; L2 is flushed (a 256 MiB write)
+between timed steps, outside the timed events.  Multi-GPU (torchrun): every rank
+runs its own replica of the workload (weak scaling, no collective; DESIGN.md
+"Multi-GPU").  `--impl reference` times the CPU oracle (oracle/) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth_inputs  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+METRIC = "FMM matvec points/sec (FP64)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 20 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # first sample lands before the timed loop starts
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is None:
+            return
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        self.rows = [[x.strip() for x in ln.split(",")] for ln in out.strip().splitlines() if ln.count(",") >= 5]
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def oracle_matvec_timer(pts, q, cfg, reps: int = 1):
+    """Time the oracle (as it stands) on the host cores: one full matvec per rep."""
+    import oracle
+    tb = oracle.precompute.build_tables(cfg["p"], cfg["k"])
+    plan = oracle.Plan(pts, cfg["leaf"], tb["n"])
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        plan.matvec(tb, q)
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    pts, q, cfg = synth_inputs.make(args.config)
+    N = cfg["N"]
+    # warm-up and timed steps: each step one full oracle matvec of the same workload
+    ts = oracle_matvec_timer(pts, q, cfg, reps=args.warmup + args.steps)[args.warmup:]
+    sec = float(np.mean(ts))
+    value = N / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "N": N, "p": cfg["p"], "k": cfg["k"], "leaf_size": cfg["leaf"],
+                   "kind": cfg["kind"]},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": f"full {args.config} matvec (N={N}) per step, oracle/ C++ -O2 OpenMP"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1211_2517_b200 as K
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pts, q, cfg = synth_inputs.make(args.config)
+    N = cfg["N"]
+    stream = torch.cuda.current_stream()
+    P = torch.from_numpy(pts).to(dev)
+    Q = torch.from_numpy(q).to(dev)
+    t0 = time.perf_counter()
+    plan = K.Plan(P, Q, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    out = torch.empty(N, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(max(3, args.warmup)):
+        plan.matvec(Q, out)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    m2l_ms, phase_tot, launches = 0.0, {}, 0
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # L2 flush outside the timed events
+            evs[i][0].record(stream)
+            plan.matvec(Q, out)
+            evs[i][1].record(stream)
+            inf = plan.get_info()  # waits for this step's phase events
+            for kname, v in inf["phase_ms"].items():
+                phase_tot[kname] = phase_tot.get(kname, 0.0) + v
+            launches += inf["launches"]
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.sum(step_ms)) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    phase = {k: v / args.steps for k, v in phase_tot.items()}
+    info = plan.get_info()
+    # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside the timing
+    hq = torch.from_numpy(q).pin_memory()
+    hp = torch.empty(N, dtype=torch.float64).pin_memory()
+    hq_np, hp_np = hq.numpy(), hp.numpy()
+    for _ in range(3):
+        plan.matvec_host(hq_np, hp_np)
+    if ws > 1:
+        dist.barrier()
+    e2e_steps = max(5, args.steps // 2)
+    te = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.matvec_host(hq_np, hp_np)
+    e2e_s = (time.perf_counter() - te) / e2e_steps
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    # ---- roofline of the dominant kernel (M2L, DMMA) from the live per-phase events
+    k = info["k"]
+    m2l_flops = 2.0 * k * k * info["nV"]
+    m2l_s = phase["m2l"] * 1e-3
+    peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")))
+    peak = float(peaks["dmma_m8n8k4_tflops"])
+    achieved = m2l_flops / m2l_s / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "m2l_dram_bytes.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("bytes_per_launch")
+    # ---- cpu baseline: the oracle on the host cores, one full matvec (rank 0, N = 1 only)
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        ts = oracle_matvec_timer(pts, q, cfg, reps=1)
+        cpu = {"value": N / ts[0], "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"one full {args.config} matvec (N={N}), oracle/ C++ -O2 OpenMP, {ts[0]:.2f} s"}
+    value = N * ws / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "N_per_gpu": N, "p": cfg["p"], "k": cfg["k"], "k_eff": k,
+                   "leaf_size": cfg["leaf"], "kind": cfg["kind"], "parallelism": f"replicas{ws}",
+                   "l2": "flushed (256 MiB write) between timed steps"},
+        "roofline": {"bound": "tensor", "kernel": "k_ggs (M2L, DMMA.8x8x4 FP64)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": "measured: tools/microbench/fp64_peaks.cu DMMA m8n8k4 loop on this pool's B200 "
+                                    "(profiles/fp64_peaks_r01.json)",
+                     "flops_per_launch": m2l_flops, "ms_per_launch": phase["m2l"]},
+        "phase_ms": phase,
+        "clocks": clk.summary(),
+        "e2e": {"value": N * ws / e2e_s, "unit": "points/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+                "ms_per_step": e2e_s * 1e3, "api": "fmm_matvec_host (pinned host buffers)"},
+        "gpu_launches": launches,
+        "setup_s": setup_s,
+        "precompute_ms": info["precompute_ms"],
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

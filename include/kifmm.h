@@ -75,6 +75,7 @@ typedef struct {
   int64_t nU, nV, nW, nX;     /* list sizes (pairs of boxes) */
   int64_t n_s2m, n_xnd, n_l2t, n_wnd;  /* evaluation work items */
   int64_t m2l_tiles, m2l_pairs;
+  int64_t launches;           /* kernels of this library launched by the last fmm_matvec */
   double r0, lo_root[3];
   double precompute_ms, tree_ms, lists_ms, schedule_ms;
   float phase_ms[8];          /* last profiled matvec: P2P, S2M, M2M, M2L, X, L2L, L2T+W, output */

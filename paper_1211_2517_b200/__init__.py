@@ -41,6 +41,7 @@ class Info(ctypes.Structure):
                 ("nU", ctypes.c_int64), ("nV", ctypes.c_int64), ("nW", ctypes.c_int64), ("nX", ctypes.c_int64),
                 ("n_s2m", ctypes.c_int64), ("n_xnd", ctypes.c_int64), ("n_l2t", ctypes.c_int64),
                 ("n_wnd", ctypes.c_int64), ("m2l_tiles", ctypes.c_int64), ("m2l_pairs", ctypes.c_int64),
+                ("launches", ctypes.c_int64),
                 ("r0", ctypes.c_double), ("lo_root", ctypes.c_double * 3), ("precompute_ms", ctypes.c_double),
                 ("tree_ms", ctypes.c_double), ("lists_ms", ctypes.c_double), ("schedule_ms", ctypes.c_double),
                 ("phase_ms", ctypes.c_float * 8)]

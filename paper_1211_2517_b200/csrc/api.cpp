@@ -232,6 +232,7 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
   info->nU = P.lists.nU; info->nV = P.lists.nV; info->nW = P.lists.nW; info->nX = P.lists.nX;
   info->n_s2m = P.n_s2m; info->n_xnd = P.n_xnd; info->n_l2t = P.n_l2t; info->n_wnd = P.n_wnd;
   info->m2l_tiles = P.g_m2l.ntiles; info->m2l_pairs = P.g_m2l.npairs;
+  info->launches = P.launches;
   info->r0 = P.tree.r0;
   for (int d = 0; d < 3; ++d) info->lo_root[d] = P.tree.lo_root[d];
   info->precompute_ms = h->precompute_ms; info->tree_ms = h->tree_ms; info->lists_ms = h->lists_ms;

@@ -119,7 +119,8 @@ struct Plan {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_phase;
   bool profile = false;
-  bool profiled = false;  // a profiled matvec has recorded the phase events
+  bool profiled = false;
+  int launches = 0;       // kernels of this library launched by the last matvec  // a profiled matvec has recorded the phase events
 };
 
 // error helpers (thread-local last error)

@@ -245,9 +245,12 @@ inline int nblk(int64_t n, int t = 256) { return std::max(1, (int)((n + t - 1) /
 
 int ggs_nt(int M, int K) { return (size_t)(K + 4 + M + 2) * 64 * 8 <= 116 * 1024 ? 64 : 32; }
 
+int g_launches = 0;
+
 int launch_ggs(const GemmLaunch& g, const double* ops, int op_stride, int M, int K, int mvalid, const double* X,
                int ldx, double* Y, int ldy, bool atomic, cudaStream_t st) {
   if (g.ntiles == 0) return 0;
+  ++g_launches;
   const int NT = ggs_nt(M, K);
   const size_t smem = (size_t)NT * (K + 4 + M + 2) * sizeof(double);
   if (NT == 64)
@@ -277,7 +280,9 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
   const int64_t N = T.N;
   const int kp = P.kp, np = P.np, k = P.k, n = P.n;
   auto mark = [&](int i) { if (P.profile) cudaEventRecord(P.ev_phase[i], st); };
+  g_launches = 0;
   mark(0);
+  ++g_launches;
   k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N);
   KIFMM_CUDA(cudaGetLastError());
   KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
@@ -290,6 +295,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     EvalArgs a = ea;
     a.items = P.d_tleaf_items; a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
     k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
+    ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
   mark(1);
@@ -299,6 +305,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     a.items = P.d_s2m_items; a.seg_off = P.d_s2m_off; a.segs = P.d_s2m_seg; a.tgt_f = 3.0 - 2.0 * P.d;
     a.out = P.d_chk_s2m; a.ldo = np;
     k_eval<true><<<P.n_s2m, EV_NT, 0, st>>>(a);
+    ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
   // S2M stage 2: q^'_B = S' c  (store)
@@ -317,6 +324,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     a.items = P.d_x_items; a.seg_off = P.d_x_off; a.segs = P.d_x_seg; a.tgt_f = 1.0 + P.d;
     a.out = P.d_chk_x; a.ldo = np;
     k_eval<true><<<P.n_xnd, EV_NT, 0, st>>>(a);
+    ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
     if (launch_ggs(P.g_x, P.d_Ut, 0, kp, np, k, P.d_chk_x, np, P.d_lhat, kp, true, st)) return -3;
   }
@@ -334,10 +342,13 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     a.items = P.d_tleaf_items; a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far;
     a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
     k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
+    ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
   mark(7);
   k_gather_output<<<nblk(N), 256, 0, st>>>(P.d_pot_near, P.d_pot_far, T.d_perm, N, d_pot);
+  ++g_launches;
+  P.launches = g_launches;
   KIFMM_CUDA(cudaGetLastError());
   mark(8);
   if (P.profile) P.profiled = true;
