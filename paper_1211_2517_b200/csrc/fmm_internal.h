@@ -41,6 +41,15 @@ struct GemmLaunch {
   int npairs = 0;
 };
 
+// Sibling-grouped M2L (k_m2l_sib): tiles (class, first column, count, 0); columns
+// (target, src[8]); classes (nvalid, b[8], offset id[8]) for class = delta * 8 + a.
+struct SibLaunch {
+  int ntiles = 0, ncols = 0;
+  int4* d_tiles = nullptr;
+  int* d_cols = nullptr;
+  int* d_classes = nullptr;
+};
+
 struct Tree {
   int64_t N = 0;
   int nboxes = 0, nleaves = 0, nlevels = 0;
@@ -110,6 +119,8 @@ struct Plan {
   std::vector<void*> allocations;              // everything cudaMalloc'ed for the plan
   // dense-algebra launches
   GemmLaunch g_s2m, g_m2l, g_x, g_l2t, g_w;
+  SibLaunch g_m2l_sib;
+  double sib_min_density = 0.5;   // sibling groups at least this full go to k_m2l_sib
   std::vector<GemmLaunch> g_m2m;   // per child level (descending)
   std::vector<GemmLaunch> g_l2l;   // per parent level (ascending)
   // timing of the last matvec (ms per phase), filled when profiling is on
@@ -145,5 +156,6 @@ int upload_tables(Plan& P);
 int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t st);
 int kernels_init();
 int ggs_tile_width(int M, int K);
+int sib_tile_width(int kp);
 
 }  // namespace kifmm

@@ -96,6 +96,229 @@ __global__ void __launch_bounds__(256) k_ggs(const GemmTile* __restrict__ tiles,
 }
 
 // ----------------------------------------------------------------------------
+// k_ggs_sq: the square (M = K = KP) grouped GEMM of M2L / M2M / L2L, persistent.
+// Each CTA walks a contiguous range of tiles (consecutive tiles mostly share the
+// operator, so its DMMA A-fragments stay in registers).  The B panel of the next
+// tile is gathered with cp.async (LDGSTS, L2 -> smem, 16 B per copy) while the
+// current tile runs on the tensor pipe; results are staged in smem and
+// scatter-added with coalesced RED.F64 rows.  Warp w owns output rows 8w..8w+7.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gmem_src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int KP, int NT>
+__global__ void __launch_bounds__(KP * 4) k_ggs_sq(const GemmTile* __restrict__ tiles, int ntiles,
+                                                 const int2* __restrict__ pairs, const double* __restrict__ ops,
+                                                 int mvalid, const double* X, double* Y, int atomic) {
+  constexpr int NW = KP / 8;        // warps: one 8-row block each
+  constexpr int NTH = NW * 32;
+  constexpr int SB = KP + 4;        // conflict-free B fragment loads
+  constexpr int KS = KP / 4;        // k-steps
+  constexpr int K2 = KP / 2;        // 16-byte chunks per row
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int2 s_pair[3][NT];    // pair indices, two tiles ahead
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  if (t0 >= t1) return;
+
+  // pair indices of tile ti -> s_pair[slot] (cp.async, 8 B each; -1 padding)
+  auto load_pairs = [&](const GemmTile& tl, int slot) {
+    for (int p = threadIdx.x; p < NT; p += NTH) {
+      if (p < tl.count) cp_async8(&s_pair[slot][p], pairs + tl.begin + p);
+      else s_pair[slot][p] = make_int2(-1, -1);
+    }
+  };
+  // B panel of a tile whose pairs are in s_pair[slot] -> buffer buf
+  auto gather = [&](int slot, int buf) {
+    double* B = sm + buf * NT * SB;
+    for (int p = warp; p < NT; p += NW) {
+      const int src = s_pair[slot][p].x;
+      for (int c = lane; c < K2; c += 32) {
+        double* dst = B + p * SB + 2 * c;
+        if (src >= 0) cp_async16(dst, X + (size_t)src * KP + 2 * c);
+        else { dst[0] = 0.0; dst[1] = 0.0; }
+      }
+    }
+  };
+
+  const GemmTile nil{0, 0, 0, 0, 0.0};
+  GemmTile d0 = tiles[t0];
+  GemmTile d1 = t0 + 1 < t1 ? tiles[t0 + 1] : nil;
+  GemmTile d2 = t0 + 2 < t1 ? tiles[t0 + 2] : nil;
+  load_pairs(d0, 0);
+  load_pairs(d1, 1);
+  cp_async_commit();
+  cp_async_wait0();
+  __syncthreads();
+  gather(0, 0);
+  cp_async_commit();
+
+  double a[KS];
+  int cur_op = -1;
+  for (int ti = t0; ti < t1; ++ti) {
+    const int k = ti - t0;
+    const int buf = k & 1, slot = k % 3;
+    cp_async_wait0();
+    __syncthreads();  // B(ti), pairs(ti), pairs(ti+1) landed; zero fills visible
+    GemmTile d3 = ti + 3 < t1 ? tiles[ti + 3] : nil;  // register prefetch, used next iteration
+    if (ti + 1 < t1) gather((k + 1) % 3, buf ^ 1);
+    if (ti + 2 < t1) load_pairs(d2, (k + 2) % 3);
+    cp_async_commit();
+    if (d0.op != cur_op) {
+      cur_op = d0.op;
+      const double* Arow = ops + (size_t)cur_op * KP * KP + (size_t)(warp * 8 + g) * KP + t;
+#pragma unroll
+      for (int s = 0; s < KS; ++s) a[s] = __ldg(Arow + 4 * s);
+    }
+    const double* B = sm + buf * NT * SB;
+    double acc[NT / 8][2];
+#pragma unroll
+    for (int j = 0; j < NT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const double* bp = B + g * SB + 4 * s + t;
+#pragma unroll
+      for (int j = 0; j < NT / 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], a[s], bp[j * 8 * SB]);
+    }
+    // scatter straight from the accumulators: lane (g, t) holds rows warp*8+g of
+    // pairs j*8+2t and j*8+2t+1 (fire-and-forget RED.F64, 64 B contiguous per pair)
+    const double scale = d0.scale;
+    const int row = warp * 8 + g;
+    if (row < mvalid) {
+#pragma unroll
+      for (int j = 0; j < NT / 8; ++j) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int tg = s_pair[slot][j * 8 + 2 * t + c].y;
+          if (tg >= 0) {
+            double* y = Y + (size_t)tg * KP + row;
+            if (atomic) atomicAdd(y, acc[j][c] * scale);
+            else *y = acc[j][c] * scale;
+          }
+        }
+      }
+    }
+    d0 = d1; d1 = d2; d2 = d3;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// k_m2l_sib: M2L grouped by sibling structure.  Every V pair (B, A) joins child a
+// of P = parent(B) with child b of a colleague Q = P + delta of P, and
+// its operator is C_{2 delta + b - a}.  A column = (target B, source parent Q);
+// a tile = up to NT columns of one class (delta, a).  For each non-adjacent b the
+// CTA gathers q^'(child b of Q) (zero if absent) and accumulates
+// C_{2 delta + b - a} q^' in the DMMA accumulators, so each target receives one
+// RED per (target, delta) instead of one per (target, offset).
+// ----------------------------------------------------------------------------
+template <int KP, int NT>
+__global__ void __launch_bounds__(KP * 4) k_m2l_sib(const int4* __restrict__ tiles, int ntiles,
+                                                  const int* __restrict__ cols, const int* __restrict__ classes,
+                                                  const double* __restrict__ C, int mvalid, const double* X, double* Y) {
+  constexpr int NW = KP / 8;
+  constexpr int NTH = NW * 32;
+  constexpr int SB = KP + 4;
+  constexpr int KS = KP / 4;
+  constexpr int K2 = KP / 2;
+  constexpr int CW = 9;                 // column record: target, src[8]
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_meta[2][NT * CW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  if (t0 >= t1) return;
+
+  // class record: [0] = nvalid, [1..8] = b, [9..16] = offset id
+  // simple (synchronous) metadata load: one int per thread iteration
+  auto fetch_meta = [&](int ti, int slot) {
+    const int4 tl = tiles[ti];
+    for (int e = threadIdx.x; e < NT * CW; e += NTH) {
+      int c = e / CW;
+      s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
+    }
+  };
+  auto gather = [&](int slot, int b, int buf) {
+    double* Bd = sm + buf * NT * SB;
+    for (int p = warp; p < NT; p += NW) {
+      const int src = s_meta[slot][p * CW + 1 + b];
+      for (int c = lane; c < K2; c += 32) {
+        double* dst = Bd + p * SB + 2 * c;
+        if (src >= 0) cp_async16(dst, X + (size_t)src * KP + 2 * c);
+        else { dst[0] = 0.0; dst[1] = 0.0; }
+      }
+    }
+  };
+
+  fetch_meta(t0, 0);
+  __syncthreads();
+  int4 tl = tiles[t0];
+  const int* cls = classes + tl.x * 17;
+  gather(0, cls[1], 0);
+  cp_async_commit();
+  int buf = 0;
+  for (int ti = t0; ti < t1; ++ti) {
+    const int mslot = (ti - t0) & 1;
+    tl = tiles[ti];
+    cls = classes + tl.x * 17;
+    const int nv = cls[0];
+    double acc[NT / 8][2];
+#pragma unroll
+    for (int j = 0; j < NT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int jb = 0; jb < nv; ++jb) {
+      cp_async_wait0();
+      __syncthreads();  // B panel (ti, jb) landed
+      if (jb + 1 < nv) {
+        gather(mslot, cls[2 + jb], buf ^ 1);
+      } else if (ti + 1 < t1) {
+        fetch_meta(ti + 1, mslot ^ 1);
+        __syncthreads();
+        const int* ncls = classes + tiles[ti + 1].x * 17;
+        gather(mslot ^ 1, ncls[1], buf ^ 1);
+      }
+      cp_async_commit();
+      double a_cur[KS];
+      {
+        const double* Arow = C + (size_t)cls[9 + jb] * KP * KP + (size_t)(warp * 8 + g) * KP + t;
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) a_cur[s2] = __ldg(Arow + 4 * s2);
+      }
+      const double* B = sm + buf * NT * SB;
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) {
+        const double* bp = B + g * SB + 4 * s2 + t;
+#pragma unroll
+        for (int j = 0; j < NT / 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], a_cur[s2], bp[j * 8 * SB]);
+      }
+      buf ^= 1;
+    }
+    const int row = warp * 8 + g;
+    if (row < mvalid) {
+#pragma unroll
+      for (int j = 0; j < NT / 8; ++j) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int tg = s_meta[mslot][(j * 8 + 2 * t + c) * CW];
+          if (tg >= 0) atomicAdd(Y + (size_t)tg * KP + row, acc[j][c]);
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
 // k_eval: one CTA per target item.  Targets are either the points of a box
 // (SURF_TGT = false; result stored to out[pbeg + i]) or the n surface points
 // c_B + rad * e_i of a box (SURF_TGT = true; result stored to out[row * ldo + i]).
@@ -125,16 +348,34 @@ struct EvalArgs {
   int ldo;
 };
 
-constexpr int EV_NT = 256;
-constexpr int EV_CH = 512;
-constexpr int EV_SEG = 128;
+constexpr int EV_NT = 256;    // threads for point targets
+constexpr int EV_MAXT = 320;  // max threads (surface targets: roundup(n, 32) <= 320)
+constexpr int EV_CH = 512;    // sources staged per chunk
+constexpr int EV_SEG = 128;   // segments per batch (= 32 lanes x 4)
 
 template <bool SURF_TGT>
-__global__ void __launch_bounds__(EV_NT) k_eval(EvalArgs A) {
+__device__ __forceinline__ void eval_target_pos(const EvalArgs& A, const double4& gb, int tbeg, int i, double& x0,
+                                                double& x1, double& x2) {
+  if (SURF_TGT) {
+    const double rad = gb.w * A.tgt_f;
+    x0 = gb.x + rad * A.surf[3 * i];
+    x1 = gb.y + rad * A.surf[3 * i + 1];
+    x2 = gb.z + rad * A.surf[3 * i + 2];
+  } else {
+    const double4 p = A.pts[tbeg + i];
+    x0 = p.x; x1 = p.y; x2 = p.z;
+  }
+}
+
+// Register-blocked: a pass handles up to 2*NT targets; thread (ti, gi) owns targets
+// t0+ti and t0+ti+mh (mh = ceil(mm/2)) and sweeps source slice gi (stride G).
+template <bool SURF_TGT>
+__global__ void __launch_bounds__(EV_MAXT) k_eval(EvalArgs A) {
   __shared__ double4 sbuf[EV_CH];
-  __shared__ double red[EV_NT];
+  __shared__ double red[2 * EV_MAXT];
   __shared__ int s_pref[EV_SEG + 1];
   __shared__ int4 s_seg[EV_SEG];
+  const int NT = blockDim.x;
   const int item = blockIdx.x;
   const int4 it = A.items[item];
   const int box = it.x;
@@ -143,43 +384,57 @@ __global__ void __launch_bounds__(EV_NT) k_eval(EvalArgs A) {
   if (SURF_TGT) m = A.n;
   else { tbeg = A.pbeg[box]; m = A.pend[box] - tbeg; }
   const int sb = A.seg_off[item], se = A.seg_off[item + 1];
-  for (int t0 = 0; t0 < m; t0 += EV_NT) {
-    const int mm = min(m - t0, EV_NT);
-    const int G = EV_NT / mm;
-    const int ti = threadIdx.x % mm, gi = threadIdx.x / mm;
+  const int lane = threadIdx.x & 31;
+  for (int t0 = 0; t0 < m; t0 += 2 * NT) {
+    const int mm = min(m - t0, 2 * NT);
+    const int mh = (mm + 1) >> 1;
+    const int G = NT / mh;
+    const int ti = threadIdx.x % mh, gi = threadIdx.x / mh;
     const bool act = gi < G;
-    double x0 = 0, x1 = 0, x2 = 0;
+    const bool has2 = ti + mh < mm;
+    double xa0 = 0, xa1 = 0, xa2 = 0, xb0 = 1e300, xb1 = 0, xb2 = 0;
     if (act) {
-      if (SURF_TGT) {
-        double rad = gb.w * A.tgt_f;
-        x0 = gb.x + rad * A.surf[3 * (t0 + ti)];
-        x1 = gb.y + rad * A.surf[3 * (t0 + ti) + 1];
-        x2 = gb.z + rad * A.surf[3 * (t0 + ti) + 2];
-      } else {
-        double4 p = A.pts[tbeg + t0 + ti];
-        x0 = p.x; x1 = p.y; x2 = p.z;
-      }
+      eval_target_pos<SURF_TGT>(A, gb, tbeg, t0 + ti, xa0, xa1, xa2);
+      if (has2) eval_target_pos<SURF_TGT>(A, gb, tbeg, t0 + ti + mh, xb0, xb1, xb2);
     }
-    double acc = 0.0;
+    double acca = 0.0, accb = 0.0;
     for (int s0 = sb; s0 < se; s0 += EV_SEG) {
       const int ns = min(EV_SEG, se - s0);
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int run = 0;
-        for (int s = 0; s < ns; ++s) {
-          int4 sg = A.segs[s0 + s];
-          s_seg[s] = sg;
-          s_pref[s] = run;
-          run += sg.w;
+      if (threadIdx.x < 32) {  // warp 0: segment table + exclusive prefix of lengths
+        int len[4], run = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int sidx = lane * 4 + u;
+          len[u] = 0;
+          if (sidx < ns) {
+            int4 sg = A.segs[s0 + sidx];
+            s_seg[sidx] = sg;
+            len[u] = sg.w;
+          }
+          run += len[u];
         }
-        s_pref[ns] = run;
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        int excl = incl - run;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int sidx = lane * 4 + u;
+          if (sidx < ns) s_pref[sidx] = excl;
+          excl += len[u];
+        }
+        if (lane == 31) s_pref[ns] = incl;
       }
       __syncthreads();
       const int total = s_pref[ns];
       for (int c0 = 0; c0 < total; c0 += EV_CH) {
         const int cn = min(EV_CH, total - c0);
         __syncthreads();
-        for (int f = threadIdx.x; f < cn; f += EV_NT) {
+        for (int f = threadIdx.x; f < cn; f += NT) {
           int fi = c0 + f;
           int lo = 0, hi = ns;  // last segment with prefix <= fi
           while (hi - lo > 1) {
@@ -201,25 +456,31 @@ __global__ void __launch_bounds__(EV_NT) k_eval(EvalArgs A) {
         }
         __syncthreads();
         if (act) {
-#pragma unroll 4
+#pragma unroll 2
           for (int j = gi; j < cn; j += G) {
-            const double4 s = sbuf[j];
-            const double dx = x0 - s.x, dy = x1 - s.y, dz = x2 - s.z;
-            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-            acc = fma(s.w, rinv_or_zero(r2), acc);
+            const double4 sv = sbuf[j];
+            const double ax = xa0 - sv.x, ay = xa1 - sv.y, az = xa2 - sv.z;
+            const double bx = xb0 - sv.x, by = xb1 - sv.y, bz = xb2 - sv.z;
+            const double ra = fma(az, az, fma(ay, ay, ax * ax));
+            const double rb = fma(bz, bz, fma(by, by, bx * bx));
+            acca = fma(sv.w, rinv_or_zero(ra), acca);
+            accb = fma(sv.w, rinv_or_zero(rb), accb);
           }
         }
       }
     }
     __syncthreads();
-    red[threadIdx.x] = acc;
+    red[threadIdx.x] = acca;
+    red[NT + threadIdx.x] = accb;
     __syncthreads();
-    if (threadIdx.x < mm) {
-      double s = 0;
-      for (int gg = 0; gg < G; ++gg) s += red[gg * mm + threadIdx.x];
-      s *= kInv4Pi;
-      if (SURF_TGT) A.out[(size_t)it.y * A.ldo + t0 + threadIdx.x] = s;
-      else A.out[tbeg + t0 + threadIdx.x] = s;
+    for (int i = threadIdx.x; i < mm; i += NT) {
+      const int half = i < mh ? 0 : 1;
+      const int tl = i - half * mh;
+      double sum = 0;
+      for (int gg = 0; gg < G; ++gg) sum += red[half * NT + gg * mh + tl];
+      sum *= kInv4Pi;
+      if (SURF_TGT) A.out[(size_t)it.y * A.ldo + t0 + i] = sum;
+      else A.out[tbeg + t0 + i] = sum;
     }
   }
 }
@@ -245,12 +506,35 @@ inline int nblk(int64_t n, int t = 256) { return std::max(1, (int)((n + t - 1) /
 
 int ggs_nt(int M, int K) { return (size_t)(K + 4 + M + 2) * 64 * 8 <= 116 * 1024 ? 64 : 32; }
 
+int g_num_sms = 148;
+
+constexpr int sq_nt(int kp) { return kp <= 64 ? 64 : 32; }
+size_t sq_smem(int kp) { return (size_t)sq_nt(kp) * 2 * (kp + 4) * sizeof(double); }
+
+template <int KP>
+int launch_sq(const GemmLaunch& g, const double* ops, int mvalid, const double* X, double* Y, bool atomic,
+              cudaStream_t st) {
+  constexpr int NT = sq_nt(KP);
+  const size_t smem = sq_smem(KP);
+  const int per_sm = std::max(1, (int)((220 * 1024) / (smem + 1024)));
+  const int grid = std::min(g.ntiles, g_num_sms * per_sm);
+  k_ggs_sq<KP, NT><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_pairs, ops, mvalid, X, Y, atomic);
+  return 0;
+}
+
 int g_launches = 0;
 
 int launch_ggs(const GemmLaunch& g, const double* ops, int op_stride, int M, int K, int mvalid, const double* X,
                int ldx, double* Y, int ldy, bool atomic, cudaStream_t st) {
   if (g.ntiles == 0) return 0;
   ++g_launches;
+  if (M == K && ldx == K && ldy == K && op_stride == K * K && (K == 32 || K == 64 || K == 104)) {
+    if (K == 32) launch_sq<32>(g, ops, mvalid, X, Y, atomic, st);
+    else if (K == 64) launch_sq<64>(g, ops, mvalid, X, Y, atomic, st);
+    else launch_sq<104>(g, ops, mvalid, X, Y, atomic, st);
+    KIFMM_CUDA(cudaGetLastError());
+    return 0;
+  }
   const int NT = ggs_nt(M, K);
   const size_t smem = (size_t)NT * (K + 4 + M + 2) * sizeof(double);
   if (NT == 64)
@@ -263,10 +547,44 @@ int launch_ggs(const GemmLaunch& g, const double* ops, int op_stride, int M, int
 
 }  // namespace
 
-int ggs_tile_width(int M, int K) { return ggs_nt(M, K); }
+template <int KP>
+int launch_sib(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
+  constexpr int NT = sq_nt(KP);
+  const size_t smem = (size_t)NT * 2 * (KP + 4) * sizeof(double);
+  const int per_sm = std::max(1, (int)((220 * 1024) / (smem + 6 * 1024)));
+  const int grid = std::min(g.ntiles, g_num_sms * per_sm);
+  k_m2l_sib<KP, NT><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y);
+  return 0;
+}
+
+int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, const double* X, double* Y, cudaStream_t st) {
+  if (g.ntiles == 0) return 0;
+  ++g_launches;
+  if (kp == 32) launch_sib<32>(g, C, mvalid, X, Y, st);
+  else if (kp == 64) launch_sib<64>(g, C, mvalid, X, Y, st);
+  else launch_sib<104>(g, C, mvalid, X, Y, st);
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int sib_tile_width(int kp) { return sq_nt(kp); }
+
+int ggs_tile_width(int M, int K) {
+  if (M == K && (K == 32 || K == 64 || K == 104)) return sq_nt(K);
+  return ggs_nt(M, K);
+}
 
 int kernels_init() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  KIFMM_CUDA(cudaFuncSetAttribute(k_ggs_sq<32, sq_nt(32)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_ggs_sq<64, sq_nt(64)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_ggs_sq<104, sq_nt(104)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
 }
@@ -280,6 +598,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
   const int64_t N = T.N;
   const int kp = P.kp, np = P.np, k = P.k, n = P.n;
   auto mark = [&](int i) { if (P.profile) cudaEventRecord(P.ev_phase[i], st); };
+  const int surf_threads = std::min(EV_MAXT, ((n + 1) / 2 + 31) / 32 * 32 * 2);
   g_launches = 0;
   mark(0);
   ++g_launches;
@@ -304,7 +623,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     EvalArgs a = ea;
     a.items = P.d_s2m_items; a.seg_off = P.d_s2m_off; a.segs = P.d_s2m_seg; a.tgt_f = 3.0 - 2.0 * P.d;
     a.out = P.d_chk_s2m; a.ldo = np;
-    k_eval<true><<<P.n_s2m, EV_NT, 0, st>>>(a);
+    k_eval<true><<<P.n_s2m, surf_threads, 0, st>>>(a);
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
@@ -315,7 +634,9 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
   for (auto& g : P.g_m2m)
     if (launch_ggs(g, P.d_M, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_qhat, kp, true, st)) return -3;
   mark(3);
-  // M2L, all levels in one launch: l^_B += C_delta q^'_A
+  // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
+  //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
+  if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, st)) return -3;
   if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, st)) return -3;
   mark(4);
   // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
@@ -323,7 +644,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     EvalArgs a = ea;
     a.items = P.d_x_items; a.seg_off = P.d_x_off; a.segs = P.d_x_seg; a.tgt_f = 1.0 + P.d;
     a.out = P.d_chk_x; a.ldo = np;
-    k_eval<true><<<P.n_xnd, EV_NT, 0, st>>>(a);
+    k_eval<true><<<P.n_xnd, surf_threads, 0, st>>>(a);
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
     if (launch_ggs(P.g_x, P.d_Ut, 0, kp, np, k, P.d_chk_x, np, P.d_lhat, kp, true, st)) return -3;

@@ -180,14 +180,111 @@ int build_schedules(Plan& P, cudaStream_t st) {
   if (make_launch(P, P.g_s2m, sgroup, w_kn, st) || make_launch(P, P.g_x, xgroup, w_kn, st) ||
       make_launch(P, P.g_l2t, lgroups, w_nk, st) || make_launch(P, P.g_w, wgroups, w_nk, st))
     return -3;
-  // M2L: V is in (offset, target) order -> one group per offset
+  // M2L.  Sibling groups (target B, source parent Q) at least sib_min_density full run
+  // in k_m2l_sib; the remaining pairs run offset-major in k_ggs_sq.
   {
-    std::vector<PairGroup> groups;
-    for (auto& v : V) {
-      if (groups.empty() || groups.back().op != v.z) groups.push_back(PairGroup{v.z, 1.0, {}});
-      groups.back().pairs.push_back(make_int2(v.y, v.x));
+    auto anchor = [&](int b, int out[3]) {
+      uint64_t k = T.key[b];
+      out[0] = out[1] = out[2] = 0;
+      for (int bit = 0; bit < 21; ++bit) {
+        out[0] |= (int)((k >> (3 * bit + 2)) & 1) << bit;
+        out[1] |= (int)((k >> (3 * bit + 1)) & 1) << bit;
+        out[2] |= (int)((k >> (3 * bit)) & 1) << bit;
+      }
+    };
+    // class table: class = didx * 8 + a; record = nvalid, b[8], offset id[8]
+    std::vector<int> classes(26 * 8 * 17, -1);
+    std::vector<int> nvalid(26 * 8, 0);
+    for (int lin = 0; lin < 27; ++lin) {
+      if (lin == 13) continue;
+      const int didx = lin < 13 ? lin : lin - 1;
+      const int dl[3] = {lin / 9 - 1, (lin / 3) % 3 - 1, lin % 3 - 1};
+      for (int a = 0; a < 8; ++a) {
+        const int av[3] = {(a >> 2) & 1, (a >> 1) & 1, a & 1};
+        int* rec = &classes[(didx * 8 + a) * 17];
+        int nv = 0;
+        for (int b = 0; b < 8; ++b) {
+          const int bv[3] = {(b >> 2) & 1, (b >> 1) & 1, b & 1};
+          int D[3], m = 0;
+          for (int d = 0; d < 3; ++d) { D[d] = 2 * dl[d] + bv[d] - av[d]; m = std::max(m, std::abs(D[d])); }
+          if (m <= 1) continue;
+          int id = 0;  // lexicographic index in [-3,3]^3 \ [-1,1]^3
+          for (int i = -3; i <= 3; ++i)
+            for (int j = -3; j <= 3; ++j)
+              for (int l = -3; l <= 3; ++l) {
+                if (std::max(std::abs(i), std::max(std::abs(j), std::abs(l))) <= 1) continue;
+                if (i == D[0] && j == D[1] && l == D[2]) { rec[1 + nv] = b; rec[9 + nv] = id; }
+                ++id;
+              }
+          ++nv;
+        }
+        rec[0] = nv;
+        nvalid[didx * 8 + a] = nv;
+      }
+    }
+    // V pairs -> CSR by target, then sibling groups per (target, Q)
+    std::vector<int> vcnt(nb + 1, 0);
+    for (auto& v : V) ++vcnt[v.x + 1];
+    for (int b = 0; b < nb; ++b) vcnt[b + 1] += vcnt[b];
+    std::vector<int4> vby(V.size());
+    {
+      std::vector<int> fill(vcnt.begin(), vcnt.end() - 1);
+      for (auto& v : V) vby[fill[v.x]++] = v;
+    }
+    std::vector<std::vector<int>> cls_cols(26 * 8);  // column records (9 ints) per class
+    std::vector<PairGroup> groups(kNumOffsets);
+    for (int o = 0; o < kNumOffsets; ++o) groups[o] = PairGroup{o, 1.0, {}};
+    int ap[3], aq[3];
+    for (int b = 0; b < nb; ++b) {
+      const int e0 = vcnt[b], e1 = vcnt[b + 1];
+      if (e0 == e1) continue;
+      anchor(T.parent[b], ap);
+      const int a = (int)(T.key[b] & 7);
+      // distinct source parents (<= 26)
+      int qs[27], nq = 0;
+      for (int e = e0; e < e1; ++e) {
+        int q = T.parent[vby[e].y];
+        bool seen = false;
+        for (int i = 0; i < nq; ++i) seen |= qs[i] == q;
+        if (!seen) qs[nq++] = q;
+      }
+      for (int i = 0; i < nq; ++i) {
+        anchor(qs[i], aq);
+        const int lin = (aq[0] - ap[0] + 1) * 9 + (aq[1] - ap[1] + 1) * 3 + (aq[2] - ap[2] + 1);
+        const int cls = (lin < 13 ? lin : lin - 1) * 8 + a;
+        int src[8] = {-1, -1, -1, -1, -1, -1, -1, -1}, cnt = 0;
+        for (int e = e0; e < e1; ++e)
+          if (T.parent[vby[e].y] == qs[i]) { src[T.key[vby[e].y] & 7] = vby[e].y; ++cnt; }
+        // cost model (per column, FP64 peak 37 TF/s, fp64 L2 RED 5.2e11/s): the sibling
+        // kernel spends nvalid GEMM columns + 1 RED row, offset-major cnt x (GEMM + RED row)
+        const double Gc = 2.0 * kp * kp / 37e12, Rr = kp / 5.2e11;
+        if (cnt * (Gc + Rr) >= nvalid[cls] * Gc + Rr) {
+          auto& cc = cls_cols[cls];
+          cc.push_back(b);
+          for (int j = 0; j < 8; ++j) cc.push_back(src[j]);
+        } else {
+          for (int e = e0; e < e1; ++e)
+            if (T.parent[vby[e].y] == qs[i]) groups[vby[e].z].pairs.push_back(make_int2(vby[e].y, b));
+        }
+      }
     }
     if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
+    // sibling tiles: per class, columns in target order, NT columns per tile
+    const int NTs = sib_tile_width(kp);
+    std::vector<int> cols;
+    std::vector<int4> tiles;
+    for (int cls = 0; cls < 26 * 8; ++cls) {
+      const auto& cc = cls_cols[cls];
+      const int ncol = (int)cc.size() / 9;
+      const int base = (int)cols.size() / 9;
+      cols.insert(cols.end(), cc.begin(), cc.end());
+      for (int c = 0; c < ncol; c += NTs) tiles.push_back(make_int4(cls, base + c, std::min(NTs, ncol - c), 0));
+    }
+    P.g_m2l_sib.ntiles = (int)tiles.size();
+    P.g_m2l_sib.ncols = (int)cols.size() / 9;
+    if (upload(P, &P.g_m2l_sib.d_tiles, tiles, st) || upload(P, &P.g_m2l_sib.d_cols, cols, st) ||
+        upload(P, &P.g_m2l_sib.d_classes, classes, st))
+      return -3;
   }
   // M2M per child level (finest first) and L2L per parent level (coarsest first), by octant
   P.g_m2m.clear();
