@@ -66,6 +66,8 @@ typedef struct {
   const fmm_tables_view* tables;  /* NULL: compute the tables (host precompute);
                                      else use these (e.g. the oracle's, for parity) */
   int profile;        /* 1: record per-phase CUDA events in fmm_matvec (fmm_info.phase_ms) */
+  int split_phases;   /* 1: evaluate the near field and the far field in separate passes so that
+                         fmm_export_phase can return both; 0 (default): one fused pass */
 } fmm_options;
 
 typedef struct {

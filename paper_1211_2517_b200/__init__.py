@@ -32,7 +32,7 @@ class TablesView(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("p", ctypes.c_int), ("k", ctypes.c_int), ("leaf_size", ctypes.c_int), ("d", ctypes.c_double),
                 ("pinv_rcond", ctypes.c_double), ("wx_direct_max", ctypes.c_int),
-                ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int)]
+                ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -125,7 +125,7 @@ class Plan:
 
     def __init__(self, points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, d: float = 0.1,
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
-                 stream=None):
+                 split_phases: bool = False, stream=None):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -134,7 +134,7 @@ class Plan:
         opt = Options()
         lib().fmm_default_options(ctypes.byref(opt))
         opt.p, opt.k, opt.leaf_size, opt.d, opt.pinv_rcond = p, k, leaf_size, d, rcond
-        opt.wx_direct_max, opt.profile = wx_direct_max, int(profile)
+        opt.wx_direct_max, opt.profile, opt.split_phases = wx_direct_max, int(profile), int(split_phases)
         self._keep = []
         if tables is not None:
             arrs = {x: np.ascontiguousarray(tables[x], dtype=np.float64) for x in "UCSTML"}

@@ -59,6 +59,7 @@ void fmm_default_options(fmm_options* o) {
   o->wx_direct_max = -1;
   o->tables = nullptr;
   o->profile = 0;
+  o->split_phases = 0;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -116,6 +117,7 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   P.d = opt->d;
   P.rcond = opt->pinv_rcond;
   P.profile = opt->profile != 0;
+  P.split_phases = opt->split_phases != 0;
   auto fail = [&](int rc) { free_plan_memory(h); delete h; return rc; };
   if (kifmm::kernels_init()) return fail(FMM_ECUDA);
   // ---- operator tables

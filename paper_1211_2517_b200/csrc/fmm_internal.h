@@ -113,6 +113,8 @@ struct Plan {
   int n_tleaf = 0; int4* d_tleaf_items = nullptr;
   int* d_near_off = nullptr; int4* d_near_seg = nullptr; int n_near_seg = 0;
   int* d_far_off = nullptr;  int4* d_far_seg = nullptr;  int n_far_seg = 0;
+  int* d_all_off = nullptr;  int4* d_all_seg = nullptr;  // near + far segments (fused pass)
+  bool split_phases = false;  // separate near / far passes (phase exports)
   int n_s2m = 0; int4* d_s2m_items = nullptr; int* d_s2m_off = nullptr; int4* d_s2m_seg = nullptr;
   int n_xnd = 0; int4* d_x_items = nullptr;   int* d_x_off = nullptr;   int4* d_x_seg = nullptr;
   int n_l2t = 0, n_wnd = 0;

@@ -485,6 +485,62 @@ __global__ void __launch_bounds__(EV_MAXT) k_eval(EvalArgs A) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// k_chk: check potentials of S2M (UC of a leaf at (3-2d) r, sources =
+// the leaf's points) and of the X list (DC of the target at (1+d) r, sources = the
+// X source leaf).  One warp per item, no block barriers: the warp stages 32 sources
+// at a time in shared memory and every lane accumulates CHK_TB check points.
+// ----------------------------------------------------------------------------
+constexpr int CHK_TB = 5;
+constexpr int CHK_WARPS = 8;
+
+__global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) {
+  __shared__ double4 ssrc[CHK_WARPS][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int item = blockIdx.x * CHK_WARPS + w;
+  if (item >= nitems) return;
+  const int4 it = A.items[item];
+  const double4 gb = A.geom[it.x];
+  const int4 sg = A.segs[A.seg_off[item]];  // one point segment per item
+  const double rad = gb.w * A.tgt_f;
+  const int n = A.n;
+  for (int r0 = 0; r0 < n; r0 += 32 * CHK_TB) {
+    double x[CHK_TB][3], acc[CHK_TB];
+#pragma unroll
+    for (int u = 0; u < CHK_TB; ++u) {
+      const int i = r0 + lane + 32 * u;
+      acc[u] = 0.0;
+      if (i < n) {
+        x[u][0] = gb.x + rad * A.surf[3 * i];
+        x[u][1] = gb.y + rad * A.surf[3 * i + 1];
+        x[u][2] = gb.z + rad * A.surf[3 * i + 2];
+      } else {
+        x[u][0] = gb.x; x[u][1] = gb.y; x[u][2] = gb.z;
+      }
+    }
+    for (int c0 = 0; c0 < sg.w; c0 += 32) {
+      const int cnt = min(32, sg.w - c0);
+      __syncwarp();
+      if (lane < cnt) ssrc[w][lane] = A.pts[sg.y + c0 + lane];
+      __syncwarp();
+      for (int j = 0; j < cnt; ++j) {
+        const double4 sv = ssrc[w][j];
+#pragma unroll
+        for (int u = 0; u < CHK_TB; ++u) {
+          const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          acc[u] = fma(sv.w, rinv_or_zero(r2), acc[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CHK_TB; ++u) {
+      const int i = r0 + lane + 32 * u;
+      if (i < n) A.out[(size_t)it.y * A.ldo + i] = acc[u] * kInv4Pi;
+    }
+  }
+}
+
 __global__ void k_set_density(double4* __restrict__ pts, const int32_t* __restrict__ perm, const double* __restrict__ q,
                               int64_t N) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -494,7 +550,7 @@ __global__ void k_set_density(double4* __restrict__ pts, const int32_t* __restri
 __global__ void k_gather_output(const double* __restrict__ pnear, const double* __restrict__ pfar,
                                 const int32_t* __restrict__ perm, int64_t N, double* __restrict__ pot) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < N) pot[perm[i]] = pnear[i] + pfar[i];
+  if (i < N) pot[perm[i]] = pfar ? pnear[i] + pfar[i] : pnear[i];
 }
 
 // ----------------------------------------------------------------------------
@@ -598,7 +654,6 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
   const int64_t N = T.N;
   const int kp = P.kp, np = P.np, k = P.k, n = P.n;
   auto mark = [&](int i) { if (P.profile) cudaEventRecord(P.ev_phase[i], st); };
-  const int surf_threads = std::min(EV_MAXT, ((n + 1) / 2 + 31) / 32 * 32 * 2);
   g_launches = 0;
   mark(0);
   ++g_launches;
@@ -606,11 +661,12 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
   KIFMM_CUDA(cudaGetLastError());
   KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
   KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
-  // near field (P2P: U + direct W/X), independent of the far field
   EvalArgs ea{};
   ea.pts = T.d_pts; ea.geom = T.d_geom; ea.pbeg = T.d_pbeg; ea.pend = T.d_pend;
   ea.surf = P.d_surf; ea.n = n; ea.f_in = 1.0 + P.d; ea.f_out = 3.0 - 2.0 * P.d; ea.ldq = np;
-  if (P.n_tleaf > 0) {
+  // near field (P2P: U + direct W/X).  split_phases: a separate pass (phase exports);
+  // otherwise fused with L2T/W into one evaluation pass at the end.
+  if (P.split_phases && P.n_tleaf > 0) {
     EvalArgs a = ea;
     a.items = P.d_tleaf_items; a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
     k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
@@ -623,7 +679,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     EvalArgs a = ea;
     a.items = P.d_s2m_items; a.seg_off = P.d_s2m_off; a.segs = P.d_s2m_seg; a.tgt_f = 3.0 - 2.0 * P.d;
     a.out = P.d_chk_s2m; a.ldo = np;
-    k_eval<true><<<P.n_s2m, surf_threads, 0, st>>>(a);
+    k_chk<<<(P.n_s2m + CHK_WARPS - 1) / CHK_WARPS, CHK_WARPS * 32, 0, st>>>(a, P.n_s2m);
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
@@ -644,7 +700,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     EvalArgs a = ea;
     a.items = P.d_x_items; a.seg_off = P.d_x_off; a.segs = P.d_x_seg; a.tgt_f = 1.0 + P.d;
     a.out = P.d_chk_x; a.ldo = np;
-    k_eval<true><<<P.n_xnd, surf_threads, 0, st>>>(a);
+    k_chk<<<(P.n_xnd + CHK_WARPS - 1) / CHK_WARPS, CHK_WARPS * 32, 0, st>>>(a, P.n_xnd);
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
     if (launch_ggs(P.g_x, P.d_Ut, 0, kp, np, k, P.d_chk_x, np, P.d_lhat, kp, true, st)) return -3;
@@ -657,17 +713,19 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
   // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
   if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
   if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
-  // L2T + W stage 2: potentials at the targets of each leaf
+  // L2T + W stage 2 (and, fused, the near field): potentials at the targets of each leaf
   if (P.n_tleaf > 0) {
     EvalArgs a = ea;
-    a.items = P.d_tleaf_items; a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far;
+    a.items = P.d_tleaf_items;
+    if (P.split_phases) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far; }
+    else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; a.out = P.d_pot_near; }
     a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
     k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
   mark(7);
-  k_gather_output<<<nblk(N), 256, 0, st>>>(P.d_pot_near, P.d_pot_far, T.d_perm, N, d_pot);
+  k_gather_output<<<nblk(N), 256, 0, st>>>(P.d_pot_near, P.split_phases ? P.d_pot_far : nullptr, T.d_perm, N, d_pot);
   ++g_launches;
   P.launches = g_launches;
   KIFMM_CUDA(cudaGetLastError());

@@ -141,20 +141,24 @@ int build_schedules(Plan& P, cudaStream_t st) {
     far[i].insert(far[i].begin(), make_int4(1, n_l2t, b, n));
     ++n_l2t;
   }
-  std::vector<int> near_off{0}, far_off{0};
-  std::vector<int4> near_seg, far_seg;
+  std::vector<int> near_off{0}, far_off{0}, all_off{0};
+  std::vector<int4> near_seg, far_seg, all_seg;
   for (int i = 0; i < nt; ++i) {
     near_seg.insert(near_seg.end(), near[i].begin(), near[i].end());
     near_off.push_back((int)near_seg.size());
     far_seg.insert(far_seg.end(), far[i].begin(), far[i].end());
     far_off.push_back((int)far_seg.size());
+    all_seg.insert(all_seg.end(), near[i].begin(), near[i].end());
+    all_seg.insert(all_seg.end(), far[i].begin(), far[i].end());
+    all_off.push_back((int)all_seg.size());
   }
   P.n_tleaf = nt;
   P.n_near_seg = (int)near_seg.size();
   P.n_far_seg = (int)far_seg.size();
   if (upload(P, &P.d_tleaf_items, titems, st) || upload(P, &P.d_near_off, near_off, st) ||
       upload(P, &P.d_near_seg, near_seg, st) || upload(P, &P.d_far_off, far_off, st) ||
-      upload(P, &P.d_far_seg, far_seg, st))
+      upload(P, &P.d_far_seg, far_seg, st) || upload(P, &P.d_all_off, all_off, st) ||
+      upload(P, &P.d_all_seg, all_seg, st))
     return -3;
   // ---- S2M: leaves at level >= 2
   std::vector<int4> sitems, ssegs;

@@ -88,7 +88,11 @@ def test_matvec_parity_shared_tables(case, wx):
     tb = tables(p, k)
     op = oracle.Plan(pts, s, tb["n"] if wx < 0 else wx)
     ref, ph = op.matvec(tb, q, phases=True)
-    gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb)
+    # fused production path
+    out = gpu_plan(pts, p, k, s, wx=wx, tb=tb).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel(out, ref) <= TOL
+    # split near / far passes (phase exports)
+    gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb, split_phases=True)
     out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
     assert rel(out, ref) <= TOL
     # per-phase parity localises failures.  q^' and l^ are intermediate: S' = U^T pinv(E_u)
