@@ -229,7 +229,7 @@ def run_ours(args):
         "config": {"workload": args.config, "N_per_gpu": N, "p": cfg["p"], "k": cfg["k"], "k_eff": k,
                    "leaf_size": cfg["leaf"], "kind": cfg["kind"], "parallelism": f"replicas{ws}",
                    "l2": "flushed (256 MiB write) between timed steps"},
-        "roofline": {"bound": "tensor", "kernel": "k_ggs (M2L, DMMA.8x8x4 FP64)", "achieved": achieved,
+        "roofline": {"bound": "tensor", "kernel": "M2L: k_m2l_sib + k_ggs_sq (DMMA.8x8x4 FP64)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "measured: tools/microbench/fp64_peaks.cu DMMA m8n8k4 loop on this pool's B200 "
                                     "(profiles/fp64_peaks_r01.json)",

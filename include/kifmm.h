@@ -80,7 +80,7 @@ typedef struct {
   int64_t launches;           /* kernels of this library launched by the last fmm_matvec */
   double r0, lo_root[3];
   double precompute_ms, tree_ms, lists_ms, schedule_ms;
-  float phase_ms[8];          /* last profiled matvec: P2P, S2M, M2M, M2L, X, L2L, L2T+W, output */
+  float phase_ms[8];          /* last profiled matvec: near (split only), S2M, M2M, M2L, X, L2L, eval (L2T+W[+near]), output */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

@@ -47,7 +47,9 @@ class Info(ctypes.Structure):
                 ("phase_ms", ctypes.c_float * 8)]
 
 
-PHASES = ("p2p", "s2m", "m2m", "m2l", "x", "l2l", "l2t_w", "output")
+# phases of fmm_matvec (profile=True); "near_split" is non-zero only with split_phases, otherwise the
+# near field is evaluated in the fused "eval" pass together with L2T and W
+PHASES = ("near_split", "s2m", "m2m", "m2l", "x", "l2l", "eval", "output")
 
 # every symbol declared in include/kifmm.h
 EXPORTS = ("fmm_default_options", "fmm_setup", "fmm_setup_ex", "fmm_matvec", "fmm_matvec_host", "fmm_free",

@@ -491,9 +491,9 @@ __global__ void __launch_bounds__(EV_MAXT) k_eval(EvalArgs A) {
 // X source leaf).  One warp per item, no block barriers: the warp stages 32 sources
 // at a time in shared memory and every lane accumulates CHK_TB check points.
 // ----------------------------------------------------------------------------
-constexpr int CHK_TB = 5;
 constexpr int CHK_WARPS = 8;
 
+template <int CHK_TB>
 __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) {
   __shared__ double4 ssrc[CHK_WARPS][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -572,8 +572,9 @@ int launch_sq(const GemmLaunch& g, const double* ops, int mvalid, const double* 
               cudaStream_t st) {
   constexpr int NT = sq_nt(KP);
   const size_t smem = sq_smem(KP);
-  const int per_sm = std::max(1, (int)((220 * 1024) / (smem + 1024)));
-  const int grid = std::min(g.ntiles, g_num_sms * per_sm);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ggs_sq<KP, NT>, KP * 4, smem);
+  const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
   k_ggs_sq<KP, NT><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_pairs, ops, mvalid, X, Y, atomic);
   return 0;
 }
@@ -607,8 +608,9 @@ template <int KP>
 int launch_sib(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
   constexpr int NT = sq_nt(KP);
   const size_t smem = (size_t)NT * 2 * (KP + 4) * sizeof(double);
-  const int per_sm = std::max(1, (int)((220 * 1024) / (smem + 6 * 1024)));
-  const int grid = std::min(g.ntiles, g_num_sms * per_sm);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_sib<KP, NT>, KP * 4, smem);
+  const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
   k_m2l_sib<KP, NT><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y);
   return 0;
 }
@@ -649,6 +651,19 @@ int kernels_init() {
 // Evaluation work lists live in the plan; see build_schedules (schedule.cpp).
 struct EvalLaunch;
 
+// check points per lane: one round of 32*TB when n <= 160, else rounds of 32*ceil(n/64)
+void launch_chk(const EvalArgs& a, int nitems, int n, cudaStream_t st) {
+  const int tb = n <= 160 ? (n + 31) / 32 : (n + 63) / 64;
+  const int grid = (nitems + CHK_WARPS - 1) / CHK_WARPS, thr = CHK_WARPS * 32;
+  switch (std::min(5, std::max(1, tb))) {
+    case 1: k_chk<1><<<grid, thr, 0, st>>>(a, nitems); break;
+    case 2: k_chk<2><<<grid, thr, 0, st>>>(a, nitems); break;
+    case 3: k_chk<3><<<grid, thr, 0, st>>>(a, nitems); break;
+    case 4: k_chk<4><<<grid, thr, 0, st>>>(a, nitems); break;
+    default: k_chk<5><<<grid, thr, 0, st>>>(a, nitems); break;
+  }
+}
+
 int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t st) {
   Tree& T = P.tree;
   const int64_t N = T.N;
@@ -679,7 +694,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     EvalArgs a = ea;
     a.items = P.d_s2m_items; a.seg_off = P.d_s2m_off; a.segs = P.d_s2m_seg; a.tgt_f = 3.0 - 2.0 * P.d;
     a.out = P.d_chk_s2m; a.ldo = np;
-    k_chk<<<(P.n_s2m + CHK_WARPS - 1) / CHK_WARPS, CHK_WARPS * 32, 0, st>>>(a, P.n_s2m);
+    launch_chk(a, P.n_s2m, n, st);
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
@@ -700,7 +715,7 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t 
     EvalArgs a = ea;
     a.items = P.d_x_items; a.seg_off = P.d_x_off; a.segs = P.d_x_seg; a.tgt_f = 1.0 + P.d;
     a.out = P.d_chk_x; a.ldo = np;
-    k_chk<<<(P.n_xnd + CHK_WARPS - 1) / CHK_WARPS, CHK_WARPS * 32, 0, st>>>(a, P.n_xnd);
+    launch_chk(a, P.n_xnd, n, st);
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
     if (launch_ggs(P.g_x, P.d_Ut, 0, kp, np, k, P.d_chk_x, np, P.d_lhat, kp, true, st)) return -3;
