@@ -7,9 +7,12 @@ Workload (N=1): BASELINE.json configs[1] = "C2": 1,048,576 points uniform in the
 unit cube (seed 0), densities U[-1,1], p = 6 (n = 152), k = 60 (k_eff 61), leaf
 128.  A step is one whole fmm_matvec (permute, S2M, M2M, M2L, X, L2L, L2T, W,
 P2P, unpermute) with the inputs resident in HBM; L2 is flushed (a 256 MiB write)
-between timed steps, outside the timed events.  Multi-GPU (torchrun): every rank
-runs its own replica of the workload (weak scaling, no collective; DESIGN.md
-"Multi-GPU").  `--impl reference` times the CPU oracle (oracle/) on the host.
+between timed steps, outside the timed events.  Multi-GPU (torchrun, N ranks):
+weak scaling, ONE problem of N x 2^20 points (same recipe) partitioned over the
+ranks by Morton ranges (OWNED mode: each rank's owned densities in, owned
+potentials out), ghost multipoles / densities exchanged over NCCL inside every
+step; `value` = all points / max-over-ranks step time.  `--impl reference` times
+the CPU oracle (oracle/) on the host.
 """
 from __future__ import annotations
 
@@ -144,22 +147,39 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pts, q, cfg = synth_inputs.make(args.config)
+    # N = 1: the BASELINE workload itself.  N > 1: weak scaling, one partitioned problem of
+    # N x (points of the workload), same recipe (every rank draws the same seeded cloud)
+    pts, q, cfg = synth_inputs.make(args.config, scale=ws)
     N = cfg["N"]
     stream = torch.cuda.current_stream()
     P = torch.from_numpy(pts).to(dev)
     Q = torch.from_numpy(q).to(dev)
+    nccl_id = None
+    if ws > 1:
+        box = [K.fmm_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        nccl_id = box[0]
     t0 = time.perf_counter()
-    plan = K.Plan(P, Q, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True)
+    plan = K.Plan(P, Q, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True, nranks=ws, rank=rank,
+                  nccl_id=nccl_id)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    out = torch.empty(N, dtype=torch.float64, device=dev)
+    lo, hi = plan.owned_range
+    if ws > 1:  # OWNED mode: densities / potentials of the owned points, sorted order
+        perm = plan.export_tree()["perm"]
+        Qin = torch.from_numpy(q[perm[lo:hi]].copy()).to(dev)
+        out = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+        step = lambda: plan.matvec_owned(Qin, out)
+    else:
+        Qin = Q
+        out = torch.empty(N, dtype=torch.float64, device=dev)
+        step = lambda: plan.matvec(Qin, out)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(max(3, args.warmup)):
-        plan.matvec(Q, out)
+        step()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    m2l_ms, phase_tot, launches = 0.0, {}, 0
+    phase_tot, launches = {}, 0
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -167,7 +187,7 @@ def run_ours(args):
         for i in range(args.steps):
             flush.fill_(i & 0xFF)  # L2 flush outside the timed events
             evs[i][0].record(stream)
-            plan.matvec(Q, out)
+            step()
             evs[i][1].record(stream)
             inf = plan.get_info()  # waits for this step's phase events
             for kname, v in inf["phase_ms"].items():
@@ -185,35 +205,47 @@ def run_ours(args):
     phase = {k: v / args.steps for k, v in phase_tot.items()}
     info = plan.get_info()
     # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside the timing
-    hq = torch.from_numpy(q).pin_memory()
-    hp = torch.empty(N, dtype=torch.float64).pin_memory()
-    hq_np, hp_np = hq.numpy(), hp.numpy()
+    if ws > 1:
+        hq = torch.from_numpy(q[perm[lo:hi]].copy()).pin_memory()
+        hp = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+        e2e_call = lambda: plan.matvec_owned_host(hq.numpy(), hp.numpy())
+        e2e_bytes = 8 * (hi - lo)
+        e2e_api = "fmm_matvec_owned_host (pinned host buffers, owned points)"
+    else:
+        hq = torch.from_numpy(q).pin_memory()
+        hp = torch.empty(N, dtype=torch.float64).pin_memory()
+        e2e_call = lambda: plan.matvec_host(hq.numpy(), hp.numpy())
+        e2e_bytes = 8 * N
+        e2e_api = "fmm_matvec_host (pinned host buffers)"
     for _ in range(3):
-        plan.matvec_host(hq_np, hp_np)
+        e2e_call()
     if ws > 1:
         dist.barrier()
     e2e_steps = max(5, args.steps // 2)
     te = time.perf_counter()
     for _ in range(e2e_steps):
-        plan.matvec_host(hq_np, hp_np)
+        e2e_call()
     e2e_s = (time.perf_counter() - te) / e2e_steps
     if ws > 1:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+        tl = torch.tensor([launches], device=dev, dtype=torch.float64)
+        dist.all_reduce(tl)
+        launches = int(tl.item())
     if rank != 0:
         dist.destroy_process_group()
         return
     # ---- roofline of the dominant kernel (M2L, DMMA) from the live per-phase events
     k = info["k"]
-    m2l_flops = 2.0 * k * k * info["nV"]
+    m2l_flops = 2.0 * k * k * info["nV_local"]
     m2l_s = phase["m2l"] * 1e-3
     peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")))
     peak = float(peaks["dmma_m8n8k4_tflops"])
     achieved = m2l_flops / m2l_s / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "m2l_dram_bytes.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and ws == 1:
         traffic = json.load(open(tf)).get("bytes_per_launch")
     # ---- cpu baseline: the oracle on the host cores, one full matvec (rank 0, N = 1 only)
     cpu = None
@@ -221,14 +253,18 @@ def run_ours(args):
         ts = oracle_matvec_timer(pts, q, cfg, reps=1)
         cpu = {"value": N / ts[0], "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"one full {args.config} matvec (N={N}), oracle/ C++ -O2 OpenMP, {ts[0]:.2f} s"}
-    value = N * ws / (ms * 1e-3)
+    value = N / (ms * 1e-3)
+    config = {"workload": args.config if ws == 1 else f"{args.config} x{ws} (weak)", "N": N,
+              "N_per_gpu": N // ws, "p": cfg["p"], "k": cfg["k"], "k_eff": k, "leaf_size": cfg["leaf"],
+              "kind": cfg["kind"], "parallelism": "single" if ws == 1 else f"morton-partition{ws} (NCCL ghosts)",
+              "l2": "flushed (256 MiB write) between timed steps"}
+    if ws > 1:
+        config.update(mode="owned", ghost_q_rows_rank0=info["ghost_q_recv"], ghost_dens_rank0=info["ghost_d_recv"],
+                      straddling_boxes=info["n_straddle"])
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "N_per_gpu": N, "p": cfg["p"], "k": cfg["k"], "k_eff": k,
-                   "leaf_size": cfg["leaf"], "kind": cfg["kind"], "parallelism": f"replicas{ws}",
-                   "l2": "flushed (256 MiB write) between timed steps"},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "roofline": {"bound": "tensor", "kernel": "M2L: k_m2l_sib + k_ggs_sq (DMMA.8x8x4 FP64)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "measured: tools/microbench/fp64_peaks.cu DMMA m8n8k4 loop on this pool's B200 "
@@ -236,8 +272,8 @@ def run_ours(args):
                      "flops_per_launch": m2l_flops, "ms_per_launch": phase["m2l"]},
         "phase_ms": phase,
         "clocks": clk.summary(),
-        "e2e": {"value": N * ws / e2e_s, "unit": "points/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
-                "ms_per_step": e2e_s * 1e3, "api": "fmm_matvec_host (pinned host buffers)"},
+        "e2e": {"value": N / e2e_s, "unit": "points/s", "h2d_bytes_per_step": e2e_bytes,
+                "d2h_bytes_per_step": e2e_bytes, "ms_per_step": e2e_s * 1e3, "api": e2e_api},
         "gpu_launches": launches,
         "setup_s": setup_s,
         "precompute_ms": info["precompute_ms"],

@@ -9,7 +9,8 @@
  *     p_i = sum_{j : x_j != x_i} G(x_i, x_j) q_j            (eq_eval)
  *
  * by the kernel-independent FMM whose translation operators are
- * compressed with the M2L SVD basis, on one B200.
+ * compressed with the M2L SVD basis, on one B200 or
+ * partitioned over several (one process per GPU, NCCL over NVLink).
  *
  * Conventions for every entry point:
  *   - Device pointers are CUDA device memory of the plan's device; host pointers
@@ -34,6 +35,7 @@ extern "C" {
 #define FMM_ECONFIG (-2)  /* inconsistent operator tables (p, n, k or d do not match the plan) */
 #define FMM_ECUDA (-3)    /* a CUDA runtime call or kernel launch failed */
 #define FMM_ENOMEM (-4)   /* host allocation failed */
+#define FMM_ENCCL (-5)    /* NCCL unavailable or an NCCL call failed (multi-GPU plans) */
 
 typedef struct fmm_plan fmm_plan;
 typedef struct fmm_tables fmm_tables;
@@ -67,7 +69,20 @@ typedef struct {
                                      else use these (e.g. the oracle's, for parity) */
   int profile;        /* 1: record per-phase CUDA events in fmm_matvec (fmm_info.phase_ms) */
   int split_phases;   /* 1: evaluate the near field and the far field in separate passes so that
-                         fmm_export_phase can return both; 0 (default): one fused pass */
+                         fmm_export_phase can return both; 0 (default): one fused pass.
+                         Single-GPU plans only. */
+  /* Multi-GPU.  nranks > 1 partitions the matvec: every rank passes
+     the SAME N points (replicated setup), rank r owns a contiguous Morton range of
+     leaves (fmm_owned_range) chosen by a prefix sum of estimated work, and ghost
+     multipoles / ghost densities are exchanged inside every matvec.
+       nccl_id != NULL: a 128-byte ncclUniqueId shared by all ranks (fmm_nccl_unique_id
+                        on one rank, broadcast by the caller); one process per GPU,
+                        fmm_setup_ex is collective.
+       nccl_id == NULL: a loopback rank: all nranks plans live in one process (any
+                        devices) and run together through fmm_matvec_group (tests). */
+  int nranks;         /* default 1 */
+  int rank;           /* 0 <= rank < nranks */
+  const void* nccl_id;
 } fmm_options;
 
 typedef struct {
@@ -80,7 +95,14 @@ typedef struct {
   int64_t launches;           /* kernels of this library launched by the last fmm_matvec */
   double r0, lo_root[3];
   double precompute_ms, tree_ms, lists_ms, schedule_ms;
-  float phase_ms[8];          /* last profiled matvec: near (split only), S2M, M2M, M2L, X, L2L, eval (L2T+W[+near]), output */
+  float phase_ms[9];          /* last profiled matvec (ms): density, S2M, M2M, exchange (straddlers + ghost
+                                 multipoles), M2L, X, L2L, eval (L2T + W + near field), output */
+  int nranks, rank;
+  int64_t own_lo, own_hi;     /* owned sorted points */
+  int64_t n_straddle;         /* boxes whose multipole is allreduced */
+  int64_t ghost_q_recv, ghost_q_send;  /* ghost multipole rows per matvec */
+  int64_t ghost_d_recv, ghost_d_send;  /* ghost densities per matvec (owned mode) */
+  int64_t nV_local;           /* V pairs this rank's M2L applies (= nV on one rank) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */
@@ -105,6 +127,53 @@ int fmm_matvec(fmm_plan* plan, const double* density, double* potential, void* s
 /* Same with HOST buffers: copies density in, runs fmm_matvec, copies the
  * potential out, all on `stream`; returns after the stream has synchronised. */
 int fmm_matvec_host(fmm_plan* plan, const double* h_density, double* h_potential, void* stream);
+
+/* Partitioned matvec in OWNED mode (nranks > 1; also valid on one rank, where the
+ * owned range is everything):
+ *   density_owned    device [own_hi - own_lo], densities of the owned points in
+ *                    sorted (Morton) order: density_owned[i] = q[perm[own_lo + i]]
+ *                    (perm from fmm_export_tree)
+ *   potential_owned  device [own_hi - own_lo], same order; overwritten
+ * Ghost densities and multipoles are exchanged over NCCL on `stream`.  fmm_matvec
+ * on a multi-GPU plan is the REPLICATED mode: full caller-order density in, full
+ * caller-order potential out on every rank (the owned ranges are allgathered). */
+int fmm_matvec_owned(fmm_plan* plan, const double* density_owned, double* potential_owned, void* stream);
+
+/* Same with HOST buffers (copies inside; returns after the stream synchronised). */
+int fmm_matvec_owned_host(fmm_plan* plan, const double* h_density_owned, double* h_potential_owned, void* stream);
+
+/* Owned sorted-point range [*begin, *end) of the plan's rank. */
+int fmm_owned_range(const fmm_plan* plan, int64_t* begin, int64_t* end);
+
+/* 128-byte NCCL unique id for fmm_options.nccl_id. */
+int fmm_nccl_unique_id(void* id128);
+
+/* Loopback group: one matvec of the nplans plans of one partition (plans[r] built
+ * with nranks = nplans, rank = r, nccl_id = NULL), run stage by stage with the
+ * ghost exchanges done as device copies between the plans, all on `stream`.
+ *   owned = 1: densities[r] / potentials[r] as in fmm_matvec_owned for rank r
+ *   owned = 0: densities[r] / potentials[r] as in fmm_matvec (full, caller order)
+ * The exchanges are the same buffers and lists the NCCL transport sends. */
+int fmm_matvec_group(fmm_plan* const* plans, int nplans, const double* const* densities, double* const* potentials,
+                     int owned, void* stream);
+
+/* Host-only partition (no GPU): the partition rank `rank` of `nranks` derives from a
+ * tree and its lists in the fmm_export_tree / fmm_export_lists formats
+ * (U: nU x 2, V, W, X: n x 3 int32).  n = surface points, k = rank (work model). */
+typedef struct fmm_partition fmm_partition;
+int fmm_partition_host(int nboxes, const int32_t* level, const int32_t* parent, const int32_t* pbeg,
+                       const int32_t* pend, const uint8_t* leaf, int64_t nU, const int32_t* U, int64_t nV,
+                       const int32_t* V, int64_t nW, const int32_t* W, int64_t nX, const int32_t* X, int n, int k,
+                       int nranks, int rank, fmm_partition** out);
+/* Arrays of a partition (owned by it), what =
+ *   0 bnd[nranks+1] (sorted-point boundaries)   1 inD[nboxes] (0/1: point range meets the owned range)
+ *   2 straddling boxes                           3 full[nboxes] (0/1: point range inside the owned range)
+ *   4 q send boxes, 5 q send offsets[nranks+1]   6 q recv boxes, 7 q recv offsets
+ *   8 density send points, 9 offsets             10 density recv points, 11 offsets  */
+int fmm_partition_get(const fmm_partition* part, int what, int64_t* count, const int32_t** data);
+void fmm_partition_free(fmm_partition* part);
+/* The partition of a plan (owned by the plan; valid until fmm_free). */
+const fmm_partition* fmm_plan_partition(const fmm_plan* plan);
 
 /* Release every resource of the plan.  NULL is a no-op. */
 void fmm_free(fmm_plan* plan);

@@ -16,7 +16,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libkifmm_b200.so")
 
-FMM_OK, FMM_EINVAL, FMM_ECONFIG, FMM_ECUDA, FMM_ENOMEM = 0, -1, -2, -3, -4
+FMM_OK, FMM_EINVAL, FMM_ECONFIG, FMM_ECUDA, FMM_ENOMEM, FMM_ENCCL = 0, -1, -2, -3, -4, -5
 
 
 class FmmError(RuntimeError):
@@ -32,7 +32,8 @@ class TablesView(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("p", ctypes.c_int), ("k", ctypes.c_int), ("leaf_size", ctypes.c_int), ("d", ctypes.c_double),
                 ("pinv_rcond", ctypes.c_double), ("wx_direct_max", ctypes.c_int),
-                ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int)]
+                ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int),
+                ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p)]
 
 
 class Info(ctypes.Structure):
@@ -44,17 +45,26 @@ class Info(ctypes.Structure):
                 ("launches", ctypes.c_int64),
                 ("r0", ctypes.c_double), ("lo_root", ctypes.c_double * 3), ("precompute_ms", ctypes.c_double),
                 ("tree_ms", ctypes.c_double), ("lists_ms", ctypes.c_double), ("schedule_ms", ctypes.c_double),
-                ("phase_ms", ctypes.c_float * 8)]
+                ("phase_ms", ctypes.c_float * 9), ("nranks", ctypes.c_int), ("rank", ctypes.c_int),
+                ("own_lo", ctypes.c_int64), ("own_hi", ctypes.c_int64), ("n_straddle", ctypes.c_int64),
+                ("ghost_q_recv", ctypes.c_int64), ("ghost_q_send", ctypes.c_int64),
+                ("ghost_d_recv", ctypes.c_int64), ("ghost_d_send", ctypes.c_int64), ("nV_local", ctypes.c_int64)]
 
 
-# phases of fmm_matvec (profile=True); "near_split" is non-zero only with split_phases, otherwise the
-# near field is evaluated in the fused "eval" pass together with L2T and W
-PHASES = ("near_split", "s2m", "m2m", "m2l", "x", "l2l", "eval", "output")
+# phases of fmm_matvec (profile=True): the near field is evaluated in the "eval" pass together with
+# L2T and W; "exchange" holds the multi-GPU straddler allreduce and ghost-multipole exchange
+PHASES = ("density", "s2m", "m2m", "exchange", "m2l", "x", "l2l", "eval", "output")
+
+# fmm_partition_get arrays
+PART_ARRAYS = ("bnd", "inD", "straddle", "full", "q_send", "q_send_off", "q_recv", "q_recv_off",
+               "d_send", "d_send_off", "d_recv", "d_recv_off")
 
 # every symbol declared in include/kifmm.h
 EXPORTS = ("fmm_default_options", "fmm_setup", "fmm_setup_ex", "fmm_matvec", "fmm_matvec_host", "fmm_free",
            "fmm_info", "fmm_export_tree", "fmm_export_lists", "fmm_export_phase", "fmm_tables_build",
-           "fmm_tables_view_get", "fmm_tables_free", "fmm_last_error")
+           "fmm_tables_view_get", "fmm_tables_free", "fmm_last_error", "fmm_matvec_owned", "fmm_matvec_owned_host",
+           "fmm_owned_range", "fmm_nccl_unique_id", "fmm_matvec_group", "fmm_partition_host", "fmm_partition_get",
+           "fmm_partition_free", "fmm_plan_partition")
 
 _lib = None
 
@@ -85,6 +95,18 @@ def lib():
         L.fmm_tables_free.restype = None
         L.fmm_last_error.argtypes = []
         L.fmm_last_error.restype = ctypes.c_char_p
+        L.fmm_matvec_owned.argtypes = [vp, vp, vp, vp]
+        L.fmm_matvec_owned_host.argtypes = [vp, vp, vp, vp]
+        L.fmm_owned_range.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.fmm_nccl_unique_id.argtypes = [vp]
+        L.fmm_matvec_group.argtypes = [ctypes.POINTER(vp), ci, ctypes.POINTER(vp), ctypes.POINTER(vp), ci, vp]
+        L.fmm_partition_host.argtypes = [ci, vp, vp, vp, vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, ci, ci, ci, ci,
+                                         ctypes.POINTER(vp)]
+        L.fmm_partition_get.argtypes = [vp, ci, ctypes.POINTER(i64), ctypes.POINTER(ctypes.POINTER(ctypes.c_int32))]
+        L.fmm_partition_free.argtypes = [vp]
+        L.fmm_partition_free.restype = None
+        L.fmm_plan_partition.argtypes = [vp]
+        L.fmm_plan_partition.restype = vp
         _lib = L
     return _lib
 
@@ -122,12 +144,53 @@ def fmm_tables_build(p: int, k: int, d: float = 0.1, rcond: float = 1e-10) -> di
         lib().fmm_tables_free(h)
 
 
+def _partition_dict(handle) -> dict:
+    out = {}
+    for i, name in enumerate(PART_ARRAYS):
+        cnt = ctypes.c_int64()
+        ptr = ctypes.POINTER(ctypes.c_int32)()
+        _check(lib().fmm_partition_get(handle, i, ctypes.byref(cnt), ctypes.byref(ptr)), "fmm_partition_get")
+        out[name] = (np.ctypeslib.as_array(ptr, shape=(cnt.value,)).copy() if cnt.value
+                     else np.zeros(0, np.int32))
+    return out
+
+
+def fmm_partition_host(tree: dict, lists: dict, n: int, k: int, nranks: int, rank: int) -> dict:
+    """Host-only partition (no GPU) of a tree / lists in the export formats."""
+    c = lambda a, t: np.ascontiguousarray(a, dtype=t)
+    lv, par, pb, pe = (c(tree[x], np.int32) for x in ("level", "parent", "pbeg", "pend"))
+    lf = c(tree["leaf"], np.uint8)
+    L = {x: c(lists[x], np.int32) for x in "UVWX"}
+    h = ctypes.c_void_p()
+    _check(lib().fmm_partition_host(len(lv), lv.ctypes.data, par.ctypes.data, pb.ctypes.data, pe.ctypes.data,
+                                     lf.ctypes.data, len(L["U"]), L["U"].ctypes.data, len(L["V"]), L["V"].ctypes.data,
+                                     len(L["W"]), L["W"].ctypes.data, len(L["X"]), L["X"].ctypes.data, n, k, nranks,
+                                     rank, ctypes.byref(h)), "fmm_partition_host")
+    try:
+        return _partition_dict(h)
+    finally:
+        lib().fmm_partition_free(h)
+
+
+def fmm_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().fmm_nccl_unique_id(buf), "fmm_nccl_unique_id")
+    return buf.raw
+
+
 class Plan:
-    """An immutable FMM plan (tree, lists, operator tables) on the current device."""
+    """An immutable FMM plan (tree, lists, operator tables) on the current device.
+
+    Multi-GPU: nranks > 1 partitions the matvec (every rank passes the same points);
+    nccl_id (128 bytes, fmm_nccl_unique_id() on one rank, broadcast by the caller)
+    connects the ranks over NCCL; without it the plan is a loopback rank that runs
+    through matvec_group() together with the other ranks' plans in this process.
+    """
 
     def __init__(self, points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, d: float = 0.1,
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
-                 split_phases: bool = False, stream=None):
+                 split_phases: bool = False, stream=None, nranks: int = 1, rank: int = 0,
+                 nccl_id: bytes | None = None):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -137,7 +200,12 @@ class Plan:
         lib().fmm_default_options(ctypes.byref(opt))
         opt.p, opt.k, opt.leaf_size, opt.d, opt.pinv_rcond = p, k, leaf_size, d, rcond
         opt.wx_direct_max, opt.profile, opt.split_phases = wx_direct_max, int(profile), int(split_phases)
+        opt.nranks, opt.rank = nranks, rank
         self._keep = []
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            self._keep.append(idbuf)
+            opt.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
         if tables is not None:
             arrs = {x: np.ascontiguousarray(tables[x], dtype=np.float64) for x in "UCSTML"}
             self._keep.append(arrs)
@@ -190,6 +258,39 @@ class Plan:
                "fmm_matvec_host")
         return out
 
+    @property
+    def owned_range(self) -> tuple[int, int]:
+        b, e = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().fmm_owned_range(self._h, ctypes.byref(b), ctypes.byref(e)), "fmm_owned_range")
+        return b.value, e.value
+
+    def matvec_owned(self, density_owned, out=None, stream=None):
+        """OWNED mode: densities / potentials of the owned points in sorted (Morton) order."""
+        import torch
+        lo, hi = self.owned_range
+        if out is None:
+            out = torch.empty(hi - lo, dtype=torch.float64, device=self.points.device)
+        if not (density_owned.is_cuda and density_owned.dtype == torch.float64 and density_owned.is_contiguous()
+                and density_owned.numel() == hi - lo):
+            raise TypeError("density_owned must be a contiguous CUDA float64 tensor of the owned length")
+        _check(lib().fmm_matvec_owned(self._h, ctypes.c_void_p(density_owned.data_ptr()),
+                                      ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)), "fmm_matvec_owned")
+        return out
+
+    def matvec_owned_host(self, density_owned: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
+        lo, hi = self.owned_range
+        density_owned = np.ascontiguousarray(density_owned, dtype=np.float64)
+        if density_owned.shape != (hi - lo,):
+            raise ValueError("density_owned must have the owned length")
+        if out is None:
+            out = np.empty(hi - lo, dtype=np.float64)
+        _check(lib().fmm_matvec_owned_host(self._h, density_owned.ctypes.data, out.ctypes.data, _stream_ptr(stream)),
+               "fmm_matvec_owned_host")
+        return out
+
+    def partition(self) -> dict:
+        return _partition_dict(lib().fmm_plan_partition(self._h))
+
     def export_tree(self) -> dict:
         nb = self.info["nboxes"]
         t = dict(level=np.zeros(nb, np.int32), key=np.zeros(nb, np.uint64), parent=np.zeros(nb, np.int32),
@@ -232,3 +333,21 @@ def fmm_matvec_host(plan: Plan, density: np.ndarray, potential: np.ndarray | Non
 
 def fmm_free(plan: Plan) -> None:
     plan.free()
+
+
+def fmm_matvec_group(plans: list, densities: list, potentials: list | None = None, owned: bool = False, stream=None):
+    """One matvec of a loopback group (plans[r] = rank r of len(plans)), stage by stage
+    with the ghost exchanges as device copies between the plans."""
+    import torch
+    n = len(plans)
+    if potentials is None:
+        potentials = []
+        for pl in plans:
+            lo, hi = pl.owned_range
+            potentials.append(torch.empty(hi - lo if owned else pl.N, dtype=torch.float64, device=pl.points.device))
+    vp = ctypes.c_void_p
+    hs = (vp * n)(*[pl._h.value for pl in plans])
+    ds = (vp * n)(*[d.data_ptr() if d is not None and d.numel() else None for d in densities])
+    ps = (vp * n)(*[p_.data_ptr() if p_.numel() else None for p_ in potentials])
+    _check(lib().fmm_matvec_group(hs, n, ds, ps, int(owned), _stream_ptr(stream)), "fmm_matvec_group")
+    return potentials

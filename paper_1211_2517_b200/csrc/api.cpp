@@ -5,11 +5,24 @@
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "fmm_internal.h"
 
+struct fmm_partition {
+  kifmm::DistPlan own;                 // host-built partitions
+  const kifmm::DistPlan* D = nullptr;  // -> own, or a plan's partition
+  std::vector<int32_t> inD32, full32;
+  void view(const kifmm::DistPlan* d) {
+    D = d;
+    inD32.assign(d->inD.begin(), d->inD.end());
+    full32.assign(d->full.begin(), d->full.end());
+  }
+};
+
 struct fmm_plan {
   kifmm::Plan P;
+  fmm_partition part;
   double* d_default_density = nullptr;
   double precompute_ms = 0, tree_ms = 0, lists_ms = 0, schedule_ms = 0;
 };
@@ -43,7 +56,10 @@ void free_plan_memory(fmm_plan* h) {
     if (p) cudaFree(p);
   for (auto e : P.ev_phase) cudaEventDestroy(e);
   P.ev_phase.clear();
+  kifmm::nccl_comm_destroy(P);
 }
+
+constexpr int kPhases = 9;
 
 }  // namespace
 
@@ -60,6 +76,9 @@ void fmm_default_options(fmm_options* o) {
   o->tables = nullptr;
   o->profile = 0;
   o->split_phases = 0;
+  o->nranks = 1;
+  o->rank = 0;
+  o->nccl_id = nullptr;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -105,6 +124,10 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     set_error("fmm_setup: invalid argument (points, N in [1, 2^31), p >= 2, k >= 1, leaf_size >= 1, 0 <= d < 2/3)");
     return FMM_EINVAL;
   }
+  if (opt->nranks < 1 || opt->rank < 0 || opt->rank >= opt->nranks || (opt->nranks > 1 && opt->split_phases)) {
+    set_error("fmm_setup: invalid nranks / rank (0 <= rank < nranks; split_phases needs nranks == 1)");
+    return FMM_EINVAL;
+  }
   const int n_expect = 6 * (opt->p - 1) * (opt->p - 1) + 2;
   if (opt->p * 1 > 0 && n_expect > 296) { set_error("fmm_setup: p > 8 is not supported (n <= 296)"); return FMM_EINVAL; }
   fmm_plan* h = new (std::nothrow) fmm_plan();
@@ -118,6 +141,8 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   P.rcond = opt->pinv_rcond;
   P.profile = opt->profile != 0;
   P.split_phases = opt->split_phases != 0;
+  P.dist.nranks = opt->nranks;
+  P.dist.rank = opt->rank;
   auto fail = [&](int rc) { free_plan_memory(h); delete h; return rc; };
   if (kifmm::kernels_init()) return fail(FMM_ECUDA);
   // ---- operator tables
@@ -172,6 +197,11 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   t0 = std::chrono::steady_clock::now();
   if (kifmm::build_schedules(P, st)) return fail(FMM_ECUDA);
   h->schedule_ms = ms_since(t0);
+  h->part.view(&P.dist);
+  if (opt->nccl_id) {  // (a one-rank communicator is allowed: it exercises the transport setup)
+    if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("fmm_setup: CUDA error before NCCL init"); return fail(FMM_ECUDA); }
+    if (kifmm::nccl_comm_init(P, opt->nccl_id)) return fail(FMM_ENCCL);
+  }
   if (densities) {
     if (cudaMalloc(&h->d_default_density, sizeof(double) * N) != cudaSuccess ||
         cudaMemcpyAsync(h->d_default_density, densities, sizeof(double) * N, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
@@ -179,7 +209,7 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
       return fail(FMM_ECUDA);
     }
   }
-  P.ev_phase.resize(9);
+  P.ev_phase.resize(kPhases + 1);
   for (auto& e : P.ev_phase) cudaEventCreate(&e);
   if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
     set_error("fmm_setup: CUDA error during setup");
@@ -193,9 +223,200 @@ int fmm_matvec(fmm_plan* h, const double* density, double* potential, void* stre
   if (!h || !potential) { set_error("fmm_matvec: null plan or potential"); return FMM_EINVAL; }
   const double* q = density ? density : h->d_default_density;
   if (!q) { set_error("fmm_matvec: no density given and none at setup"); return FMM_EINVAL; }
-  int rc = kifmm::matvec_device(h->P, q, potential, (cudaStream_t)stream);
-  return rc ? FMM_ECUDA : FMM_OK;
+  if (h->P.dist.nranks > 1 && !h->P.nccl_comm) { set_error("fmm_matvec: loopback plan, use fmm_matvec_group"); return FMM_EINVAL; }
+  int rc = kifmm::matvec_device(h->P, q, potential, false, (cudaStream_t)stream);
+  return rc == 0 ? FMM_OK : rc == -5 ? FMM_ENCCL : FMM_ECUDA;
 }
+
+int fmm_matvec_owned(fmm_plan* h, const double* density_owned, double* potential_owned, void* stream) {
+  if (!h) { set_error("fmm_matvec_owned: null plan"); return FMM_EINVAL; }
+  const kifmm::DistPlan& D = h->P.dist;
+  if (D.own_hi > D.own_lo && (!density_owned || !potential_owned)) {
+    set_error("fmm_matvec_owned: null density or potential");
+    return FMM_EINVAL;
+  }
+  if (D.nranks > 1 && !h->P.nccl_comm) { set_error("fmm_matvec_owned: loopback plan, use fmm_matvec_group"); return FMM_EINVAL; }
+  int rc = kifmm::matvec_device(h->P, density_owned, potential_owned, true, (cudaStream_t)stream);
+  return rc == 0 ? FMM_OK : rc == -5 ? FMM_ENCCL : FMM_ECUDA;
+}
+
+int fmm_matvec_owned_host(fmm_plan* h, const double* h_density, double* h_potential, void* stream) {
+  if (!h) { set_error("fmm_matvec_owned_host: null plan"); return FMM_EINVAL; }
+  kifmm::Plan& P = h->P;
+  const int64_t cnt = P.dist.own_hi - P.dist.own_lo;
+  if (cnt > 0 && (!h_density || !h_potential)) { set_error("fmm_matvec_owned_host: null argument"); return FMM_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* d_q = P.d_io;
+  double* d_p = P.d_io + P.tree.N;
+  if (cnt > 0 && cudaMemcpyAsync(d_q, h_density, sizeof(double) * cnt, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    set_error("fmm_matvec_owned_host: H2D copy failed");
+    return FMM_ECUDA;
+  }
+  int rc = fmm_matvec_owned(h, d_q, d_p, stream);
+  if (rc) return rc;
+  if ((cnt > 0 && cudaMemcpyAsync(h_potential, d_p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("fmm_matvec_owned_host: D2H copy failed");
+    return FMM_ECUDA;
+  }
+  return FMM_OK;
+}
+
+int fmm_owned_range(const fmm_plan* h, int64_t* begin, int64_t* end) {
+  if (!h || !begin || !end) { set_error("fmm_owned_range: null argument"); return FMM_EINVAL; }
+  *begin = h->P.dist.own_lo;
+  *end = h->P.dist.own_hi;
+  return FMM_OK;
+}
+
+int fmm_nccl_unique_id(void* id128) {
+  if (!id128) { set_error("fmm_nccl_unique_id: null argument"); return FMM_EINVAL; }
+  return kifmm::nccl_unique_id(id128) ? FMM_ENCCL : FMM_OK;
+}
+
+// Loopback transport: the same stage sequence as matvec_device, with every exchange
+// done as device-to-device copies between the group's plans.
+int fmm_matvec_group(fmm_plan* const* plans, int np, const double* const* dens, double* const* pots, int owned,
+                     void* stream) {
+  if (!plans || np < 1 || !dens || !pots) { set_error("fmm_matvec_group: invalid argument"); return FMM_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<kifmm::Plan*> Ps(np);
+  for (int r = 0; r < np; ++r) {
+    if (!plans[r] || plans[r]->P.dist.nranks != np || plans[r]->P.dist.rank != r) {
+      set_error("fmm_matvec_group: plans[r] must be rank r of an nplans-rank partition");
+      return FMM_EINVAL;
+    }
+    Ps[r] = &plans[r]->P;
+  }
+  for (int r = 1; r < np; ++r)
+    if (Ps[r]->tree.N != Ps[0]->tree.N || Ps[r]->tree.nboxes != Ps[0]->tree.nboxes || Ps[r]->kp != Ps[0]->kp ||
+        Ps[r]->dist.bnd != Ps[0]->dist.bnd || Ps[r]->n_straddle != Ps[0]->n_straddle) {
+      set_error("fmm_matvec_group: the plans do not describe one partition of one problem");
+      return FMM_EINVAL;
+    }
+  auto stage = [&](int sg) -> int {
+    for (int r = 0; r < np; ++r)
+      if (kifmm::matvec_stage(*Ps[r], sg, dens[r], pots[r], owned != 0, st)) return FMM_ECUDA;
+    return 0;
+  };
+  auto exchange = [&](kifmm::Exchange kifmm::Plan::*which) -> int {
+    for (int r = 0; r < np; ++r)
+      for (int s = 0; s < np; ++s) {
+        if (s == r) continue;
+        kifmm::Exchange& R = Ps[r]->*which;
+        kifmm::Exchange& S = Ps[s]->*which;
+        const int nr = R.recv_off[s + 1] - R.recv_off[s], ns = S.send_off[r + 1] - S.send_off[r];
+        if (nr != ns) { set_error("fmm_matvec_group: send / receive lists disagree"); return FMM_EINVAL; }
+        if (nr && cudaMemcpyAsync(R.d_recv + (size_t)R.recv_off[s] * R.row, S.d_send + (size_t)S.send_off[r] * S.row,
+                                  sizeof(double) * nr * R.row, cudaMemcpyDefault, st) != cudaSuccess) {
+          set_error("fmm_matvec_group: exchange copy failed");
+          return FMM_ECUDA;
+        }
+      }
+    return 0;
+  };
+  int rc;
+  if ((rc = stage(0))) return rc;
+  if (owned && (rc = exchange(&kifmm::Plan::xd))) return rc;
+  if ((rc = stage(1))) return rc;
+  // allreduce of the straddlers' partial multipoles: accumulate on the host (exact
+  // order: rank 0, 1, ...), as NCCL's ring / tree order is unspecified anyway
+  const size_t cnt = (size_t)Ps[0]->n_straddle * Ps[0]->kp;
+  if (cnt) {
+    std::vector<double> sum(cnt, 0.0), part(cnt);
+    for (int r = 0; r < np; ++r) {
+      if (cudaMemcpyAsync(part.data(), Ps[r]->d_straddle_buf, sizeof(double) * cnt, cudaMemcpyDefault, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("fmm_matvec_group: straddler copy failed");
+        return FMM_ECUDA;
+      }
+      for (size_t i = 0; i < cnt; ++i) sum[i] += part[i];
+    }
+    for (int r = 0; r < np; ++r)
+      if (cudaMemcpyAsync(Ps[r]->d_straddle_buf, sum.data(), sizeof(double) * cnt, cudaMemcpyDefault, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess) {
+        set_error("fmm_matvec_group: straddler copy failed");
+        return FMM_ECUDA;
+      }
+  }
+  if ((rc = stage(2))) return rc;
+  if ((rc = exchange(&kifmm::Plan::xq))) return rc;
+  if ((rc = stage(3))) return rc;
+  if (!owned) {
+    for (int r = 0; r < np; ++r)
+      for (int s = 0; s < np; ++s) {
+        const auto& b = Ps[s]->dist.bnd;
+        const size_t c = (size_t)(b[s + 1] - b[s]);
+        if (s == r || !c) continue;
+        if (cudaMemcpyAsync(Ps[r]->d_pot_near + b[s], Ps[s]->d_pot_near + b[s], sizeof(double) * c, cudaMemcpyDefault,
+                            st) != cudaSuccess) {
+          set_error("fmm_matvec_group: allgather copy failed");
+          return FMM_ECUDA;
+        }
+      }
+  }
+  if ((rc = stage(4))) return rc;
+  return FMM_OK;
+}
+
+int fmm_partition_host(int nboxes, const int32_t* level, const int32_t* parent, const int32_t* pbeg,
+                       const int32_t* pend, const uint8_t* leaf, int64_t nU, const int32_t* U, int64_t nV,
+                       const int32_t* V, int64_t nW, const int32_t* W, int64_t nX, const int32_t* X, int n, int k,
+                       int nranks, int rank, fmm_partition** out) {
+  if (!out || nboxes < 1 || !level || !parent || !pbeg || !pend || !leaf || (nU && !U) || (nV && !V) || (nW && !W) ||
+      (nX && !X) || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_error("fmm_partition_host: invalid argument");
+    return FMM_EINVAL;
+  }
+  *out = nullptr;
+  kifmm::PartitionInput in;
+  in.nboxes = nboxes;
+  in.level = level; in.parent = parent; in.pbeg = pbeg; in.pend = pend; in.leaf = leaf;
+  in.nU = nU; in.U = U; in.ustride = 2;
+  in.nV = nV; in.V = V; in.vstride = 3;
+  in.nW = nW; in.W = W; in.wstride = 3;
+  in.nX = nX; in.X = X; in.xstride = 3;
+  in.n = n; in.k = k;
+  for (int b = 0; b < nboxes; ++b)
+    if (parent[b] >= b || (b > 0 && parent[b] < 0) || pbeg[b] > pend[b]) {
+      set_error("fmm_partition_host: boxes must be level-major with parents first");
+      return FMM_EINVAL;
+    }
+  fmm_partition* p = new (std::nothrow) fmm_partition();
+  if (!p) { set_error("fmm_partition_host: out of host memory"); return FMM_ENOMEM; }
+  if (kifmm::build_partition(in, nranks, rank, &p->own)) { delete p; return FMM_EINVAL; }
+  p->view(&p->own);
+  *out = p;
+  return FMM_OK;
+}
+
+int fmm_partition_get(const fmm_partition* p, int what, int64_t* count, const int32_t** data) {
+  if (!p || !p->D || !count || !data) { set_error("fmm_partition_get: null argument"); return FMM_EINVAL; }
+  const kifmm::DistPlan& D = *p->D;
+  const std::vector<int>* v = nullptr;
+  switch (what) {
+    case 0: v = &D.bnd; break;
+    case 1: v = &p->inD32; break;
+    case 2: v = &D.straddle; break;
+    case 3: v = &p->full32; break;
+    case 4: v = &D.q_send; break;
+    case 5: v = &D.q_send_off; break;
+    case 6: v = &D.q_recv; break;
+    case 7: v = &D.q_recv_off; break;
+    case 8: v = &D.d_send; break;
+    case 9: v = &D.d_send_off; break;
+    case 10: v = &D.d_recv; break;
+    case 11: v = &D.d_recv_off; break;
+    default: set_error("fmm_partition_get: unknown array"); return FMM_EINVAL;
+  }
+  *count = (int64_t)v->size();
+  *data = v->data();
+  return FMM_OK;
+}
+
+void fmm_partition_free(fmm_partition* p) { delete p; }
+
+const fmm_partition* fmm_plan_partition(const fmm_plan* h) { return h ? &h->part : nullptr; }
 
 int fmm_matvec_host(fmm_plan* h, const double* h_density, double* h_potential, void* stream) {
   if (!h || !h_density || !h_potential) { set_error("fmm_matvec_host: null argument"); return FMM_EINVAL; }
@@ -208,8 +429,9 @@ int fmm_matvec_host(fmm_plan* h, const double* h_density, double* h_potential, v
     set_error("fmm_matvec_host: H2D copy failed");
     return FMM_ECUDA;
   }
-  int rc = kifmm::matvec_device(P, d_q, d_p, st);
-  if (rc) return FMM_ECUDA;
+  if (P.dist.nranks > 1 && !P.nccl_comm) { set_error("fmm_matvec_host: loopback plan, use fmm_matvec_group"); return FMM_EINVAL; }
+  int rc = kifmm::matvec_device(P, d_q, d_p, false, st);
+  if (rc) return rc == -5 ? FMM_ENCCL : FMM_ECUDA;
   if (cudaMemcpyAsync(h_potential, d_p, sizeof(double) * N, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess) {
     set_error("fmm_matvec_host: D2H copy failed");
@@ -239,8 +461,18 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
   for (int d = 0; d < 3; ++d) info->lo_root[d] = P.tree.lo_root[d];
   info->precompute_ms = h->precompute_ms; info->tree_ms = h->tree_ms; info->lists_ms = h->lists_ms;
   info->schedule_ms = h->schedule_ms;
-  if (P.profile && P.profiled && P.ev_phase.size() == 9 && cudaEventSynchronize(P.ev_phase[8]) == cudaSuccess)
-    for (int i = 0; i < 8; ++i) cudaEventElapsedTime(&info->phase_ms[i], P.ev_phase[i], P.ev_phase[i + 1]);
+  if (P.profile && P.profiled && P.ev_phase.size() == kPhases + 1 && cudaEventSynchronize(P.ev_phase[kPhases]) == cudaSuccess)
+    for (int i = 0; i < kPhases; ++i) cudaEventElapsedTime(&info->phase_ms[i], P.ev_phase[i], P.ev_phase[i + 1]);
+  info->nranks = P.dist.nranks;
+  info->rank = P.dist.rank;
+  info->own_lo = P.dist.own_lo;
+  info->own_hi = P.dist.own_hi;
+  info->n_straddle = P.n_straddle;
+  info->ghost_q_recv = P.xq.nrecv;
+  info->ghost_q_send = P.xq.nsend;
+  info->ghost_d_recv = P.xd.nrecv;
+  info->ghost_d_send = P.xd.nsend;
+  info->nV_local = P.nV_local;
   return FMM_OK;
 }
 

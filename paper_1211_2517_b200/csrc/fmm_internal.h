@@ -82,6 +82,48 @@ struct Lists {
   int4* d_X = nullptr;     // (tgt, src, direct, 0) by (tgt, src)
 };
 
+// Host-side view of a tree and its canonical lists (partition input).  Lists are
+// strided int32 records: U (tgt, src), V (tgt, src, offset id), W / X (tgt, src, direct).
+struct PartitionInput {
+  int nboxes = 0;
+  const int* level = nullptr;
+  const int* parent = nullptr;
+  const int* pbeg = nullptr;
+  const int* pend = nullptr;
+  const uint8_t* leaf = nullptr;
+  int64_t nU = 0, nV = 0, nW = 0, nX = 0;
+  const int* U = nullptr; int ustride = 2;
+  const int* V = nullptr; int vstride = 3;
+  const int* W = nullptr; int wstride = 3;
+  const int* X = nullptr; int xstride = 3;
+  int n = 0, k = 0;
+};
+
+// Morton-range partition of one matvec over nranks (partition.cpp).
+struct DistPlan {
+  int nranks = 1, rank = 0;
+  std::vector<int> bnd;              // nranks + 1 sorted-point boundaries
+  int own_lo = 0, own_hi = 0;        // owned sorted points [own_lo, own_hi)
+  std::vector<double> work;          // estimated work per rank
+  std::vector<uint8_t> inD, full;    // per box: range meets / lies in the owned range
+  std::vector<int> straddle;         // boxes spanning >= 2 ranks (all ranks agree)
+  std::vector<int> q_send, q_send_off, q_recv, q_recv_off;  // ghost q^' boxes, CSR by peer
+  std::vector<int> d_send, d_send_off, d_recv, d_recv_off;  // ghost density points, CSR by peer
+};
+
+int build_partition(const PartitionInput& in, int nranks, int rank, DistPlan* out);
+
+// Device side of one ghost exchange (rows of `row` doubles).
+struct Exchange {
+  int row = 0;
+  std::vector<int> send_off, recv_off;  // per peer, in rows
+  int nsend = 0, nrecv = 0;
+  int* d_send_idx = nullptr;
+  int* d_recv_idx = nullptr;
+  double* d_send = nullptr;
+  double* d_recv = nullptr;
+};
+
 struct Plan {
   int device = 0;
   int p = 0, k = 0, kp = 0, n = 0, leaf_size = 0, wx = 0;
@@ -133,8 +175,36 @@ struct Plan {
   std::vector<cudaEvent_t> ev_phase;
   bool profile = false;
   bool profiled = false;
-  int launches = 0;       // kernels of this library launched by the last matvec  // a profiled matvec has recorded the phase events
+  int launches = 0;       // kernels of this library launched by the last matvec
+  int launch_acc = 0;     // running count across the stages of the current matvec
+  // ---- multi-GPU; nranks == 1: everything owned, exchanges empty
+  DistPlan dist;
+  Exchange xq, xd;                 // ghost q^' rows / ghost densities
+  int n_straddle = 0;
+  int64_t nV_local = 0;            // V pairs with a target in D (this rank's M2L work)
+  int* d_straddle = nullptr;       // straddling boxes
+  double* d_straddle_buf = nullptr;  // n_straddle x kp partial multipoles
+  void* nccl_comm = nullptr;       // ncclComm_t (NULL: single GPU or loopback group)
 };
+
+// matvec stages; between them the transport runs the exchanges:
+//   0 densities (+ pack ghost densities)            -> exchange xd (owned mode)
+//   1 unpack densities, S2M, M2M, pack straddlers   -> allreduce straddlers
+//   2 unpack straddlers, pack ghost q^'             -> exchange xq
+//   3 unpack ghost q^', M2L, X, L2L, L2T, W, P2P, owned output
+//                                                   -> allgather potentials (replicated mode)
+//   4 potential in caller order (replicated mode)
+int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st);
+constexpr int kNumStages = 5;
+int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st);
+
+// NCCL transport (nccl_transport.cpp; libnccl.so.2 resolved at run time)
+int nccl_unique_id(void* id128);
+int nccl_comm_init(Plan& P, const void* id128);
+void nccl_comm_destroy(Plan& P);
+int nccl_exchange(Plan& P, Exchange& X, cudaStream_t st);
+int nccl_allreduce_sum(Plan& P, double* buf, size_t count, cudaStream_t st);
+int nccl_allgather_ranges(Plan& P, double* buf, cudaStream_t st);
 
 // error helpers (thread-local last error)
 void set_error(const std::string& msg);
@@ -155,7 +225,6 @@ int build_tree_device(Plan& P, const double* d_points_caller, cudaStream_t st);
 int build_lists_device(Plan& P, cudaStream_t st);
 int build_schedules(Plan& P, cudaStream_t st);
 int upload_tables(Plan& P);
-int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t st);
 int kernels_init();
 int ggs_tile_width(int M, int K);
 int sib_tile_width(int kp);

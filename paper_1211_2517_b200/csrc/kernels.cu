@@ -547,10 +547,40 @@ __global__ void k_set_density(double4* __restrict__ pts, const int32_t* __restri
   if (i < N) pts[i].w = q[perm[i]];
 }
 
+__global__ void k_set_density_owned(double4* __restrict__ pts, const double* __restrict__ q, int lo, int cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) pts[lo + i].w = q[i];
+}
+
 __global__ void k_gather_output(const double* __restrict__ pnear, const double* __restrict__ pfar,
                                 const int32_t* __restrict__ perm, int64_t N, double* __restrict__ pot) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < N) pot[perm[i]] = pfar ? pnear[i] + pfar[i] : pnear[i];
+}
+
+// owned output in sorted order: pot[i] = near[lo + i] (+ far[lo + i])
+__global__ void k_owned_output(const double* __restrict__ pnear, const double* __restrict__ pfar, int lo, int cnt,
+                               double* __restrict__ pot) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) pot[i] = pfar ? pnear[lo + i] + pfar[lo + i] : pnear[lo + i];
+}
+
+// exchange packing: buf[i][c] = src[idx[i] * ld + c] (c < row), and the inverse store
+__global__ void k_pack_rows(const double* __restrict__ src, int ld, const int* __restrict__ idx, int nrows, int row,
+                            double* __restrict__ buf) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < (int64_t)nrows * row) {
+    int i = (int)(e / row), c = (int)(e - (int64_t)i * row);
+    buf[e] = src[(size_t)idx[i] * ld + c];
+  }
+}
+__global__ void k_unpack_rows(double* __restrict__ dst, int ld, const int* __restrict__ idx, int nrows, int row,
+                              const double* __restrict__ buf) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < (int64_t)nrows * row) {
+    int i = (int)(e / row), c = (int)(e - (int64_t)i * row);
+    dst[(size_t)idx[i] * ld + c] = buf[e];
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -664,89 +694,166 @@ void launch_chk(const EvalArgs& a, int nitems, int n, cudaStream_t st) {
   }
 }
 
-int matvec_device(Plan& P, const double* d_density, double* d_pot, cudaStream_t st) {
+namespace {
+int pack(const double* src, int ld, const int* idx, int nrows, int row, double* buf, cudaStream_t st) {
+  if (nrows == 0) return 0;
+  ++g_launches;
+  const int64_t e = (int64_t)nrows * row;
+  k_pack_rows<<<(int)((e + 255) / 256), 256, 0, st>>>(src, ld, idx, nrows, row, buf);
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
+}
+int unpack(double* dst, int ld, const int* idx, int nrows, int row, const double* buf, cudaStream_t st) {
+  if (nrows == 0) return 0;
+  ++g_launches;
+  const int64_t e = (int64_t)nrows * row;
+  k_unpack_rows<<<(int)((e + 255) / 256), 256, 0, st>>>(dst, ld, idx, nrows, row, buf);
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
+}
+}  // namespace
+
+// Profile events (fmm_info.phase_ms): 0 density (+ghost densities) | 1 S2M | 2 M2M |
+// 3 exchange (straddlers + ghost q^') | 4 M2L | 5 X | 6 L2L | 7 evaluation (L2T, W, P2P) | 8 output
+int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st) {
   Tree& T = P.tree;
   const int64_t N = T.N;
   const int kp = P.kp, np = P.np, k = P.k, n = P.n;
+  const DistPlan& Dp = P.dist;
   auto mark = [&](int i) { if (P.profile) cudaEventRecord(P.ev_phase[i], st); };
-  g_launches = 0;
-  mark(0);
-  ++g_launches;
-  k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N);
-  KIFMM_CUDA(cudaGetLastError());
-  KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
-  KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
+  double* pts_w = reinterpret_cast<double*>(T.d_pts) + 3;  // the q column of the (x, y, z, q) points
   EvalArgs ea{};
   ea.pts = T.d_pts; ea.geom = T.d_geom; ea.pbeg = T.d_pbeg; ea.pend = T.d_pend;
   ea.surf = P.d_surf; ea.n = n; ea.f_in = 1.0 + P.d; ea.f_out = 3.0 - 2.0 * P.d; ea.ldq = np;
-  // near field (P2P: U + direct W/X).  split_phases: a separate pass (phase exports);
-  // otherwise fused with L2T/W into one evaluation pass at the end.
-  if (P.split_phases && P.n_tleaf > 0) {
-    EvalArgs a = ea;
-    a.items = P.d_tleaf_items; a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
-    k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
-    ++g_launches;
-    KIFMM_CUDA(cudaGetLastError());
+  // per-plan launch count across stages (plans of a loopback group interleave)
+  struct LaunchCount {
+    Plan& P;
+    LaunchCount(Plan& p, int stage) : P(p) { g_launches = stage == 0 ? 0 : P.launch_acc; }
+    ~LaunchCount() { P.launch_acc = g_launches; P.launches = g_launches; }
+  } counter(P, stage);
+  switch (stage) {
+    case 0: {  // densities into the Morton-ordered points
+      mark(0);
+      ++g_launches;
+      if (owned) {
+        const int cnt = Dp.own_hi - Dp.own_lo;
+        if (cnt > 0) k_set_density_owned<<<nblk(cnt), 256, 0, st>>>(T.d_pts, d_density, Dp.own_lo, cnt);
+        if (pack(pts_w, 4, P.xd.d_send_idx, P.xd.nsend, 1, P.xd.d_send, st)) return -3;
+      } else {
+        k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N);
+      }
+      KIFMM_CUDA(cudaGetLastError());
+      return 0;
+    }
+    case 1: {  // upward pass (partial multipoles of straddling boxes)
+      if (owned && unpack(pts_w, 4, P.xd.d_recv_idx, P.xd.nrecv, 1, P.xd.d_recv, st)) return -3;
+      KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
+      KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
+      mark(1);
+      // S2M stage 1: check potentials of leaves at level >= 2
+      if (P.n_s2m > 0) {
+        EvalArgs a = ea;
+        a.items = P.d_s2m_items; a.seg_off = P.d_s2m_off; a.segs = P.d_s2m_seg; a.tgt_f = 3.0 - 2.0 * P.d;
+        a.out = P.d_chk_s2m; a.ldo = np;
+        launch_chk(a, P.n_s2m, n, st);
+        ++g_launches;
+        KIFMM_CUDA(cudaGetLastError());
+      }
+      // S2M stage 2: q^'_B = S' c  (store)
+      if (launch_ggs(P.g_s2m, P.d_S, 0, kp, np, k, P.d_chk_s2m, np, P.d_qhat, kp, false, st)) return -3;
+      mark(2);
+      // M2M, finest child level first: q^'_P += 1/2 M~_o q^'_c
+      for (auto& g : P.g_m2m)
+        if (launch_ggs(g, P.d_M, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_qhat, kp, true, st)) return -3;
+      mark(3);
+      return pack(P.d_qhat, kp, P.d_straddle, P.n_straddle, kp, P.d_straddle_buf, st);
+    }
+    case 2:  // complete straddlers, then the ghost multipoles other ranks need
+      if (unpack(P.d_qhat, kp, P.d_straddle, P.n_straddle, kp, P.d_straddle_buf, st)) return -3;
+      return pack(P.d_qhat, kp, P.xq.d_send_idx, P.xq.nsend, kp, P.xq.d_send, st);
+    case 3: {  // interactions and downward pass for the owned targets
+      if (unpack(P.d_qhat, kp, P.xq.d_recv_idx, P.xq.nrecv, kp, P.xq.d_recv, st)) return -3;
+      mark(4);
+      // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
+      //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
+      if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, st)) return -3;
+      if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, st)) return -3;
+      mark(5);
+      // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
+      if (P.n_xnd > 0) {
+        EvalArgs a = ea;
+        a.items = P.d_x_items; a.seg_off = P.d_x_off; a.segs = P.d_x_seg; a.tgt_f = 1.0 + P.d;
+        a.out = P.d_chk_x; a.ldo = np;
+        launch_chk(a, P.n_xnd, n, st);
+        ++g_launches;
+        KIFMM_CUDA(cudaGetLastError());
+        if (launch_ggs(P.g_x, P.d_Ut, 0, kp, np, k, P.d_chk_x, np, P.d_lhat, kp, true, st)) return -3;
+      }
+      mark(6);
+      // L2L, coarsest parent level first: l^_c += L~_o l^_P
+      for (auto& g : P.g_l2l)
+        if (launch_ggs(g, P.d_L, kp * kp, kp, kp, k, P.d_lhat, kp, P.d_lhat, kp, true, st)) return -3;
+      mark(7);
+      // near field alone (split_phases: phase exports)
+      if (P.split_phases && P.n_tleaf > 0) {
+        EvalArgs a = ea;
+        a.items = P.d_tleaf_items; a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
+        k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
+        ++g_launches;
+        KIFMM_CUDA(cudaGetLastError());
+      }
+      // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
+      if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
+      if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
+      // L2T + W stage 2 (and, fused, the near field): potentials at the targets of each leaf
+      if (P.n_tleaf > 0) {
+        EvalArgs a = ea;
+        a.items = P.d_tleaf_items;
+        if (P.split_phases) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far; }
+        else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; a.out = P.d_pot_near; }
+        a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
+        k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
+        ++g_launches;
+        KIFMM_CUDA(cudaGetLastError());
+      }
+      mark(8);
+      if (owned) {
+        const int cnt = Dp.own_hi - Dp.own_lo;
+        ++g_launches;
+        if (cnt > 0)
+          k_owned_output<<<nblk(cnt), 256, 0, st>>>(P.d_pot_near, P.split_phases ? P.d_pot_far : nullptr, Dp.own_lo,
+                                                     cnt, d_pot);
+        KIFMM_CUDA(cudaGetLastError());
+        mark(9);
+        if (P.profile) P.profiled = true;
+      }
+      return 0;
+    }
+    case 4: {  // caller order (replicated mode; the owned ranges were allgathered into pot_near)
+      if (owned) return 0;
+      k_gather_output<<<nblk(N), 256, 0, st>>>(P.d_pot_near, P.split_phases ? P.d_pot_far : nullptr, T.d_perm, N, d_pot);
+      ++g_launches;
+      KIFMM_CUDA(cudaGetLastError());
+      mark(9);
+      if (P.profile) P.profiled = true;
+      return 0;
+    }
   }
-  mark(1);
-  // S2M stage 1: check potentials of leaves at level >= 2
-  if (P.n_s2m > 0) {
-    EvalArgs a = ea;
-    a.items = P.d_s2m_items; a.seg_off = P.d_s2m_off; a.segs = P.d_s2m_seg; a.tgt_f = 3.0 - 2.0 * P.d;
-    a.out = P.d_chk_s2m; a.ldo = np;
-    launch_chk(a, P.n_s2m, n, st);
-    ++g_launches;
-    KIFMM_CUDA(cudaGetLastError());
-  }
-  // S2M stage 2: q^'_B = S' c  (store)
-  if (launch_ggs(P.g_s2m, P.d_S, 0, kp, np, k, P.d_chk_s2m, np, P.d_qhat, kp, false, st)) return -3;
-  mark(2);
-  // M2M, finest child level first: q^'_P += 1/2 M~_o q^'_c
-  for (auto& g : P.g_m2m)
-    if (launch_ggs(g, P.d_M, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_qhat, kp, true, st)) return -3;
-  mark(3);
-  // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
-  //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
-  if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, st)) return -3;
-  if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, st)) return -3;
-  mark(4);
-  // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
-  if (P.n_xnd > 0) {
-    EvalArgs a = ea;
-    a.items = P.d_x_items; a.seg_off = P.d_x_off; a.segs = P.d_x_seg; a.tgt_f = 1.0 + P.d;
-    a.out = P.d_chk_x; a.ldo = np;
-    launch_chk(a, P.n_xnd, n, st);
-    ++g_launches;
-    KIFMM_CUDA(cudaGetLastError());
-    if (launch_ggs(P.g_x, P.d_Ut, 0, kp, np, k, P.d_chk_x, np, P.d_lhat, kp, true, st)) return -3;
-  }
-  mark(5);
-  // L2L, coarsest parent level first: l^_c += L~_o l^_P
-  for (auto& g : P.g_l2l)
-    if (launch_ggs(g, P.d_L, kp * kp, kp, kp, k, P.d_lhat, kp, P.d_lhat, kp, true, st)) return -3;
-  mark(6);
-  // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
-  if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
-  if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
-  // L2T + W stage 2 (and, fused, the near field): potentials at the targets of each leaf
-  if (P.n_tleaf > 0) {
-    EvalArgs a = ea;
-    a.items = P.d_tleaf_items;
-    if (P.split_phases) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far; }
-    else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; a.out = P.d_pot_near; }
-    a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
-    k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
-    ++g_launches;
-    KIFMM_CUDA(cudaGetLastError());
-  }
-  mark(7);
-  k_gather_output<<<nblk(N), 256, 0, st>>>(P.d_pot_near, P.split_phases ? P.d_pot_far : nullptr, T.d_perm, N, d_pot);
-  ++g_launches;
-  P.launches = g_launches;
-  KIFMM_CUDA(cudaGetLastError());
-  mark(8);
-  if (P.profile) P.profiled = true;
-  return 0;
+  return -1;
+}
+
+// One matvec of a single-GPU plan, or of one rank of an NCCL-connected plan.
+int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st) {
+  const bool dist = P.nccl_comm != nullptr;
+  if (matvec_stage(P, 0, d_density, d_pot, owned, st)) return -3;
+  if (dist && owned && nccl_exchange(P, P.xd, st)) return -5;
+  if (matvec_stage(P, 1, d_density, d_pot, owned, st)) return -3;
+  if (dist && nccl_allreduce_sum(P, P.d_straddle_buf, (size_t)P.n_straddle * P.kp, st)) return -5;
+  if (matvec_stage(P, 2, d_density, d_pot, owned, st)) return -3;
+  if (dist && nccl_exchange(P, P.xq, st)) return -5;
+  if (matvec_stage(P, 3, d_density, d_pot, owned, st)) return -3;
+  if (dist && !owned && nccl_allgather_ranges(P, P.d_pot_near, st)) return -5;
+  return matvec_stage(P, 4, d_density, d_pot, owned, st);
 }
 
 }  // namespace kifmm

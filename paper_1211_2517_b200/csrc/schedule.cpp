@@ -90,19 +90,38 @@ int build_schedules(Plan& P, cudaStream_t st) {
   auto npts = [&](int b) { return T.pend[b] - T.pbeg[b]; };
   auto rl = [&](int b) { return std::ldexp(T.r0, -T.level[b]); };
 
-  // ---- target leaves, near (P2P) and far (L2T + W) segment CSRs
+  // ---- partition; one rank owns everything
+  {
+    PartitionInput in;
+    in.nboxes = nb;
+    in.level = T.level.data(); in.parent = T.parent.data(); in.pbeg = T.pbeg.data(); in.pend = T.pend.data();
+    in.leaf = T.leaf.data();
+    in.nU = U.size(); in.U = reinterpret_cast<const int*>(U.data()); in.ustride = 2;
+    in.nV = V.size(); in.V = reinterpret_cast<const int*>(V.data()); in.vstride = 4;
+    in.nW = W.size(); in.W = reinterpret_cast<const int*>(W.data()); in.wstride = 4;
+    in.nX = X.size(); in.X = reinterpret_cast<const int*>(X.data()); in.xstride = 4;
+    in.n = n; in.k = P.k;
+    const int nr = P.dist.nranks, rk = P.dist.rank;
+    if (build_partition(in, nr, rk, &P.dist)) return -1;
+  }
+  const DistPlan& Dp = P.dist;
+  auto inD = [&](int b) { return Dp.inD[b] != 0; };
+
+  // ---- target leaves (owned), near (P2P) and far (L2T + W) segment CSRs
   std::vector<int> leaf_row(nb, -1);
   std::vector<int4> titems;
   for (int b = 0; b < nb; ++b)
-    if (T.leaf[b]) { leaf_row[b] = (int)titems.size(); titems.push_back(make_int4(b, (int)titems.size(), 0, 0)); }
+    if (T.leaf[b] && inD(b)) { leaf_row[b] = (int)titems.size(); titems.push_back(make_int4(b, (int)titems.size(), 0, 0)); }
   const int nt = (int)titems.size();
   std::vector<std::vector<int4>> near(nt), far(nt);
-  for (auto& u : U) near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
+  for (auto& u : U)
+    if (inD(u.x)) near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
   // W pairs: direct -> P2P over the source subtree; else M2T through the source's equivalent density
   std::vector<PairGroup> wgroups;  // grouped by source level (scale r_A)
   std::map<int, int> wlevel;
   int n_wnd = 0;
   for (auto& w : W) {
+    if (!inD(w.x)) continue;
     if (w.z) {
       near[leaf_row[w.x]].push_back(make_int4(0, T.pbeg[w.y], 0, npts(w.y)));
     } else {
@@ -118,6 +137,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   std::vector<int> xoff{0};
   std::vector<PairGroup> xgroup{PairGroup{0, 1.0, {}}};
   for (auto& x : X) {
+    if (!inD(x.x)) continue;
     if (x.z) {
       near[leaf_row[x.x]].push_back(make_int4(0, T.pbeg[x.y], 0, npts(x.y)));
     } else {
@@ -165,7 +185,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   std::vector<int> soff{0};
   std::vector<PairGroup> sgroup{PairGroup{0, 1.0, {}}};
   for (int b = 0; b < nb; ++b) {
-    if (!T.leaf[b] || T.level[b] < 2) continue;
+    if (!T.leaf[b] || T.level[b] < 2 || !inD(b)) continue;
     int row = (int)sitems.size();
     sitems.push_back(make_int4(b, row, 0, 0));
     ssegs.push_back(make_int4(0, T.pbeg[b], 0, npts(b)));
@@ -241,7 +261,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
     int ap[3], aq[3];
     for (int b = 0; b < nb; ++b) {
       const int e0 = vcnt[b], e1 = vcnt[b + 1];
-      if (e0 == e1) continue;
+      if (e0 == e1 || !inD(b)) continue;
+      P.nV_local += e1 - e0;
       anchor(T.parent[b], ap);
       const int a = (int)(T.key[b] & 7);
       // distinct source parents (<= 26)
@@ -296,14 +317,16 @@ int build_schedules(Plan& P, cudaStream_t st) {
   for (int l = T.nlevels - 1; l >= 3; --l) {
     std::vector<PairGroup> groups(8);
     for (int o = 0; o < 8; ++o) groups[o] = PairGroup{o, 0.5, {}};
-    for (int b = T.level_begin[l]; b < T.level_begin[l + 1]; ++b) groups[T.key[b] & 7].pairs.push_back(make_int2(b, T.parent[b]));
+    for (int b = T.level_begin[l]; b < T.level_begin[l + 1]; ++b)
+      if (inD(b)) groups[T.key[b] & 7].pairs.push_back(make_int2(b, T.parent[b]));
     P.g_m2m.emplace_back();
     if (make_launch(P, P.g_m2m.back(), groups, w_sq, st)) return -3;
   }
   for (int l = 2; l + 1 < T.nlevels; ++l) {
     std::vector<PairGroup> groups(8);
     for (int o = 0; o < 8; ++o) groups[o] = PairGroup{o, 1.0, {}};
-    for (int b = T.level_begin[l + 1]; b < T.level_begin[l + 2]; ++b) groups[T.key[b] & 7].pairs.push_back(make_int2(T.parent[b], b));
+    for (int b = T.level_begin[l + 1]; b < T.level_begin[l + 2]; ++b)
+      if (inD(b)) groups[T.key[b] & 7].pairs.push_back(make_int2(T.parent[b], b));
     P.g_l2l.emplace_back();
     if (make_launch(P, P.g_l2l.back(), groups, w_sq, st)) return -3;
   }
@@ -319,6 +342,26 @@ int build_schedules(Plan& P, cudaStream_t st) {
       zalloc(&P.d_eqd_l2t, (size_t)n_l2t * np) || zalloc(&P.d_eqd_w, (size_t)n_wnd * np) ||
       zalloc(&P.d_pot_near, T.N) || zalloc(&P.d_pot_far, T.N) || zalloc(&P.d_io, 2 * T.N))
     return -3;
+  // ---- exchange buffers (empty on one rank)
+  auto make_exchange = [&](Exchange& E, int row, const std::vector<int>& sl, const std::vector<int>& so,
+                           const std::vector<int>& rlst, const std::vector<int>& ro) -> int {
+    E.row = row;
+    E.send_off = so.empty() ? std::vector<int>(Dp.nranks + 1, 0) : so;
+    E.recv_off = ro.empty() ? std::vector<int>(Dp.nranks + 1, 0) : ro;
+    E.nsend = (int)sl.size();
+    E.nrecv = (int)rlst.size();
+    if (upload(P, &E.d_send_idx, sl, st) || upload(P, &E.d_recv_idx, rlst, st)) return -3;
+    if (zalloc(&E.d_send, (size_t)E.nsend * row) || zalloc(&E.d_recv, (size_t)E.nrecv * row)) return -3;
+    return 0;
+  };
+  if (make_exchange(P.xq, kp, Dp.q_send, Dp.q_send_off, Dp.q_recv, Dp.q_recv_off) ||
+      make_exchange(P.xd, 1, Dp.d_send, Dp.d_send_off, Dp.d_recv, Dp.d_recv_off))
+    return -3;
+  P.n_straddle = Dp.nranks > 1 ? (int)Dp.straddle.size() : 0;
+  {
+    std::vector<int> sl = Dp.nranks > 1 ? Dp.straddle : std::vector<int>();
+    if (upload(P, &P.d_straddle, sl, st) || zalloc(&P.d_straddle_buf, (size_t)P.n_straddle * kp)) return -3;
+  }
   KIFMM_CUDA(cudaStreamSynchronize(st));
   return 0;
 }

@@ -96,11 +96,14 @@ def spheres(n_spheres: int = 64, per: int = 1 << 20, seed: int = 0):
     return pts, q
 
 
-def make(name: str, seed: int = 0, n: int | None = None):
+def make(name: str, seed: int = 0, n: int | None = None, scale: int = 1):
     """Return (points [N,3] float64, densities [N] float64, cfg dict) for a config.
-    `n` overrides N for the cube/torus kinds (scaled-down parity cases)."""
+    `n` overrides N for the cube/torus kinds (scaled-down parity cases); `scale`
+    multiplies N (weak-scaling multi-GPU runs: the same recipe, scale x the points)."""
     cfg = dict(CONFIGS[name])
     kind = cfg["kind"]
+    if scale > 1 and n is None:
+        n = cfg["N"] * scale
     if kind == "cube":
         pts, q = uniform_cube(n or cfg["N"], seed)
     elif kind == "sphere_octa":

@@ -58,3 +58,39 @@ def test_host_precompute_matches_oracle_tables(p, k, keff, sub_tol):
         x, y = a["U"] @ a["M"][o] @ a["U"].T, b["U"] @ b["M"][o] @ b["U"].T
         assert np.abs(x - y).max() <= 1e3 * sub_tol * np.abs(y).max()
     assert np.abs(a["U"].T @ a["U"] - np.eye(keff)).max() < 1e-12
+
+
+def test_struct_layouts_match_header(tmp_path):
+    # the ctypes mirrors of fmm_options / fmm_info_t / fmm_tables_view must match the C layout
+    import subprocess
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "kifmm.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(fmm_options), sizeof(fmm_info_t),'
+                   ' sizeof(fmm_tables_view), offsetof(fmm_options, nccl_id), offsetof(fmm_info_t, nV_local));'
+                   'return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert got == [ctypes.sizeof(K.Options), ctypes.sizeof(K.Info), ctypes.sizeof(K.TablesView),
+                   K.Options.nccl_id.offset, K.Info.nV_local.offset]
+
+
+def test_distributed_entry_points_validate_without_gpu():
+    L = K.lib()
+    out = ctypes.c_void_p()
+    opt = K.Options()
+    L.fmm_default_options(ctypes.byref(opt))
+    assert opt.nranks == 1 and opt.rank == 0 and not opt.nccl_id
+    for nr, rk, split in [(0, 0, 0), (2, 2, 0), (2, -1, 0), (2, 0, 1)]:
+        opt.nranks, opt.rank, opt.split_phases = nr, rk, split
+        assert L.fmm_setup_ex(ctypes.c_void_p(8), None, 10, ctypes.byref(opt), None, ctypes.byref(out)) == K.FMM_EINVAL
+    assert L.fmm_matvec_owned(None, None, None, None) == K.FMM_EINVAL
+    assert L.fmm_matvec_owned_host(None, None, None, None) == K.FMM_EINVAL
+    assert L.fmm_matvec_group(None, 0, None, None, 1, None) == K.FMM_EINVAL
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    assert L.fmm_owned_range(None, ctypes.byref(b), ctypes.byref(e)) == K.FMM_EINVAL
+    assert L.fmm_nccl_unique_id(None) == K.FMM_EINVAL
+    assert L.fmm_plan_partition(None) is None
+    z = np.zeros(4, np.int32)
+    assert L.fmm_partition_host(0, *([z.ctypes.data] * 5), 0, None, 0, None, 0, None, 0, None, 56, 25, 2, 0,
+                                ctypes.byref(out)) == K.FMM_EINVAL
