@@ -45,9 +45,10 @@ struct GemmLaunch {
 // (target, src[8]); classes (nvalid, b[8], offset id[8]) for class = delta * 8 + a.
 struct SibLaunch {
   int ntiles = 0, ncols = 0;
-  int4* d_tiles = nullptr;
+  int4* d_tiles = nullptr;   // sorted by decreasing work (operators per column)
   int* d_cols = nullptr;
   int* d_classes = nullptr;
+  int* d_counter = nullptr;  // dynamic tile scheduler (reset before every launch)
 };
 
 struct Tree {

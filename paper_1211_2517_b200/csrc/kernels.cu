@@ -11,6 +11,7 @@
 //             rsqrt: near-field P2P (S2T), S2M / X check potentials,
 //             L2T / W potentials from equivalent densities.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "fmm_internal.h"
@@ -222,31 +223,42 @@ __global__ void __launch_bounds__(KP * 4) k_ggs_sq(const GemmTile* __restrict__ 
 // CTA gathers q^'(child b of Q) (zero if absent) and accumulates
 // C_{2 delta + b - a} q^' in the DMMA accumulators, so each target receives one
 // RED per (target, delta) instead of one per (target, offset).
+//
+// Pipeline (one "step" = one operator b of one tile):
+//   * tiles are handed out dynamically (atomic counter; tiles sorted longest
+//     first), the metadata of the next tile is fetched one tile ahead into a
+//     3-slot ring;
+//   * the B panel of step i+1 is gathered with cp.async (LDGSTS) while step i runs;
+//   * the operator rows (A fragments) stream through registers in chunks of CH
+//     k-steps, chunk c+1 (or chunk 0 of the next step's operator) loaded while
+//     chunk c feeds the tensor pipe.
 // ----------------------------------------------------------------------------
-template <int KP, int NT>
-__global__ void __launch_bounds__(KP * 4) k_m2l_sib(const int4* __restrict__ tiles, int ntiles,
+template <int KP, int NT, int MINB>
+__global__ void __launch_bounds__(KP * 4, MINB) k_m2l_sib(const int4* __restrict__ tiles, int ntiles,
                                                   const int* __restrict__ cols, const int* __restrict__ classes,
-                                                  const double* __restrict__ C, int mvalid, const double* X, double* Y) {
+                                                  const double* __restrict__ C, int mvalid, const double* X, double* Y,
+                                                  int* __restrict__ counter) {
   constexpr int NW = KP / 8;
   constexpr int NTH = NW * 32;
   constexpr int SB = KP + 4;
   constexpr int KS = KP / 4;
   constexpr int K2 = KP / 2;
-  constexpr int CW = 9;                 // column record: target, src[8]
+  constexpr int CW = 9;                        // column record: target, src[8]
+  constexpr int CH = (KS % 4 == 0) ? 4 : 2;    // k-steps per A chunk
+  constexpr int NCH = KS / CH;
   extern __shared__ __align__(16) double sm[];
-  __shared__ int s_meta[2][NT * CW];
+  __shared__ int s_meta[3][NT * CW];
+  __shared__ int s_tile[3];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
-  if (t0 >= t1) return;
+  const int row = warp * 8 + g;
+  int ti = blockIdx.x;
+  if (ti >= ntiles) return;
 
-  // class record: [0] = nvalid, [1..8] = b, [9..16] = offset id
-  // simple (synchronous) metadata load: one int per thread iteration
-  auto fetch_meta = [&](int ti, int slot) {
-    const int4 tl = tiles[ti];
+  auto fetch_meta = [&](int tid, int slot) {
+    const int4 tl = tiles[tid];
     for (int e = threadIdx.x; e < NT * CW; e += NTH) {
-      int c = e / CW;
+      const int c = e / CW;
       s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
     }
   };
@@ -261,60 +273,86 @@ __global__ void __launch_bounds__(KP * 4) k_m2l_sib(const int4* __restrict__ til
       }
     }
   };
+  auto op_rows = [&](int id) { return C + (size_t)id * KP * KP + (size_t)row * KP + t; };
 
-  fetch_meta(t0, 0);
+  int slot = 0;
+  fetch_meta(ti, 0);
+  if (threadIdx.x == 0) s_tile[1] = gridDim.x + atomicAdd(counter, 1);
   __syncthreads();
-  int4 tl = tiles[t0];
-  const int* cls = classes + tl.x * 17;
+  const int* cls = classes + tiles[ti].x * 17;
   gather(0, cls[1], 0);
   cp_async_commit();
-  int buf = 0;
-  for (int ti = t0; ti < t1; ++ti) {
-    const int mslot = (ti - t0) & 1;
-    tl = tiles[ti];
-    cls = classes + tl.x * 17;
-    const int nv = cls[0];
-    double acc[NT / 8][2];
+  double a_cur[CH];
+  const double* Aop = op_rows(cls[9]);
 #pragma unroll
-    for (int j = 0; j < NT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int s = 0; s < CH; ++s) a_cur[s] = __ldg(Aop + 4 * s);
+  int buf = 0;
+  double acc[NT / 8][2];
+#pragma unroll
+  for (int j = 0; j < NT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+
+  while (true) {
+    const int nv = cls[0];
+    const int nslot = slot == 2 ? 0 : slot + 1;
+    const int tnext = s_tile[nslot];
     for (int jb = 0; jb < nv; ++jb) {
+      const bool last = jb + 1 == nv;
+      if (jb == 0 && tnext < ntiles) {  // one tile ahead: its metadata, and the id of the tile after it
+        fetch_meta(tnext, nslot);
+        if (threadIdx.x == 0) s_tile[nslot == 2 ? 0 : nslot + 1] = gridDim.x + atomicAdd(counter, 1);
+      }
       cp_async_wait0();
-      __syncthreads();  // B panel (ti, jb) landed
-      if (jb + 1 < nv) {
-        gather(mslot, cls[2 + jb], buf ^ 1);
-      } else if (ti + 1 < t1) {
-        fetch_meta(ti + 1, mslot ^ 1);
-        __syncthreads();
-        const int* ncls = classes + tiles[ti + 1].x * 17;
-        gather(mslot ^ 1, ncls[1], buf ^ 1);
+      __syncthreads();  // B panel of this step landed; next metadata visible
+      const double* Anext = nullptr;
+      if (!last) {
+        gather(slot, cls[2 + jb], buf ^ 1);
+        Anext = op_rows(cls[9 + jb + 1]);
+      } else if (tnext < ntiles) {
+        const int* ncls = classes + tiles[tnext].x * 17;
+        gather(nslot, ncls[1], buf ^ 1);
+        Anext = op_rows(ncls[9]);
       }
       cp_async_commit();
-      double a_cur[KS];
-      {
-        const double* Arow = C + (size_t)cls[9 + jb] * KP * KP + (size_t)(warp * 8 + g) * KP + t;
+      const double* B = sm + buf * NT * SB + g * SB + t;
 #pragma unroll
-        for (int s2 = 0; s2 < KS; ++s2) a_cur[s2] = __ldg(Arow + 4 * s2);
-      }
-      const double* B = sm + buf * NT * SB;
+      for (int c = 0; c < NCH; ++c) {
+        double a_nxt[CH];
+        const double* src = c + 1 < NCH ? Aop + 4 * CH * (c + 1) : Anext;
+        if (src) {
 #pragma unroll
-      for (int s2 = 0; s2 < KS; ++s2) {
-        const double* bp = B + g * SB + 4 * s2 + t;
-#pragma unroll
-        for (int j = 0; j < NT / 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], a_cur[s2], bp[j * 8 * SB]);
-      }
-      buf ^= 1;
-    }
-    const int row = warp * 8 + g;
-    if (row < mvalid) {
-#pragma unroll
-      for (int j = 0; j < NT / 8; ++j) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int tg = s_meta[mslot][(j * 8 + 2 * t + c) * CW];
-          if (tg >= 0) atomicAdd(Y + (size_t)tg * KP + row, acc[j][c]);
+          for (int s = 0; s < CH; ++s) a_nxt[s] = __ldg(src + 4 * s);
         }
+#pragma unroll
+        for (int s = 0; s < CH; ++s) {
+          const double* bp = B + 4 * (c * CH + s);
+#pragma unroll
+          for (int j = 0; j < NT / 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], a_cur[s], bp[j * 8 * SB]);
+        }
+#pragma unroll
+        for (int s = 0; s < CH; ++s) a_cur[s] = a_nxt[s];
+      }
+      Aop = Anext;
+      buf ^= 1;
+      if (last) {
+        // D(g, 2t + c) of n-block j = output row `row` of column j*8 + 2t + c
+        if (row < mvalid) {
+#pragma unroll
+          for (int j = 0; j < NT / 8; ++j) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int tg = s_meta[slot][(j * 8 + 2 * t + c) * CW];
+              if (tg >= 0) atomicAdd(Y + (size_t)tg * KP + row, acc[j][c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
       }
     }
+    if (tnext >= ntiles) break;
+    ti = tnext;
+    slot = nslot;
+    cls = classes + tiles[ti].x * 17;
   }
 }
 
@@ -348,140 +386,169 @@ struct EvalArgs {
   int ldo;
 };
 
-constexpr int EV_NT = 256;    // threads for point targets
-constexpr int EV_MAXT = 320;  // max threads (surface targets: roundup(n, 32) <= 320)
-constexpr int EV_CH = 512;    // sources staged per chunk
+constexpr int EV_NT = 256;    // threads per target item (default variant)
+constexpr int EV_CH_MAX = 512;  // sources staged per chunk (max over variants)
 constexpr int EV_SEG = 128;   // segments per batch (= 32 lanes x 4)
+constexpr int EV_TB = 4;      // targets per thread (register blocking)
 
-template <bool SURF_TGT>
-__device__ __forceinline__ void eval_target_pos(const EvalArgs& A, const double4& gb, int tbeg, int i, double& x0,
-                                                double& x1, double& x2) {
-  if (SURF_TGT) {
-    const double rad = gb.w * A.tgt_f;
-    x0 = gb.x + rad * A.surf[3 * i];
-    x1 = gb.y + rad * A.surf[3 * i + 1];
-    x2 = gb.z + rad * A.surf[3 * i + 2];
-  } else {
-    const double4 p = A.pts[tbeg + i];
-    x0 = p.x; x1 = p.y; x2 = p.z;
+// Sum over sources sbuf[j0, j1) step G into TB accumulators; CHECK: pairs with
+// r^2 == 0 contribute 0 (reading Q1), else r > 0 is known.
+template <int TB, bool CHECK>
+__device__ __forceinline__ void eval_sources(const double4* sbuf, int j0, int j1, int G, const double (&x)[TB][3],
+                                             double (&acc)[TB]) {
+#pragma unroll 2
+  for (int j = j0; j < j1; j += G) {
+    const double4 sv = sbuf[j];
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      acc[u] = fma(sv.w, CHECK ? rinv_or_zero(r2) : rinv_nonzero(r2), acc[u]);
+    }
   }
 }
 
-// Register-blocked: a pass handles up to 2*NT targets; thread (ti, gi) owns targets
-// t0+ti and t0+ti+mh (mh = ceil(mm/2)) and sweeps source slice gi (stride G).
-template <bool SURF_TGT>
-__global__ void __launch_bounds__(EV_MAXT) k_eval(EvalArgs A) {
-  __shared__ double4 sbuf[EV_CH];
-  __shared__ double red[2 * EV_MAXT];
+// One pass over up to TB * NT targets [t0, t0 + mm) of item `it`: thread (ti, gi)
+// owns targets t0 + ti + u * mq (u < TB, mq = ceil(mm / TB)) and sweeps source slice
+// gi (stride G = NT / mq); slices are summed in shared memory.  Sources are the
+// concatenated segments, staged EV_CH at a time into a double buffer (point sources
+// by cp.async, so chunk c + 1 lands while chunk c is evaluated); the first `nchk`
+// sources are tested for r = 0.
+template <int TB, int EV_CH>
+__device__ __forceinline__ void eval_pass(const EvalArgs& A, const int4& it, int tbeg, int t0, int mm, int sb, int se,
+                                          int nchk, double4 (*sbuf)[EV_CH], double* red, int* s_pref, int4* s_seg) {
+  const int NT = blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int mq = (mm + TB - 1) / TB;
+  const int G = NT / mq;
+  const int ti = threadIdx.x % mq, gi = threadIdx.x / mq;
+  const bool act = gi < G;
+  double x[TB][3], acc[TB];
+#pragma unroll
+  for (int u = 0; u < TB; ++u) {
+    const int i = ti + u * mq;
+    acc[u] = 0.0;
+    if (act && i < mm) {
+      const double4 p = A.pts[tbeg + t0 + i];
+      x[u][0] = p.x; x[u][1] = p.y; x[u][2] = p.z;
+    } else {  // padding target far from everything (result discarded)
+      x[u][0] = 1e100; x[u][1] = 0.0; x[u][2] = 0.0;
+    }
+  }
+  // stage sources [c0, c0 + cn) of the current segment batch into buffer b
+  auto stage = [&](int ns, int c0, int cn, int b) {
+    for (int f = threadIdx.x; f < cn; f += NT) {
+      const int fi = c0 + f;
+      int lo = 0, hi = ns;  // last segment with prefix <= fi
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pref[mid] <= fi) lo = mid; else hi = mid;
+      }
+      const int4 sg = s_seg[lo];
+      const int j = fi - s_pref[lo];
+      if (sg.x == 0) {
+        const double* src = reinterpret_cast<const double*>(A.pts + sg.y + j);
+        double* dst = reinterpret_cast<double*>(&sbuf[b][f]);
+        cp_async16(dst, src);
+        cp_async16(dst + 2, src + 2);
+      } else {
+        const double4 gs = A.geom[sg.z];
+        const double rad = gs.w * (sg.x == 1 ? A.f_out : A.f_in);
+        const double* q = (sg.x == 1 ? A.eqd1 : A.eqd2) + (size_t)sg.y * A.ldq;
+        sbuf[b][f] = make_double4(gs.x + rad * A.surf[3 * j], gs.y + rad * A.surf[3 * j + 1],
+                                  gs.z + rad * A.surf[3 * j + 2], q[j]);
+      }
+    }
+  };
+  int base = 0;  // sources consumed before this segment batch
+  for (int s0 = sb; s0 < se; s0 += EV_SEG) {
+    const int ns = min(EV_SEG, se - s0);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0: segment table + exclusive prefix of lengths
+      int len[4], run = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int sidx = lane * 4 + u;
+        len[u] = 0;
+        if (sidx < ns) {
+          int4 sg = A.segs[s0 + sidx];
+          s_seg[sidx] = sg;
+          len[u] = sg.w;
+        }
+        run += len[u];
+      }
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int excl = incl - run;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int sidx = lane * 4 + u;
+        if (sidx < ns) s_pref[sidx] = excl;
+        excl += len[u];
+      }
+      if (lane == 31) s_pref[ns] = incl;
+    }
+    __syncthreads();
+    const int total = s_pref[ns];
+    stage(ns, 0, min(EV_CH, total), 0);
+    cp_async_commit();
+    int b = 0;
+    for (int c0 = 0; c0 < total; c0 += EV_CH) {
+      const int cn = min(EV_CH, total - c0);
+      cp_async_wait0();
+      __syncthreads();  // chunk c0 staged by every thread; buffer b ^ 1 free
+      if (c0 + EV_CH < total) stage(ns, c0 + EV_CH, min(EV_CH, total - c0 - EV_CH), b ^ 1);
+      cp_async_commit();
+      if (act) {
+        const int split = min(cn, max(0, nchk - (base + c0)));  // checked prefix of this chunk
+        const int j0 = gi;
+        int jc = j0;
+        if (split > 0) {
+          eval_sources<TB, true>(sbuf[b], j0, split, G, x, acc);
+          jc = j0 + ((split - j0 + G - 1) / G) * G;  // first j >= split in this slice
+        }
+        eval_sources<TB, false>(sbuf[b], jc, cn, G, x, acc);
+      }
+      b ^= 1;
+    }
+    base += total;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < TB; ++u) red[u * NT + threadIdx.x] = acc[u];
+  __syncthreads();
+  for (int i = threadIdx.x; i < mm; i += NT) {
+    const int u = i / mq, tl = i - u * mq;
+    double sum = 0;
+    for (int gg = 0; gg < G; ++gg) sum += red[u * NT + gg * mq + tl];
+    A.out[tbeg + t0 + i] = sum * kInv4Pi;
+  }
+}
+
+// k_eval: one CTA per target leaf (item (box, row, 0, 0)): potentials of the leaf's
+// points from its source segments (kind, a, b, len):
+//   kind 0: points pts[a .. a+len)                       (P2P: U, direct W / X)
+//   kind 1: surface of box b, radius r_b * f_out, densities eqd1[a * ldq + m]   (L2T)
+//   kind 2: surface of box b, radius r_b * f_in,  densities eqd2[a * ldq + m]   (W)
+// chk_self: the first m_B sources are the leaf's own points (r = 0 possible).
+template <int NT, int CH>
+__global__ void __launch_bounds__(NT) k_eval(EvalArgs A, int chk_self) {
+  __shared__ __align__(16) double4 sbuf[2][CH];
+  __shared__ double red[EV_TB * NT];
   __shared__ int s_pref[EV_SEG + 1];
   __shared__ int4 s_seg[EV_SEG];
-  const int NT = blockDim.x;
-  const int item = blockIdx.x;
-  const int4 it = A.items[item];
-  const int box = it.x;
-  const double4 gb = A.geom[box];
-  int m, tbeg = 0;
-  if (SURF_TGT) m = A.n;
-  else { tbeg = A.pbeg[box]; m = A.pend[box] - tbeg; }
-  const int sb = A.seg_off[item], se = A.seg_off[item + 1];
-  const int lane = threadIdx.x & 31;
-  for (int t0 = 0; t0 < m; t0 += 2 * NT) {
-    const int mm = min(m - t0, 2 * NT);
-    const int mh = (mm + 1) >> 1;
-    const int G = NT / mh;
-    const int ti = threadIdx.x % mh, gi = threadIdx.x / mh;
-    const bool act = gi < G;
-    const bool has2 = ti + mh < mm;
-    double xa0 = 0, xa1 = 0, xa2 = 0, xb0 = 1e300, xb1 = 0, xb2 = 0;
-    if (act) {
-      eval_target_pos<SURF_TGT>(A, gb, tbeg, t0 + ti, xa0, xa1, xa2);
-      if (has2) eval_target_pos<SURF_TGT>(A, gb, tbeg, t0 + ti + mh, xb0, xb1, xb2);
-    }
-    double acca = 0.0, accb = 0.0;
-    for (int s0 = sb; s0 < se; s0 += EV_SEG) {
-      const int ns = min(EV_SEG, se - s0);
-      __syncthreads();
-      if (threadIdx.x < 32) {  // warp 0: segment table + exclusive prefix of lengths
-        int len[4], run = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          int sidx = lane * 4 + u;
-          len[u] = 0;
-          if (sidx < ns) {
-            int4 sg = A.segs[s0 + sidx];
-            s_seg[sidx] = sg;
-            len[u] = sg.w;
-          }
-          run += len[u];
-        }
-        int incl = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        int excl = incl - run;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          int sidx = lane * 4 + u;
-          if (sidx < ns) s_pref[sidx] = excl;
-          excl += len[u];
-        }
-        if (lane == 31) s_pref[ns] = incl;
-      }
-      __syncthreads();
-      const int total = s_pref[ns];
-      for (int c0 = 0; c0 < total; c0 += EV_CH) {
-        const int cn = min(EV_CH, total - c0);
-        __syncthreads();
-        for (int f = threadIdx.x; f < cn; f += NT) {
-          int fi = c0 + f;
-          int lo = 0, hi = ns;  // last segment with prefix <= fi
-          while (hi - lo > 1) {
-            int mid = (lo + hi) >> 1;
-            if (s_pref[mid] <= fi) lo = mid; else hi = mid;
-          }
-          const int4 sg = s_seg[lo];
-          const int j = fi - s_pref[lo];
-          double4 v;
-          if (sg.x == 0) {
-            v = A.pts[sg.y + j];
-          } else {
-            const double4 gs = A.geom[sg.z];
-            const double rad = gs.w * (sg.x == 1 ? A.f_out : A.f_in);
-            const double* q = (sg.x == 1 ? A.eqd1 : A.eqd2) + (size_t)sg.y * A.ldq;
-            v = make_double4(gs.x + rad * A.surf[3 * j], gs.y + rad * A.surf[3 * j + 1], gs.z + rad * A.surf[3 * j + 2], q[j]);
-          }
-          sbuf[f] = v;
-        }
-        __syncthreads();
-        if (act) {
-#pragma unroll 2
-          for (int j = gi; j < cn; j += G) {
-            const double4 sv = sbuf[j];
-            const double ax = xa0 - sv.x, ay = xa1 - sv.y, az = xa2 - sv.z;
-            const double bx = xb0 - sv.x, by = xb1 - sv.y, bz = xb2 - sv.z;
-            const double ra = fma(az, az, fma(ay, ay, ax * ax));
-            const double rb = fma(bz, bz, fma(by, by, bx * bx));
-            acca = fma(sv.w, rinv_or_zero(ra), acca);
-            accb = fma(sv.w, rinv_or_zero(rb), accb);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    red[threadIdx.x] = acca;
-    red[NT + threadIdx.x] = accb;
-    __syncthreads();
-    for (int i = threadIdx.x; i < mm; i += NT) {
-      const int half = i < mh ? 0 : 1;
-      const int tl = i - half * mh;
-      double sum = 0;
-      for (int gg = 0; gg < G; ++gg) sum += red[half * NT + gg * mh + tl];
-      sum *= kInv4Pi;
-      if (SURF_TGT) A.out[(size_t)it.y * A.ldo + t0 + i] = sum;
-      else A.out[tbeg + t0 + i] = sum;
-    }
+  const int4 it = A.items[blockIdx.x];
+  const int tbeg = A.pbeg[it.x], m = A.pend[it.x] - tbeg;
+  const int sb = A.seg_off[blockIdx.x], se = A.seg_off[blockIdx.x + 1];
+  const int nchk = chk_self ? m : 0;
+  for (int t0 = 0; t0 < m; t0 += EV_TB * NT) {
+    const int mm = min(m - t0, EV_TB * NT);
+    if (mm >= 12) eval_pass<EV_TB, CH>(A, it, tbeg, t0, mm, sb, se, nchk, sbuf, red, s_pref, s_seg);
+    else eval_pass<2, CH>(A, it, tbeg, t0, mm, sb, se, nchk, sbuf, red, s_pref, s_seg);
   }
 }
 
@@ -634,23 +701,31 @@ int launch_ggs(const GemmLaunch& g, const double* ops, int op_stride, int M, int
 
 }  // namespace
 
-template <int KP>
+template <int KP, int MINB>
 int launch_sib(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
   constexpr int NT = sq_nt(KP);
   const size_t smem = (size_t)NT * 2 * (KP + 4) * sizeof(double);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_sib<KP, NT>, KP * 4, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_sib<KP, NT, MINB>, KP * 4, smem);
   const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
-  k_m2l_sib<KP, NT><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y);
+  KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
+  k_m2l_sib<KP, NT, MINB><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y,
+                                                      g.d_counter);
   return 0;
+}
+
+// KIFMM_SIB_MINB (diagnostics): 2 = no register cap for the KP <= 64 kernels
+static int sib_minb() {
+  static int v = [] { const char* e = std::getenv("KIFMM_SIB_MINB"); return e ? std::atoi(e) : 3; }();
+  return v;
 }
 
 int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, const double* X, double* Y, cudaStream_t st) {
   if (g.ntiles == 0) return 0;
   ++g_launches;
-  if (kp == 32) launch_sib<32>(g, C, mvalid, X, Y, st);
-  else if (kp == 64) launch_sib<64>(g, C, mvalid, X, Y, st);
-  else launch_sib<104>(g, C, mvalid, X, Y, st);
+  if (kp == 32) { if (sib_minb() == 3) launch_sib<32, 3>(g, C, mvalid, X, Y, st); else launch_sib<32, 1>(g, C, mvalid, X, Y, st); }
+  else if (kp == 64) { if (sib_minb() == 3) launch_sib<64, 3>(g, C, mvalid, X, Y, st); else launch_sib<64, 1>(g, C, mvalid, X, Y, st); }
+  else launch_sib<104, 1>(g, C, mvalid, X, Y, st);
   KIFMM_CUDA(cudaGetLastError());
   return 0;
 }
@@ -670,16 +745,25 @@ int kernels_init() {
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs_sq<64, sq_nt(64)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs_sq<104, sq_nt(104)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
 }
 
 
 // Evaluation work lists live in the plan; see build_schedules (schedule.cpp).
-struct EvalLaunch;
+// k_eval with 128 threads per target leaf (measured best of 128 / 256 threads and
+// a warp-per-leaf variant; KIFMM_EVAL_NT=256 selects the 256-thread kernel)
+static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st) {
+  static const int nt = [] { const char* e = std::getenv("KIFMM_EVAL_NT"); return e ? std::atoi(e) : 128; }();
+  a.items = P.d_tleaf_items;
+  if (nt == 256) k_eval<256, 512><<<P.n_tleaf, 256, 0, st>>>(a, chk_self);
+  else k_eval<128, 256><<<P.n_tleaf, 128, 0, st>>>(a, chk_self);
+}
 
 // check points per lane: one round of 32*TB when n <= 160, else rounds of 32*ceil(n/64)
 void launch_chk(const EvalArgs& a, int nitems, int n, cudaStream_t st) {
@@ -798,7 +882,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       if (P.split_phases && P.n_tleaf > 0) {
         EvalArgs a = ea;
         a.items = P.d_tleaf_items; a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
-        k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
+        launch_eval(P, a, 1, st);
         ++g_launches;
         KIFMM_CUDA(cudaGetLastError());
       }
@@ -812,7 +896,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (P.split_phases) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far; }
         else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; a.out = P.d_pot_near; }
         a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
-        k_eval<false><<<P.n_tleaf, EV_NT, 0, st>>>(a);
+        launch_eval(P, a, P.split_phases ? 0 : 1, st);
         ++g_launches;
         KIFMM_CUDA(cudaGetLastError());
       }

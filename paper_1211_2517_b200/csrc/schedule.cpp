@@ -114,8 +114,15 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (T.leaf[b] && inD(b)) { leaf_row[b] = (int)titems.size(); titems.push_back(make_int4(b, (int)titems.size(), 0, 0)); }
   const int nt = (int)titems.size();
   std::vector<std::vector<int4>> near(nt), far(nt);
+  // the target leaf's own points first: only they can coincide with a target (equal
+  // coordinates give equal Morton keys, hence the same leaf), so k_eval tests r = 0
+  // on the first m_B sources only
+  for (int i = 0; i < nt; ++i) {
+    const int b = titems[i].x;
+    near[i].push_back(make_int4(0, T.pbeg[b], 0, npts(b)));
+  }
   for (auto& u : U)
-    if (inD(u.x)) near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
+    if (inD(u.x) && u.y != u.x) near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
   // W pairs: direct -> P2P over the source subtree; else M2T through the source's equivalent density
   std::vector<PairGroup> wgroups;  // grouped by source level (scale r_A)
   std::map<int, int> wlevel;
@@ -173,6 +180,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     all_off.push_back((int)all_seg.size());
   }
   P.n_tleaf = nt;
+
   P.n_near_seg = (int)near_seg.size();
   P.n_far_seg = (int)far_seg.size();
   if (upload(P, &P.d_tleaf_items, titems, st) || upload(P, &P.d_near_off, near_off, st) ||
@@ -305,10 +313,14 @@ int build_schedules(Plan& P, cudaStream_t st) {
       cols.insert(cols.end(), cc.begin(), cc.end());
       for (int c = 0; c < ncol; c += NTs) tiles.push_back(make_int4(cls, base + c, std::min(NTs, ncol - c), 0));
     }
+    // longest tiles first (the kernel hands tiles out dynamically: LPT order balances the SMs)
+    std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
+      return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
+    });
     P.g_m2l_sib.ntiles = (int)tiles.size();
     P.g_m2l_sib.ncols = (int)cols.size() / 9;
     if (upload(P, &P.g_m2l_sib.d_tiles, tiles, st) || upload(P, &P.g_m2l_sib.d_cols, cols, st) ||
-        upload(P, &P.g_m2l_sib.d_classes, classes, st))
+        upload(P, &P.g_m2l_sib.d_classes, classes, st) || upload(P, &P.g_m2l_sib.d_counter, std::vector<int>(1, 0), st))
       return -3;
   }
   // M2M per child level (finest first) and L2L per parent level (coarsest first), by octant
