@@ -83,6 +83,10 @@ typedef struct {
   int nranks;         /* default 1 */
   int rank;           /* 0 <= rank < nranks */
   const void* nccl_id;
+  int leaf_ops;       /* per-leaf S2M / L2T operators built at setup (2 x owned points x kp
+                         doubles): a matvec then streams them from HBM instead of evaluating
+                         2n kernel values per point.  -1 (default): when they fit in 40% of the
+                         free device memory; 0 off; 1 on. */
 } fmm_options;
 
 typedef struct {
@@ -103,6 +107,7 @@ typedef struct {
   int64_t ghost_q_recv, ghost_q_send;  /* ghost multipole rows per matvec */
   int64_t ghost_d_recv, ghost_d_send;  /* ghost densities per matvec (owned mode) */
   int64_t nV_local;           /* V pairs this rank's M2L applies (= nV on one rank) */
+  int64_t leaf_op_bytes;      /* device bytes of the per-leaf operators (0: not used) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

@@ -33,7 +33,8 @@ class Options(ctypes.Structure):
     _fields_ = [("p", ctypes.c_int), ("k", ctypes.c_int), ("leaf_size", ctypes.c_int), ("d", ctypes.c_double),
                 ("pinv_rcond", ctypes.c_double), ("wx_direct_max", ctypes.c_int),
                 ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int),
-                ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p)]
+                ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+                ("leaf_ops", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -48,7 +49,8 @@ class Info(ctypes.Structure):
                 ("phase_ms", ctypes.c_float * 9), ("nranks", ctypes.c_int), ("rank", ctypes.c_int),
                 ("own_lo", ctypes.c_int64), ("own_hi", ctypes.c_int64), ("n_straddle", ctypes.c_int64),
                 ("ghost_q_recv", ctypes.c_int64), ("ghost_q_send", ctypes.c_int64),
-                ("ghost_d_recv", ctypes.c_int64), ("ghost_d_send", ctypes.c_int64), ("nV_local", ctypes.c_int64)]
+                ("ghost_d_recv", ctypes.c_int64), ("ghost_d_send", ctypes.c_int64), ("nV_local", ctypes.c_int64),
+                ("leaf_op_bytes", ctypes.c_int64)]
 
 
 # phases of fmm_matvec (profile=True): the near field is evaluated in the "eval" pass together with
@@ -190,7 +192,7 @@ class Plan:
     def __init__(self, points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, d: float = 0.1,
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
                  split_phases: bool = False, stream=None, nranks: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, leaf_ops: int = -1):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -200,7 +202,7 @@ class Plan:
         lib().fmm_default_options(ctypes.byref(opt))
         opt.p, opt.k, opt.leaf_size, opt.d, opt.pinv_rcond = p, k, leaf_size, d, rcond
         opt.wx_direct_max, opt.profile, opt.split_phases = wx_direct_max, int(profile), int(split_phases)
-        opt.nranks, opt.rank = nranks, rank
+        opt.nranks, opt.rank, opt.leaf_ops = nranks, rank, int(leaf_ops)
         self._keep = []
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

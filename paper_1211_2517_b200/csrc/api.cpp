@@ -79,6 +79,7 @@ void fmm_default_options(fmm_options* o) {
   o->nranks = 1;
   o->rank = 0;
   o->nccl_id = nullptr;
+  o->leaf_ops = -1;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -141,6 +142,7 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   P.rcond = opt->pinv_rcond;
   P.profile = opt->profile != 0;
   P.split_phases = opt->split_phases != 0;
+  P.leaf_ops_opt = opt->leaf_ops;
   P.dist.nranks = opt->nranks;
   P.dist.rank = opt->rank;
   auto fail = [&](int rc) { free_plan_memory(h); delete h; return rc; };
@@ -473,6 +475,7 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
   info->ghost_d_recv = P.xd.nrecv;
   info->ghost_d_send = P.xd.nsend;
   info->nV_local = P.nV_local;
+  info->leaf_op_bytes = P.leaf_op_bytes;
   return FMM_OK;
 }
 

@@ -158,6 +158,14 @@ struct Plan {
   int* d_far_off = nullptr;  int4* d_far_seg = nullptr;  int n_far_seg = 0;
   int* d_all_off = nullptr;  int4* d_all_seg = nullptr;  // near + far segments (fused pass)
   bool split_phases = false;  // separate near / far passes (phase exports)
+  // per-leaf operators (leaf-op mode): S2M  q^'_B = S_B q_B  with S_B = S' G(UC_B, x_B)
+  // (point-major rows of kp), L2T  pot_B = T_B l^_B  with T_B = r_l G(x_B, DE_B) T'
+  // (kp-major within a leaf block); both indexed by sorted point - own_lo
+  int leaf_ops_opt = -1;      // -1 auto, 0 off, 1 on
+  bool leaf_ops = false;
+  double* d_s2m_mat = nullptr;
+  double* d_l2t_mat = nullptr;
+  int64_t leaf_op_bytes = 0;
   int n_s2m = 0; int4* d_s2m_items = nullptr; int* d_s2m_off = nullptr; int4* d_s2m_seg = nullptr;
   int n_xnd = 0; int4* d_x_items = nullptr;   int* d_x_off = nullptr;   int4* d_x_seg = nullptr;
   int n_l2t = 0, n_wnd = 0;
@@ -195,6 +203,7 @@ struct Plan {
 //   3 unpack ghost q^', M2L, X, L2L, L2T, W, P2P, owned output
 //                                                   -> allgather potentials (replicated mode)
 //   4 potential in caller order (replicated mode)
+int build_leaf_ops(Plan& P, cudaStream_t st);
 int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st);
 constexpr int kNumStages = 5;
 int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st);

@@ -384,6 +384,7 @@ struct EvalArgs {
   double tgt_f;          // surface factor of SURF_TGT targets
   double* out;
   int ldo;
+  int accumulate;        // k_eval: out += result (leaf-op mode: L2T already stored)
 };
 
 constexpr int EV_NT = 256;    // threads per target item (default variant)
@@ -525,7 +526,8 @@ __device__ __forceinline__ void eval_pass(const EvalArgs& A, const int4& it, int
     const int u = i / mq, tl = i - u * mq;
     double sum = 0;
     for (int gg = 0; gg < G; ++gg) sum += red[u * NT + gg * mq + tl];
-    A.out[tbeg + t0 + i] = sum * kInv4Pi;
+    double* o = A.out + tbeg + t0 + i;
+    *o = A.accumulate ? *o + sum * kInv4Pi : sum * kInv4Pi;
   }
 }
 
@@ -605,6 +607,126 @@ __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) 
       const int i = r0 + lane + 32 * u;
       if (i < n) A.out[(size_t)it.y * A.ldo + i] = acc[u] * kInv4Pi;
     }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Per-leaf operators (leaf-op mode).  The S2M check potential and the L2T
+// equivalent density are linear in the leaf's densities / compressed local
+// expansion, so the two stages fold into one k x m (S2M) and m x k (L2T) operator
+// per leaf, built once at setup (Step 1) — the same products
+// S' (G q) and G (T' l^) with the sums reassociated:
+//   S2M:  q^'_B = S_B q_B,   S_B = S' G(c_B + r_B (3-2d) e, x_B)
+//   L2T:  p_B  = T_B l^_B,  T_B = r_B G(x_B, c_B + r_B (3-2d) e) T'
+// so a matvec streams 2 x kp doubles per point from HBM instead of evaluating
+// 2 n kernel values per point on the FP64 pipe.
+// k_leafop_build: out(j, a) = scale * sum_i Op[a * sa + i * si] * G(surface_i, x_j),
+//   MODE 0 (S2M): point-major rows  out[(pbeg + j - own_lo) * kp + a]
+//   MODE 1 (L2T): kp-major per leaf out[(pbeg - own_lo) * kp + a * m + j], scale r_B
+// ----------------------------------------------------------------------------
+constexpr int LO_CH = 32;
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ items, const double4* __restrict__ pts,
+                                                      const double4* __restrict__ geom, const int* __restrict__ pbeg,
+                                                      const int* __restrict__ pend, const double* __restrict__ surf,
+                                                      int n, int kp, double f, const double* __restrict__ Op, int sa,
+                                                      int si, int own_lo, double* __restrict__ out) {
+  extern __shared__ double Gs[];  // n x (LO_CH + 1)
+  const int b = items[blockIdx.x].x;
+  const double4 gb = geom[b];
+  const int p0 = pbeg[b], m = pend[b] - p0;
+  const double rad = gb.w * f;
+  const double scale = MODE == 1 ? gb.w : 1.0;
+  for (int c0 = 0; c0 < m; c0 += LO_CH) {
+    const int cm = min(LO_CH, m - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * LO_CH; e += blockDim.x) {
+      const int i = e / LO_CH, jj = e - i * LO_CH;
+      double v = 0.0;
+      if (jj < cm) {
+        const double4 x = pts[p0 + c0 + jj];
+        const double dx = gb.x + rad * surf[3 * i] - x.x;
+        const double dy = gb.y + rad * surf[3 * i + 1] - x.y;
+        const double dz = gb.z + rad * surf[3 * i + 2] - x.z;
+        v = kInv4Pi * rinv_nonzero(fma(dz, dz, fma(dy, dy, dx * dx)));  // surface outside the leaf: r > 0
+      }
+      Gs[i * (LO_CH + 1) + jj] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kp * LO_CH; e += blockDim.x) {
+      const int a = e / LO_CH, jj = e - a * LO_CH;
+      if (jj >= cm) continue;
+      const double* op = Op + (size_t)a * sa;
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc = fma(op[(size_t)i * si], Gs[i * (LO_CH + 1) + jj], acc);
+      acc *= scale;
+      const int j = c0 + jj;
+      if (MODE == 0) out[(size_t)(p0 + j - own_lo) * kp + a] = acc;
+      else out[(size_t)(p0 - own_lo) * kp + (size_t)a * m + j] = acc;
+    }
+  }
+}
+
+// S2M with leaf operators: q^'_B[a] = sum_j q_j S_B[j][a]; one warp per leaf, rows of
+// kp doubles read coalesced; stored (a leaf's multipole is written only here)
+__global__ void __launch_bounds__(256) k_s2m_leafop(const int4* __restrict__ items, int nitems,
+                                                    const double4* __restrict__ pts, const int* __restrict__ pbeg,
+                                                    const int* __restrict__ pend, const double* __restrict__ S, int kp,
+                                                    int own_lo, double* __restrict__ qhat) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nitems) return;
+  const int b = items[w].x;
+  const int p0 = pbeg[b], m = pend[b] - p0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* row = S + (size_t)(p0 - own_lo) * kp;
+#pragma unroll 4
+  for (int j = 0; j < m; ++j) {
+    const double q = pts[p0 + j].w;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int a = lane + 32 * c;
+      if (a < kp) acc[c] = fma(q, __ldcs(row + (size_t)j * kp + a), acc[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int a = lane + 32 * c;
+    if (a < kp) qhat[(size_t)b * kp + a] = acc[c];
+  }
+}
+
+// L2T with leaf operators: pot[p0 + j] = sum_a T_B[a][j] l^_B[a] for every owned target
+// leaf (leaves above level 2 have no far field: 0); one warp per leaf
+constexpr int L2T_WARPS = 8;
+__global__ void __launch_bounds__(L2T_WARPS * 32) k_l2t_leafop(const int4* __restrict__ items, int nitems,
+                                                             const int* __restrict__ level, const int* __restrict__ pbeg,
+                                                             const int* __restrict__ pend, const double* __restrict__ Tm,
+                                                             const double* __restrict__ lhat, int kp, int own_lo,
+                                                             double* __restrict__ pot) {
+  __shared__ double lh[L2T_WARPS][128];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * L2T_WARPS + wl;
+  if (w >= nitems) return;
+  const int b = items[w].x;
+  const int p0 = pbeg[b], m = pend[b] - p0;
+  if (level[b] < 2) {
+    for (int j = lane; j < m; j += 32) pot[p0 + j] = 0.0;
+    return;
+  }
+  for (int a = lane; a < kp; a += 32) lh[wl][a] = lhat[(size_t)b * kp + a];
+  __syncwarp();
+  const double* base = Tm + (size_t)(p0 - own_lo) * kp;
+  for (int j = lane; j < m; j += 32) {
+    double acc0 = 0.0, acc1 = 0.0;
+    int a = 0;
+#pragma unroll 4
+    for (; a + 1 < kp; a += 2) {
+      acc0 = fma(__ldcs(base + (size_t)a * m + j), lh[wl][a], acc0);
+      acc1 = fma(__ldcs(base + (size_t)(a + 1) * m + j), lh[wl][a + 1], acc1);
+    }
+    if (a < kp) acc0 = fma(__ldcs(base + (size_t)a * m + j), lh[wl][a], acc0);
+    pot[p0 + j] = acc0 + acc1;
   }
 }
 
@@ -730,6 +852,22 @@ int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, cons
   return 0;
 }
 
+int build_leaf_ops(Plan& P, cudaStream_t st) {
+  if (P.n_s2m == 0) return 0;
+  const Tree& T = P.tree;
+  const size_t smem = (size_t)P.n * (LO_CH + 1) * sizeof(double);
+  KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const double f = 3.0 - 2.0 * P.d;  // UC and DE halfwidth factor
+  k_leafop_build<0><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
+                                                P.kp, f, P.d_S, P.np, 1, P.dist.own_lo, P.d_s2m_mat);
+  KIFMM_CUDA(cudaGetLastError());
+  k_leafop_build<1><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
+                                                P.kp, f, P.d_T, 1, P.kp, P.dist.own_lo, P.d_l2t_mat);
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int sib_tile_width(int kp) { return sq_nt(kp); }
 
 int ggs_tile_width(int M, int K) {
@@ -834,8 +972,14 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       mark(1);
-      // S2M stage 1: check potentials of leaves at level >= 2
-      if (P.n_s2m > 0) {
+      if (P.leaf_ops) {  // S2M as one GEMV per leaf with its precomputed operator
+        if (P.n_s2m > 0) {
+          ++g_launches;
+          k_s2m_leafop<<<(P.n_s2m + 7) / 8, 256, 0, st>>>(P.d_s2m_items, P.n_s2m, T.d_pts, T.d_pbeg, T.d_pend,
+                                                          P.d_s2m_mat, kp, Dp.own_lo, P.d_qhat);
+          KIFMM_CUDA(cudaGetLastError());
+        }
+      } else if (P.n_s2m > 0) {  // S2M stage 1: check potentials of leaves at level >= 2
         EvalArgs a = ea;
         a.items = P.d_s2m_items; a.seg_off = P.d_s2m_off; a.segs = P.d_s2m_seg; a.tgt_f = 3.0 - 2.0 * P.d;
         a.out = P.d_chk_s2m; a.ldo = np;
@@ -844,7 +988,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaGetLastError());
       }
       // S2M stage 2: q^'_B = S' c  (store)
-      if (launch_ggs(P.g_s2m, P.d_S, 0, kp, np, k, P.d_chk_s2m, np, P.d_qhat, kp, false, st)) return -3;
+      if (!P.leaf_ops && launch_ggs(P.g_s2m, P.d_S, 0, kp, np, k, P.d_chk_s2m, np, P.d_qhat, kp, false, st)) return -3;
       mark(2);
       // M2M, finest child level first: q^'_P += 1/2 M~_o q^'_c
       for (auto& g : P.g_m2m)
@@ -889,10 +1033,19 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
       if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
       if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
+      // leaf-op mode: L2T as one GEMV per leaf, stored; the evaluation pass below adds to it
+      if (P.leaf_ops && P.n_tleaf > 0) {
+        ++g_launches;
+        k_l2t_leafop<<<(P.n_tleaf + L2T_WARPS - 1) / L2T_WARPS, L2T_WARPS * 32, 0, st>>>(
+            P.d_tleaf_items, P.n_tleaf, T.d_level, T.d_pbeg, T.d_pend, P.d_l2t_mat, P.d_lhat, kp, Dp.own_lo,
+            P.split_phases ? P.d_pot_far : P.d_pot_near);
+        KIFMM_CUDA(cudaGetLastError());
+      }
       // L2T + W stage 2 (and, fused, the near field): potentials at the targets of each leaf
       if (P.n_tleaf > 0) {
         EvalArgs a = ea;
         a.items = P.d_tleaf_items;
+        a.accumulate = P.leaf_ops ? 1 : 0;
         if (P.split_phases) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far; }
         else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; a.out = P.d_pot_near; }
         a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;

@@ -62,11 +62,11 @@ def tables(p, k):
     return _TABLES[(p, k)]
 
 
-def group(pts, p, k, s, R, tb, wx=-1):
+def group(pts, p, k, s, R, tb, wx=-1, leaf_ops=-1):
     dev = torch.device("cuda:0")
     P = torch.from_numpy(pts).to(dev)
-    return [K().Plan(P, None, p=p, k=k, leaf_size=s, wx_direct_max=wx, tables=tb, nranks=R, rank=r)
-            for r in range(R)]
+    return [K().Plan(P, None, p=p, k=k, leaf_size=s, wx_direct_max=wx, tables=tb, nranks=R, rank=r,
+                     leaf_ops=leaf_ops) for r in range(R)]
 
 
 def run_owned(plans, q):
@@ -86,12 +86,12 @@ def run_owned(plans, q):
 
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("R", [2, 3, 5])
-@pytest.mark.parametrize("wx", [-1, 0])
-def test_loopback_group_parity(case, R, wx):
+@pytest.mark.parametrize("wx,leaf_ops", [(-1, 1), (0, 0)])
+def test_loopback_group_parity(case, R, wx, leaf_ops):
     pts, q, p, k, s = CASES[case]()
     tb = tables(p, k)
     ref = oracle.Plan(pts, s, tb["n"] if wx < 0 else wx).matvec(tb, q)
-    plans = group(pts, p, k, s, R, tb, wx)
+    plans = group(pts, p, k, s, R, tb, wx, leaf_ops)
     # the ranges tile [0, N) and every rank got work (these trees have >= 5 leaves per rank)
     rng = [pl.owned_range for pl in plans]
     assert rng[0][0] == 0 and rng[-1][1] == q.size
@@ -104,7 +104,8 @@ def test_loopback_group_parity(case, R, wx):
     for pt in pots:
         assert rel(pt.cpu().numpy(), ref) <= TOL
     # and the partitioned result is the single-GPU result up to summation order
-    one = K().Plan(torch.from_numpy(pts).cuda(), None, p=p, k=k, leaf_size=s, wx_direct_max=wx, tables=tb)
+    one = K().Plan(torch.from_numpy(pts).cuda(), None, p=p, k=k, leaf_size=s, wx_direct_max=wx, tables=tb,
+                   leaf_ops=leaf_ops)
     assert rel(out, one.matvec(Q).cpu().numpy()) <= 1e-13
 
 

@@ -83,16 +83,19 @@ def test_tree_and_lists_bit_exact(case):
 
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("wx", [-1, 0])
-def test_matvec_parity_shared_tables(case, wx):
+@pytest.mark.parametrize("leaf_ops", [0, 1])
+def test_matvec_parity_shared_tables(case, wx, leaf_ops):
     pts, q, p, k, s = CASES[case]()
     tb = tables(p, k)
     op = oracle.Plan(pts, s, tb["n"] if wx < 0 else wx)
     ref, ph = op.matvec(tb, q, phases=True)
-    # fused production path
-    out = gpu_plan(pts, p, k, s, wx=wx, tb=tb).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    # fused production path (leaf_ops = 1: S2M / L2T through the per-leaf operators)
+    gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb, leaf_ops=leaf_ops)
+    assert (gp.info["leaf_op_bytes"] > 0) == bool(leaf_ops)
+    out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
     assert rel(out, ref) <= TOL
     # split near / far passes (phase exports)
-    gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb, split_phases=True)
+    gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb, split_phases=True, leaf_ops=leaf_ops)
     out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
     assert rel(out, ref) <= TOL
     # per-phase parity localises failures.  q^' and l^ are intermediate: S' = U^T pinv(E_u)
@@ -109,13 +112,14 @@ def test_matvec_parity_shared_tables(case, wx):
         assert rel(gp.export_phase("far"), ph["far"]) <= TOL
 
 
-def test_c2_full_size_parity():
+@pytest.mark.parametrize("leaf_ops", [0, 1])
+def test_c2_full_size_parity(leaf_ops):
     # BASELINE configs[1] at full size, in the launch configuration bench.py times
     pts, q, cfg = synth_inputs.make("C2")
     tb = tables(cfg["p"], cfg["k"])
     op = oracle.Plan(pts, cfg["leaf"], tb["n"])
     ref = op.matvec(tb, q)
-    gp = gpu_plan(pts, cfg["p"], cfg["k"], cfg["leaf"], tb=tb)
+    gp = gpu_plan(pts, cfg["p"], cfg["k"], cfg["leaf"], tb=tb, leaf_ops=leaf_ops)
     out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
     assert gp.info["nlevels"] == 6 and gp.info["nleaves"] == 32768
     assert rel(out, ref) <= TOL
