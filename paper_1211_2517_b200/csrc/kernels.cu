@@ -357,6 +357,159 @@ __global__ void __launch_bounds__(KP * 4, MINB) k_m2l_sib(const int4* __restrict
 }
 
 // ----------------------------------------------------------------------------
+// k_m2l_sib16: k_m2l_sib with the m16n8k8 FP64 MMA (kp = 32, 64): each B fragment
+// serves two 8-row halves, halving the shared-memory loads per DMMA.  8 warps;
+// warp w owns rows 16 (w % RB) .. +16 and columns (w / RB) * NCW .. +NCW of a tile.
+// Same tile scheduler, metadata ring and cp.async B pipeline as k_m2l_sib.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4], double b0, double b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b0), "d"(b1));
+}
+
+template <int KP, int NT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_m2l_sib16(const int4* __restrict__ tiles, int ntiles,
+                                                       const int* __restrict__ cols, const int* __restrict__ classes,
+                                                       const double* __restrict__ C, int mvalid, const double* X,
+                                                       double* Y, int* __restrict__ counter) {
+  constexpr int NW = 8;
+  constexpr int NTH = NW * 32;
+  constexpr int SB = KP + 4;
+  constexpr int K2 = KP / 2;
+  constexpr int CW = 9;
+  constexpr int RB = KP / 16;        // row blocks of 16
+  constexpr int CS = NW / RB;        // column groups
+  constexpr int NCW = NT / CS;       // columns per warp
+  constexpr int NB = NCW / 8;        // n-blocks per warp
+  constexpr int KS8 = KP / 8;        // k8-steps
+  constexpr int CH = 2;              // k8-steps per A chunk
+  constexpr int NCH = KS8 / CH;
+  static_assert(KS8 % CH == 0 && NB >= 1, "tile shape");
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_meta[3][NT * CW];
+  __shared__ int s_tile[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp % RB) * 16;
+  const int cbase = (warp / RB) * NCW;
+  int ti = blockIdx.x;
+  if (ti >= ntiles) return;
+
+  auto fetch_meta = [&](int tid, int slot) {
+    const int4 tl = tiles[tid];
+    for (int e = threadIdx.x; e < NT * CW; e += NTH) {
+      const int c = e / CW;
+      s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
+    }
+  };
+  auto gather = [&](int slot, int b, int buf) {
+    double* Bd = sm + buf * NT * SB;
+    for (int p = warp; p < NT; p += NW) {
+      const int src = s_meta[slot][p * CW + 1 + b];
+      for (int c = lane; c < K2; c += 32) {
+        double* dst = Bd + p * SB + 2 * c;
+        if (src >= 0) cp_async16(dst, X + (size_t)src * KP + 2 * c);
+        else { dst[0] = 0.0; dst[1] = 0.0; }
+      }
+    }
+  };
+  // A fragment of k8-step ks: rows r0+g, r0+g+8; columns 8 ks + t, 8 ks + t + 4
+  auto op_rows = [&](int id) { return C + (size_t)id * KP * KP + (size_t)(r0 + g) * KP + t; };
+  auto load_a = [&](const double* Ar, int ks, double (&a)[4]) {
+    a[0] = __ldg(Ar + 8 * ks);
+    a[1] = __ldg(Ar + 8 * KP + 8 * ks);
+    a[2] = __ldg(Ar + 8 * ks + 4);
+    a[3] = __ldg(Ar + 8 * KP + 8 * ks + 4);
+  };
+
+  int slot = 0;
+  fetch_meta(ti, 0);
+  if (threadIdx.x == 0) s_tile[1] = gridDim.x + atomicAdd(counter, 1);
+  __syncthreads();
+  const int* cls = classes + tiles[ti].x * 17;
+  gather(0, cls[1], 0);
+  cp_async_commit();
+  double a_cur[CH][4];
+  const double* Aop = op_rows(cls[9]);
+#pragma unroll
+  for (int s = 0; s < CH; ++s) load_a(Aop, s, a_cur[s]);
+  int buf = 0;
+  double acc[NB][4];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+
+  while (true) {
+    const int nv = cls[0];
+    const int nslot = slot == 2 ? 0 : slot + 1;
+    const int tnext = s_tile[nslot];
+    for (int jb = 0; jb < nv; ++jb) {
+      const bool last = jb + 1 == nv;
+      if (jb == 0 && tnext < ntiles) {
+        fetch_meta(tnext, nslot);
+        if (threadIdx.x == 0) s_tile[nslot == 2 ? 0 : nslot + 1] = gridDim.x + atomicAdd(counter, 1);
+      }
+      cp_async_wait0();
+      __syncthreads();
+      const double* Anext = nullptr;
+      if (!last) {
+        gather(slot, cls[2 + jb], buf ^ 1);
+        Anext = op_rows(cls[9 + jb + 1]);
+      } else if (tnext < ntiles) {
+        const int* ncls = classes + tiles[tnext].x * 17;
+        gather(nslot, ncls[1], buf ^ 1);
+        Anext = op_rows(ncls[9]);
+      }
+      cp_async_commit();
+      // B fragment (k8-step ks, n-block j): b0 = B[8ks + t][col], b1 = B[8ks + t + 4][col], col = cbase + 8j + g
+      const double* B = sm + buf * NT * SB + (size_t)(cbase + g) * SB + t;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        double a_nxt[CH][4];
+        const bool more = c + 1 < NCH;
+        if (more || Anext) {
+#pragma unroll
+          for (int s = 0; s < CH; ++s) load_a(more ? Aop : Anext, more ? (c + 1) * CH + s : s, a_nxt[s]);
+        }
+#pragma unroll
+        for (int s = 0; s < CH; ++s) {
+          const int ks = c * CH + s;
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            const double* bp = B + (size_t)j * 8 * SB + 8 * ks;
+            dmma_16x8x8(acc[j], a_cur[s], bp[0], bp[4]);
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < CH; ++s)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a_cur[s][e] = a_nxt[s][e];
+      }
+      Aop = Anext;
+      buf ^= 1;
+      if (last) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int tg = s_meta[slot][(cbase + j * 8 + 2 * t + c) * CW];
+            if (tg >= 0) {
+              if (r0 + g < mvalid) atomicAdd(Y + (size_t)tg * KP + r0 + g, acc[j][c]);
+              if (r0 + g + 8 < mvalid) atomicAdd(Y + (size_t)tg * KP + r0 + g + 8, acc[j][2 + c]);
+            }
+          }
+          acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+        }
+      }
+    }
+    if (tnext >= ntiles) break;
+    ti = tnext;
+    slot = nslot;
+    cls = classes + tiles[ti].x * 17;
+  }
+}
+
+// ----------------------------------------------------------------------------
 // k_eval: one CTA per target item.  Targets are either the points of a box
 // (SURF_TGT = false; result stored to out[pbeg + i]) or the n surface points
 // c_B + rad * e_i of a box (SURF_TGT = true; result stored to out[row * ldo + i]).
@@ -842,9 +995,34 @@ static int sib_minb() {
   return v;
 }
 
+template <int KP, int MINB>
+int launch_sib16(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
+  constexpr int NT = sq_nt(KP);
+  const size_t smem = (size_t)NT * 2 * (KP + 4) * sizeof(double);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_sib16<KP, NT, MINB>, 256, smem);
+  const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
+  KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
+  k_m2l_sib16<KP, NT, MINB><<<grid, 256, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y,
+                                                     g.d_counter);
+  return 0;
+}
+
+static int sib16() {
+  static int v = [] { const char* e = std::getenv("KIFMM_SIB16"); return e ? std::atoi(e) : 1; }();
+  return v;
+}
+
 int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, const double* X, double* Y, cudaStream_t st) {
   if (g.ntiles == 0) return 0;
   ++g_launches;
+  if (sib16() && (kp == 32 || kp == 64)) {
+    if (kp == 32) launch_sib16<32, 3>(g, C, mvalid, X, Y, st);
+    else if (sib_minb() == 3) launch_sib16<64, 3>(g, C, mvalid, X, Y, st);
+    else launch_sib16<64, 2>(g, C, mvalid, X, Y, st);
+    KIFMM_CUDA(cudaGetLastError());
+    return 0;
+  }
   if (kp == 32) { if (sib_minb() == 3) launch_sib<32, 3>(g, C, mvalid, X, Y, st); else launch_sib<32, 1>(g, C, mvalid, X, Y, st); }
   else if (kp == 64) { if (sib_minb() == 3) launch_sib<64, 3>(g, C, mvalid, X, Y, st); else launch_sib<64, 1>(g, C, mvalid, X, Y, st); }
   else launch_sib<104, 1>(g, C, mvalid, X, Y, st);
@@ -888,6 +1066,9 @@ int kernels_init() {
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<32, sq_nt(32), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
 }
