@@ -3,6 +3,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -143,6 +144,7 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   P.profile = opt->profile != 0;
   P.split_phases = opt->split_phases != 0;
   P.leaf_ops_opt = opt->leaf_ops;
+  if (const char* e = std::getenv("KIFMM_SYM")) P.sym_opt = std::atoi(e);  // diagnostics: 0 = one-sided near field
   P.dist.nranks = opt->nranks;
   P.dist.rank = opt->rank;
   auto fail = [&](int rc) { free_plan_memory(h); delete h; return rc; };

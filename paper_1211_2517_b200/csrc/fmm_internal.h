@@ -154,6 +154,8 @@ struct Plan {
   // evaluation work lists (k_eval items: (box, out row, 0, 0); CSR of segments (kind, a, b, len))
   int np = 0;                                  // n rounded up to a multiple of 8
   int n_tleaf = 0; int4* d_tleaf_items = nullptr;
+  int n_sym = 0; int2* d_sym = nullptr;   // symmetric near-field leaf pairs (both owned), k_p2p_sym
+  int sym_opt = -1;                        // -1 / 1 on, 0 off (all near pairs one-sided)
   int* d_near_off = nullptr; int4* d_near_seg = nullptr; int n_near_seg = 0;
   int* d_far_off = nullptr;  int4* d_far_seg = nullptr;  int n_far_seg = 0;
   int* d_all_off = nullptr;  int4* d_all_seg = nullptr;  // near + far segments (fused pass)

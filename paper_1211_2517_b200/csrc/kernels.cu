@@ -684,6 +684,105 @@ __device__ __forceinline__ void eval_pass(const EvalArgs& A, const int4& it, int
   }
 }
 
+// ----------------------------------------------------------------------------
+// k_p2p_sym: symmetric near field.  G is symmetric, so an unordered pair of
+// leaves {B, A} (a U pair, or a direct W / X pair whose source is a leaf) is
+// evaluated ONCE for both directions:  p_i += sum_j G_ij q_j (i in B) and
+// p_j += sum_i G_ij q_i (j in A), i.e. ~13 FP64 ops per pair instead of 24.
+// One warp per pair.  Lane l holds TB targets of B (l + 32 u); A's points stream
+// through a per-warp shared buffer 32 at a time; lane l accumulates, for each of
+// the 32 sources j, s_j = sum_u q_u G(x_u, y_j), and a butterfly reduce-scatter
+// across the warp leaves sum_l s_j on lane j (31 shuffles per 32 x 32 TB pairs).
+// Both sides are added to the potential with RED (the pair's leaves also receive
+// other contributions).  Distinct leaves never share a point position.
+// ----------------------------------------------------------------------------
+constexpr int SYM_WARPS = 4;
+constexpr int SYM_SB = 16;    // sources per batch (partial sums per lane)
+constexpr int SYM_CH = 256;   // source points staged per warp
+
+// targets pts[tb0, tb0 + mt) (TB per lane) against the staged sources sbuf[0, cn)
+// (global index sb0 + j); both sides' sums go to pot with RED
+template <int TB>
+__device__ __forceinline__ void p2p_sym_pass(const double4* __restrict__ pts, int tb0, int mt, int sb0, int cn,
+                                             const double4* sbuf, double* __restrict__ pot) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double x[TB][3], q[TB], acc[TB];
+#pragma unroll
+  for (int u = 0; u < TB; ++u) {
+    const int i = lane + 32 * u;
+    acc[u] = 0.0;
+    if (i < mt) {
+      const double4 p = pts[tb0 + i];
+      x[u][0] = p.x; x[u][1] = p.y; x[u][2] = p.z; q[u] = p.w;
+    } else {
+      x[u][0] = 1e100; x[u][1] = 0.0; x[u][2] = 0.0; q[u] = 0.0;
+    }
+  }
+  for (int j0 = 0; j0 < cn; j0 += SYM_SB) {
+    double v[SYM_SB];
+#pragma unroll
+    for (int j = 0; j < SYM_SB; ++j) {
+      const double4 sv = sbuf[j0 + j];
+      double sj = 0.0;
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+        const double r = rinv_nonzero(fma(dz, dz, fma(dy, dy, dx * dx)));
+        acc[u] = fma(sv.w, r, acc[u]);
+        sj = fma(q[u], r, sj);
+      }
+      v[j] = sj;
+    }
+    // reduce-scatter within each 16-lane half, then fold the halves: lane l ends with
+    // the sum over all lanes of the original v[l % 16]
+#pragma unroll
+    for (int off = SYM_SB / 2; off >= 1; off >>= 1) {
+      const bool up = lane & off;
+#pragma unroll
+      for (int i = 0; i < off; ++i) {
+        const double send = up ? v[i] : v[i + off];
+        const double keep = up ? v[i + off] : v[i];
+        v[i] = keep + __shfl_xor_sync(FULL, send, off);
+      }
+    }
+    v[0] += __shfl_xor_sync(FULL, v[0], 16);
+    if (lane < SYM_SB && j0 + lane < cn) atomicAdd(pot + sb0 + j0 + lane, v[0] * kInv4Pi);
+  }
+#pragma unroll
+  for (int u = 0; u < TB; ++u) {
+    const int i = lane + 32 * u;
+    if (i < mt) atomicAdd(pot + tb0 + i, acc[u] * kInv4Pi);
+  }
+}
+
+__global__ void __launch_bounds__(SYM_WARPS * 32, 6) k_p2p_sym(const int2* __restrict__ pairs, int npairs,
+                                                              const double4* __restrict__ pts,
+                                                              const int* __restrict__ pbeg, const int* __restrict__ pend,
+                                                              double* __restrict__ pot) {
+  __shared__ __align__(16) double4 sbuf[SYM_WARPS][SYM_CH];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pi = blockIdx.x * SYM_WARPS + w;
+  if (pi >= npairs) return;
+  const int2 pr = pairs[pi];
+  const int tb0 = pbeg[pr.x], mt_all = pend[pr.x] - tb0;
+  const int sb0 = pbeg[pr.y], ms = pend[pr.y] - sb0;
+  for (int c0 = 0; c0 < ms; c0 += SYM_CH) {
+    const int cn = min(SYM_CH, ms - c0);
+    const int cpad = (cn + SYM_SB - 1) / SYM_SB * SYM_SB;
+    __syncwarp();
+    for (int j = lane; j < cpad; j += 32)  // padding sources: zero density, far away
+      sbuf[w][j] = j < cn ? pts[sb0 + c0 + j] : make_double4(-1e100, 0.0, 0.0, 0.0);
+    __syncwarp();
+    for (int t0 = 0; t0 < mt_all; t0 += 96) {
+      const int mt = min(96, mt_all - t0);
+      if (mt > 64) p2p_sym_pass<3>(pts, tb0 + t0, mt, sb0 + c0, cn, sbuf[w], pot);
+      else if (mt > 32) p2p_sym_pass<2>(pts, tb0 + t0, mt, sb0 + c0, cn, sbuf[w], pot);
+      else p2p_sym_pass<1>(pts, tb0 + t0, mt, sb0 + c0, cn, sbuf[w], pot);
+    }
+  }
+}
+
 // k_eval: one CTA per target leaf (item (box, row, 0, 0)): potentials of the leaf's
 // points from its source segments (kind, a, b, len):
 //   kind 0: points pts[a .. a+len)                       (P2P: U, direct W / X)
@@ -1084,6 +1183,15 @@ static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st
   else k_eval<128, 256><<<P.n_tleaf, 128, 0, st>>>(a, chk_self);
 }
 
+static int launch_sym(const Plan& P, cudaStream_t st) {
+  if (P.n_sym == 0) return 0;
+  ++g_launches;
+  k_p2p_sym<<<(P.n_sym + SYM_WARPS - 1) / SYM_WARPS, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts,
+                                                                            P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
+}
+
 // check points per lane: one round of 32*TB when n <= 160, else rounds of 32*ceil(n/64)
 void launch_chk(const EvalArgs& a, int nitems, int n, cudaStream_t st) {
   const int tb = n <= 160 ? (n + 31) / 32 : (n + 63) / 64;
@@ -1210,6 +1318,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         launch_eval(P, a, 1, st);
         ++g_launches;
         KIFMM_CUDA(cudaGetLastError());
+        if (launch_sym(P, st)) return -3;
       }
       // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
       if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
@@ -1234,6 +1343,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         ++g_launches;
         KIFMM_CUDA(cudaGetLastError());
       }
+      if (!P.split_phases && launch_sym(P, st)) return -3;
       mark(8);
       if (owned) {
         const int cnt = Dp.own_hi - Dp.own_lo;

@@ -129,14 +129,47 @@ int build_schedules(Plan& P, cudaStream_t st) {
     const int b = titems[i].x;
     near[i].push_back(make_int4(0, T.pbeg[b], 0, npts(b)));
   }
-  for (auto& u : U)
-    if (inD(u.x) && u.y != u.x) near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
+  // symmetric pairs (k_p2p_sym): U pairs and direct W pairs with a leaf source (whose
+  // mirror is the direct X pair), both leaves owned; evaluated once for both sides
+  // A pair goes symmetric when k_p2p_sym's padding (targets in passes of 32 TB lanes,
+  // sources in batches of 16) wastes little: its cost per useful pair is then ~13 FP64
+  // ops for both directions against 2 x 12 one-sided (measured: a win for C5's
+  // 88-point leaves, a loss for C2/C4's ~33-point ones without this filter).
+  const bool sym = P.sym_opt != 0;
+  static const double sym_r = [] { const char* e = std::getenv("KIFMM_SYM_R"); return e ? std::atof(e) : 1.4; }();
+  auto pass_slots = [](int m) { int full = m / 96, rem = m - 96 * full; return 96 * full + 32 * ((rem + 31) / 32); };
+  auto pad_ratio = [&](int mt, int ms) {
+    return (double)pass_slots(mt) / mt * (double)((ms + 15) / 16 * 16) / ms;
+  };
+  // returns 0: one-sided, 1: symmetric with (a, b), 2: symmetric with (b, a)
+  auto sym_choice = [&](int a, int b) {
+    if (!sym || !inD(a) || !inD(b)) return 0;
+    const double r1 = pad_ratio(npts(a), npts(b)), r2 = pad_ratio(npts(b), npts(a));
+    if (std::min(r1, r2) > sym_r) return 0;
+    return r1 <= r2 ? 1 : 2;
+  };
+  std::vector<int2> sympairs;
+  auto add_sym = [&](int a, int b, int c) { sympairs.push_back(c == 1 ? make_int2(a, b) : make_int2(b, a)); };
+  for (auto& u : U) {
+    if (!inD(u.x) || u.y == u.x) continue;
+    if (int c = sym_choice(u.x, u.y)) {
+      if (u.x < u.y) add_sym(u.x, u.y, c);
+      continue;
+    }
+    near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
+  }
   // W pairs: direct -> P2P over the source subtree; else M2T through the source's equivalent density
   std::vector<PairGroup> wgroups;  // grouped by source level (scale r_A)
   std::map<int, int> wlevel;
   int n_wnd = 0;
   for (auto& w : W) {
     if (!inD(w.x)) continue;
+    if (w.z && T.leaf[w.y]) {
+      if (int c = sym_choice(w.x, w.y)) {
+        add_sym(w.x, w.y, c);
+        continue;
+      }
+    }
     if (w.z) {
       near[leaf_row[w.x]].push_back(make_int4(0, T.pbeg[w.y], 0, npts(w.y)));
     } else {
@@ -153,6 +186,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   std::vector<PairGroup> xgroup{PairGroup{0, 1.0, {}}};
   for (auto& x : X) {
     if (!inD(x.x)) continue;
+    if (x.z && sym_choice(x.x, x.y)) continue;  // mirror of a symmetric W pair
     if (x.z) {
       near[leaf_row[x.x]].push_back(make_int4(0, T.pbeg[x.y], 0, npts(x.y)));
     } else {
@@ -188,6 +222,12 @@ int build_schedules(Plan& P, cudaStream_t st) {
     all_off.push_back((int)all_seg.size());
   }
   P.n_tleaf = nt;
+  // costliest pairs first (one warp each)
+  std::stable_sort(sympairs.begin(), sympairs.end(), [&](const int2& a, const int2& b) {
+    return (int64_t)npts(a.x) * npts(a.y) > (int64_t)npts(b.x) * npts(b.y);
+  });
+  P.n_sym = (int)sympairs.size();
+  if (upload(P, &P.d_sym, sympairs, st)) return -3;
 
   P.n_near_seg = (int)near_seg.size();
   P.n_far_seg = (int)far_seg.size();
