@@ -83,10 +83,10 @@ typedef struct {
   int nranks;         /* default 1 */
   int rank;           /* 0 <= rank < nranks */
   const void* nccl_id;
-  int leaf_ops;       /* per-leaf S2M / L2T operators built at setup (2 x owned points x kp
-                         doubles): a matvec then streams them from HBM instead of evaluating
-                         2n kernel values per point.  -1 (default): when they fit in 40% of the
-                         free device memory; 0 off; 1 on. */
+  int leaf_ops;       /* per-leaf S2M and L2T operators built at setup (owned points x kp
+                         doubles each): a matvec then streams them from HBM instead of
+                         evaluating n kernel values per point and operator.  -1 (default): each
+                         while max(16 GB, 25% of the device) stays free; 0 off; 1 on. */
 } fmm_options;
 
 typedef struct {

@@ -164,7 +164,7 @@ struct Plan {
   // (point-major rows of kp), L2T  pot_B = T_B l^_B  with T_B = r_l G(x_B, DE_B) T'
   // (kp-major within a leaf block); both indexed by sorted point - own_lo
   int leaf_ops_opt = -1;      // -1 auto, 0 off, 1 on
-  bool leaf_ops = false;
+  bool leaf_s2m = false, leaf_l2t = false;  // which of the two operators are used
   double* d_s2m_mat = nullptr;
   double* d_l2t_mat = nullptr;
   int64_t leaf_op_bytes = 0;

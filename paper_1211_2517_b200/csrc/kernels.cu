@@ -1136,12 +1136,16 @@ int build_leaf_ops(Plan& P, cudaStream_t st) {
   KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const double f = 3.0 - 2.0 * P.d;  // UC and DE halfwidth factor
-  k_leafop_build<0><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
-                                                P.kp, f, P.d_S, P.np, 1, P.dist.own_lo, P.d_s2m_mat);
-  KIFMM_CUDA(cudaGetLastError());
-  k_leafop_build<1><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
-                                                P.kp, f, P.d_T, 1, P.kp, P.dist.own_lo, P.d_l2t_mat);
-  KIFMM_CUDA(cudaGetLastError());
+  if (P.leaf_s2m) {
+    k_leafop_build<0><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
+                                                  P.kp, f, P.d_S, P.np, 1, P.dist.own_lo, P.d_s2m_mat);
+    KIFMM_CUDA(cudaGetLastError());
+  }
+  if (P.leaf_l2t) {
+    k_leafop_build<1><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
+                                                  P.kp, f, P.d_T, 1, P.kp, P.dist.own_lo, P.d_l2t_mat);
+    KIFMM_CUDA(cudaGetLastError());
+  }
   return 0;
 }
 
@@ -1261,7 +1265,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       mark(1);
-      if (P.leaf_ops) {  // S2M as one GEMV per leaf with its precomputed operator
+      if (P.leaf_s2m) {  // S2M as one GEMV per leaf with its precomputed operator
         if (P.n_s2m > 0) {
           ++g_launches;
           k_s2m_leafop<<<(P.n_s2m + 7) / 8, 256, 0, st>>>(P.d_s2m_items, P.n_s2m, T.d_pts, T.d_pbeg, T.d_pend,
@@ -1277,7 +1281,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaGetLastError());
       }
       // S2M stage 2: q^'_B = S' c  (store)
-      if (!P.leaf_ops && launch_ggs(P.g_s2m, P.d_S, 0, kp, np, k, P.d_chk_s2m, np, P.d_qhat, kp, false, st)) return -3;
+      if (!P.leaf_s2m && launch_ggs(P.g_s2m, P.d_S, 0, kp, np, k, P.d_chk_s2m, np, P.d_qhat, kp, false, st)) return -3;
       mark(2);
       // M2M, finest child level first: q^'_P += 1/2 M~_o q^'_c
       for (auto& g : P.g_m2m)
@@ -1324,7 +1328,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
       if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
       // leaf-op mode: L2T as one GEMV per leaf, stored; the evaluation pass below adds to it
-      if (P.leaf_ops && P.n_tleaf > 0) {
+      if (P.leaf_l2t && P.n_tleaf > 0) {
         ++g_launches;
         k_l2t_leafop<<<(P.n_tleaf + L2T_WARPS - 1) / L2T_WARPS, L2T_WARPS * 32, 0, st>>>(
             P.d_tleaf_items, P.n_tleaf, T.d_level, T.d_pbeg, T.d_pend, P.d_l2t_mat, P.d_lhat, kp, Dp.own_lo,
@@ -1335,7 +1339,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       if (P.n_tleaf > 0) {
         EvalArgs a = ea;
         a.items = P.d_tleaf_items;
-        a.accumulate = P.leaf_ops ? 1 : 0;
+        a.accumulate = P.leaf_l2t ? 1 : 0;
         if (P.split_phases) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far; }
         else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; a.out = P.d_pot_near; }
         a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;

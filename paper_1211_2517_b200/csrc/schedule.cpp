@@ -106,13 +106,16 @@ int build_schedules(Plan& P, cudaStream_t st) {
   }
   const DistPlan& Dp = P.dist;
   auto inD = [&](int b) { return Dp.inD[b] != 0; };
-  // per-leaf S2M / L2T operators (2 x owned points x kp doubles): on request, or
-  // automatically when they take at most 40% of the free device memory
+  // per-leaf S2M / L2T operators (owned points x kp doubles each): on request, or
+  // automatically while they leave max(16 GB, 25% of the device) free (S2M first)
   {
-    const double bytes = 2.0 * (Dp.own_hi - Dp.own_lo) * kp * sizeof(double);
+    const double one = (double)(Dp.own_hi - Dp.own_lo) * kp * sizeof(double);
     size_t fr = 0, tot = 0;
     KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
-    P.leaf_ops = P.leaf_ops_opt > 0 || (P.leaf_ops_opt < 0 && bytes <= 0.4 * (double)fr);
+    const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot);
+    const bool on = P.leaf_ops_opt > 0, au = P.leaf_ops_opt < 0;
+    P.leaf_s2m = on || (au && one <= budget);
+    P.leaf_l2t = on || (au && one * (P.leaf_s2m ? 2 : 1) <= budget);
   }
 
   // ---- target leaves (owned), near (P2P) and far (L2T + W) segment CSRs
@@ -203,7 +206,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   int n_l2t = 0;
   for (int i = 0; i < nt; ++i) {
     int b = titems[i].x;
-    if (T.level[b] < 2 || P.leaf_ops) continue;  // leaf-op mode: L2T is a GEMV with the leaf's operator
+    if (T.level[b] < 2 || P.leaf_l2t) continue;  // L2T as a GEMV with the leaf's operator
     int lv = T.level[b];
     if (!llevel.count(lv)) { llevel[lv] = (int)lgroups.size(); lgroups.push_back(PairGroup{0, rl(b), {}}); }
     lgroups[llevel[lv]].pairs.push_back(make_int2(b, n_l2t));
@@ -398,7 +401,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     return 0;
   };
   if (zalloc(&P.d_qhat, (size_t)nb * kp) || zalloc(&P.d_lhat, (size_t)nb * kp) ||
-      zalloc(&P.d_chk_s2m, P.leaf_ops ? 1 : (size_t)P.n_s2m * np) || zalloc(&P.d_chk_x, (size_t)P.n_xnd * np) ||
+      zalloc(&P.d_chk_s2m, P.leaf_s2m ? 1 : (size_t)P.n_s2m * np) || zalloc(&P.d_chk_x, (size_t)P.n_xnd * np) ||
       zalloc(&P.d_eqd_l2t, (size_t)n_l2t * np) || zalloc(&P.d_eqd_w, (size_t)n_wnd * np) ||
       zalloc(&P.d_pot_near, T.N) || zalloc(&P.d_pot_far, T.N) || zalloc(&P.d_io, 2 * T.N))
     return -3;
@@ -422,10 +425,11 @@ int build_schedules(Plan& P, cudaStream_t st) {
     std::vector<int> sl = Dp.nranks > 1 ? Dp.straddle : std::vector<int>();
     if (upload(P, &P.d_straddle, sl, st) || zalloc(&P.d_straddle_buf, (size_t)P.n_straddle * kp)) return -3;
   }
-  if (P.leaf_ops) {
+  if (P.leaf_s2m || P.leaf_l2t) {
     const size_t cnt = (size_t)(Dp.own_hi - Dp.own_lo) * kp;
-    if (zalloc(&P.d_s2m_mat, cnt) || zalloc(&P.d_l2t_mat, cnt)) return -3;
-    P.leaf_op_bytes = 2 * cnt * sizeof(double);
+    if (P.leaf_s2m && zalloc(&P.d_s2m_mat, cnt)) return -3;
+    if (P.leaf_l2t && zalloc(&P.d_l2t_mat, cnt)) return -3;
+    P.leaf_op_bytes = (int64_t)((P.leaf_s2m ? 1 : 0) + (P.leaf_l2t ? 1 : 0)) * cnt * sizeof(double);
     if (build_leaf_ops(P, st)) return -3;
   }
   KIFMM_CUDA(cudaStreamSynchronize(st));
