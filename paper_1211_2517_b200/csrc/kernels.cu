@@ -1124,7 +1124,11 @@ int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, cons
   }
   if (kp == 32) { if (sib_minb() == 3) launch_sib<32, 3>(g, C, mvalid, X, Y, st); else launch_sib<32, 1>(g, C, mvalid, X, Y, st); }
   else if (kp == 64) { if (sib_minb() == 3) launch_sib<64, 3>(g, C, mvalid, X, Y, st); else launch_sib<64, 1>(g, C, mvalid, X, Y, st); }
-  else launch_sib<104, 1>(g, C, mvalid, X, Y, st);
+  else {
+    static const int m104 = [] { const char* e = std::getenv("KIFMM_SIB104_MINB"); return e ? std::atoi(e) : 2; }();
+    if (m104 == 2) launch_sib<104, 2>(g, C, mvalid, X, Y, st);
+    else launch_sib<104, 1>(g, C, mvalid, X, Y, st);
+  }
   KIFMM_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1169,6 +1173,7 @@ int kernels_init() {
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<32, sq_nt(32), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

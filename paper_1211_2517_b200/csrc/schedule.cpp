@@ -275,9 +275,18 @@ int build_schedules(Plan& P, cudaStream_t st) {
         out[2] |= (int)((k >> (3 * bit)) & 1) << bit;
       }
     };
-    // class table: class = didx * 8 + a; record = nvalid, b[8], offset id[8]
-    std::vector<int> classes(26 * 8 * 17, -1);
-    std::vector<int> nvalid(26 * 8, 0);
+    // class table: class = didx * 8 + a; record = nvalid, b[8], offset id[8].  Classes
+    // 208 + o are one-operator pseudo-classes (C_o) carrying the pairs of sparse sibling
+    // groups through the same kernel (column: target, src, -1 x 7)
+    constexpr int kSib = 26 * 8, kCls = kSib + kNumOffsets;
+    std::vector<int> classes(kCls * 17, -1);
+    std::vector<int> nvalid(kCls, 0);
+    for (int o = 0; o < kNumOffsets; ++o) {
+      int* rec = &classes[(kSib + o) * 17];
+      rec[0] = 1; rec[1] = 0; rec[9] = o;
+      nvalid[kSib + o] = 1;
+    }
+    static const bool sparse_in_sib = [] { const char* e = std::getenv("KIFMM_M2L_SPARSE_SIB"); return !e || std::atoi(e) != 0; }();
     for (int lin = 0; lin < 27; ++lin) {
       if (lin == 13) continue;
       const int didx = lin < 13 ? lin : lin - 1;
@@ -314,7 +323,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
       std::vector<int> fill(vcnt.begin(), vcnt.end() - 1);
       for (auto& v : V) vby[fill[v.x]++] = v;
     }
-    std::vector<std::vector<int>> cls_cols(26 * 8);  // column records (9 ints) per class
+    std::vector<std::vector<int>> cls_cols(kCls);  // column records (9 ints) per class
     std::vector<PairGroup> groups(kNumOffsets);
     for (int o = 0; o < kNumOffsets; ++o) groups[o] = PairGroup{o, 1.0, {}};
     int ap[3], aq[3];
@@ -348,7 +357,16 @@ int build_schedules(Plan& P, cudaStream_t st) {
           for (int j = 0; j < 8; ++j) cc.push_back(src[j]);
         } else {
           for (int e = e0; e < e1; ++e)
-            if (T.parent[vby[e].y] == qs[i]) groups[vby[e].z].pairs.push_back(make_int2(vby[e].y, b));
+            if (T.parent[vby[e].y] == qs[i]) {
+              if (sparse_in_sib) {
+                auto& cc = cls_cols[kSib + vby[e].z];
+                cc.push_back(b);
+                cc.push_back(vby[e].y);
+                for (int j = 1; j < 8; ++j) cc.push_back(-1);
+              } else {
+                groups[vby[e].z].pairs.push_back(make_int2(vby[e].y, b));
+              }
+            }
         }
       }
     }
@@ -357,7 +375,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     const int NTs = sib_tile_width(kp);
     std::vector<int> cols;
     std::vector<int4> tiles;
-    for (int cls = 0; cls < 26 * 8; ++cls) {
+    for (int cls = 0; cls < kCls; ++cls) {
       const auto& cc = cls_cols[cls];
       const int ncol = (int)cc.size() / 9;
       const int base = (int)cols.size() / 9;
