@@ -181,6 +181,7 @@ struct Plan {
   // timing of the last matvec (ms per phase), filled when profiling is on
   std::vector<float> phase_ms;
   cudaStream_t stream = nullptr;
+  bool overlap = false;               // near field on stream_near, concurrent with the far field
   cudaStream_t stream_near = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_phase;

@@ -1006,6 +1006,11 @@ __global__ void k_owned_output(const double* __restrict__ pnear, const double* _
   if (i < cnt) pot[i] = pfar ? pnear[lo + i] + pfar[lo + i] : pnear[lo + i];
 }
 
+__global__ void k_combine(double* __restrict__ pnear, const double* __restrict__ pfar, int lo, int cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) pnear[lo + i] += pfar[lo + i];
+}
+
 // exchange packing: buf[i][c] = src[idx[i] * ld + c] (c < row), and the inverse store
 __global__ void k_pack_rows(const double* __restrict__ src, int ld, const int* __restrict__ idx, int nrows, int row,
                             double* __restrict__ buf) {
@@ -1192,6 +1197,20 @@ static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st
   else k_eval<128, 256><<<P.n_tleaf, 128, 0, st>>>(a, chk_self);
 }
 
+static int launch_sym(const Plan& P, cudaStream_t st);
+
+// near field into pot_near: one-sided segments (own leaf first, U, direct W/X) + symmetric pairs
+static int launch_near(const Plan& P, const EvalArgs& ea, cudaStream_t st) {
+  if (P.n_tleaf > 0) {
+    EvalArgs a = ea;
+    a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
+    launch_eval(P, a, 1, st);
+    ++g_launches;
+    KIFMM_CUDA(cudaGetLastError());
+  }
+  return launch_sym(P, st);
+}
+
 static int launch_sym(const Plan& P, cudaStream_t st) {
   if (P.n_sym == 0) return 0;
   ++g_launches;
@@ -1267,6 +1286,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
     }
     case 1: {  // upward pass (partial multipoles of straddling boxes)
       if (owned && unpack(pts_w, 4, P.xd.d_recv_idx, P.xd.nrecv, 1, P.xd.d_recv, st)) return -3;
+      if (P.overlap) {  // near field on its own stream, concurrent with the far field
+        KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
+        if (launch_near(P, ea, P.stream_near)) return -3;
+        KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
+      }
       KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       mark(1);
@@ -1321,38 +1346,44 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (launch_ggs(g, P.d_L, kp * kp, kp, kp, k, P.d_lhat, kp, P.d_lhat, kp, true, st)) return -3;
       mark(7);
       // near field alone (split_phases: phase exports)
-      if (P.split_phases && P.n_tleaf > 0) {
-        EvalArgs a = ea;
-        a.items = P.d_tleaf_items; a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
-        launch_eval(P, a, 1, st);
-        ++g_launches;
-        KIFMM_CUDA(cudaGetLastError());
-        if (launch_sym(P, st)) return -3;
-      }
+      if (P.split_phases && launch_near(P, ea, st)) return -3;
       // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
       if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
       if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
+      // far field of the targets into pot_far when the near field is separate (split or
+      // overlapped on the near stream), else everything fused into pot_near
+      const bool sep = P.split_phases || P.overlap;
+      double* far_out = sep ? P.d_pot_far : P.d_pot_near;
       // leaf-op mode: L2T as one GEMV per leaf, stored; the evaluation pass below adds to it
       if (P.leaf_l2t && P.n_tleaf > 0) {
         ++g_launches;
         k_l2t_leafop<<<(P.n_tleaf + L2T_WARPS - 1) / L2T_WARPS, L2T_WARPS * 32, 0, st>>>(
-            P.d_tleaf_items, P.n_tleaf, T.d_level, T.d_pbeg, T.d_pend, P.d_l2t_mat, P.d_lhat, kp, Dp.own_lo,
-            P.split_phases ? P.d_pot_far : P.d_pot_near);
+            P.d_tleaf_items, P.n_tleaf, T.d_level, T.d_pbeg, T.d_pend, P.d_l2t_mat, P.d_lhat, kp, Dp.own_lo, far_out);
         KIFMM_CUDA(cudaGetLastError());
       }
       // L2T + W stage 2 (and, fused, the near field): potentials at the targets of each leaf
-      if (P.n_tleaf > 0) {
+      if (P.n_tleaf > 0 && !(sep && P.leaf_l2t && P.n_far_seg == 0)) {
         EvalArgs a = ea;
         a.items = P.d_tleaf_items;
         a.accumulate = P.leaf_l2t ? 1 : 0;
-        if (P.split_phases) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; a.out = P.d_pot_far; }
-        else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; a.out = P.d_pot_near; }
+        if (sep) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; }
+        else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; }
+        a.out = far_out;
         a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
-        launch_eval(P, a, P.split_phases ? 0 : 1, st);
+        launch_eval(P, a, sep ? 0 : 1, st);
         ++g_launches;
         KIFMM_CUDA(cudaGetLastError());
       }
-      if (!P.split_phases && launch_sym(P, st)) return -3;
+      if (!sep && launch_sym(P, st)) return -3;
+      if (P.overlap) {  // join the near stream, then pot_near += pot_far on the owned points
+        KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_join, 0));
+        const int cnt = Dp.own_hi - Dp.own_lo;
+        if (cnt > 0) {
+          ++g_launches;
+          k_combine<<<nblk(cnt), 256, 0, st>>>(P.d_pot_near, P.d_pot_far, Dp.own_lo, cnt);
+          KIFMM_CUDA(cudaGetLastError());
+        }
+      }
       mark(8);
       if (owned) {
         const int cnt = Dp.own_hi - Dp.own_lo;

@@ -177,3 +177,15 @@ def test_edge_cases():
     s1 = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
     s2 = gpu_plan(2 * pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
     assert rel(s2, 0.5 * s1) < 1e-14
+
+
+@pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k"])
+def test_overlapped_near_stream(case, monkeypatch):
+    # diagnostics option: near field on a second stream joined before the output
+    monkeypatch.setenv("KIFMM_OVERLAP", "1")
+    pts, q, p, k, s = CASES[case]()
+    tb = tables(p, k)
+    ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q)
+    for lo in (0, 1):
+        out = gpu_plan(pts, p, k, s, tb=tb, leaf_ops=lo).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+        assert rel(out, ref) <= TOL
