@@ -357,8 +357,9 @@ __global__ void __launch_bounds__(KP * 4, MINB) k_m2l_sib(const int4* __restrict
 }
 
 // ----------------------------------------------------------------------------
-// k_m2l_sib16: k_m2l_sib with the m16n8k8 FP64 MMA (kp = 32, 64): each B fragment
-// serves two 8-row halves, halving the shared-memory loads per DMMA.  8 warps;
+// k_m2l_sib16: k_m2l_sib with the m16n8k8 FP64 MMA (kp = 32, 64, 104): each B fragment
+// serves two 8-row halves, halving the shared-memory loads per DMMA.  RB = ceil(kp/16)
+// row blocks (kp = 104: 7 blocks, rows 104..111 zero — 7.7% padded M, K unpadded);
 // warp w owns rows 16 (w % RB) .. +16 and columns (w / RB) * NCW .. +NCW of a tile.
 // Same tile scheduler, metadata ring and cp.async B pipeline as k_m2l_sib.
 // ----------------------------------------------------------------------------
@@ -368,22 +369,28 @@ __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4]
                : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b0), "d"(b1));
 }
 
+template <int KP>
+struct Sib16Shape {
+  static constexpr int RB = (KP + 15) / 16;             // row blocks of 16 (rows >= KP are zero)
+  static constexpr int CS = RB * 2 <= 8 ? 8 / RB : 1;   // column groups
+  static constexpr int NW = RB * CS;                    // warps
+};
+
 template <int KP, int NT, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_m2l_sib16(const int4* __restrict__ tiles, int ntiles,
-                                                       const int* __restrict__ cols, const int* __restrict__ classes,
-                                                       const double* __restrict__ C, int mvalid, const double* X,
-                                                       double* Y, int* __restrict__ counter) {
-  constexpr int NW = 8;
+__global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
+    const int4* __restrict__ tiles, int ntiles, const int* __restrict__ cols, const int* __restrict__ classes,
+    const double* __restrict__ C, int mvalid, const double* X, double* Y, int* __restrict__ counter) {
+  constexpr int RB = Sib16Shape<KP>::RB;
+  constexpr int CS = Sib16Shape<KP>::CS;
+  constexpr int NW = Sib16Shape<KP>::NW;
   constexpr int NTH = NW * 32;
   constexpr int SB = KP + 4;
   constexpr int K2 = KP / 2;
   constexpr int CW = 9;
-  constexpr int RB = KP / 16;        // row blocks of 16
-  constexpr int CS = NW / RB;        // column groups
   constexpr int NCW = NT / CS;       // columns per warp
   constexpr int NB = NCW / 8;        // n-blocks per warp
   constexpr int KS8 = KP / 8;        // k8-steps
-  constexpr int CH = 2;              // k8-steps per A chunk
+  constexpr int CH = KS8 % 2 == 0 ? 2 : 1;  // k8-steps per A chunk
   constexpr int NCH = KS8 / CH;
   static_assert(KS8 % CH == 0 && NB >= 1, "tile shape");
   extern __shared__ __align__(16) double sm[];
@@ -416,11 +423,12 @@ __global__ void __launch_bounds__(256, MINB) k_m2l_sib16(const int4* __restrict_
   };
   // A fragment of k8-step ks: rows r0+g, r0+g+8; columns 8 ks + t, 8 ks + t + 4
   auto op_rows = [&](int id) { return C + (size_t)id * KP * KP + (size_t)(r0 + g) * KP + t; };
+  const bool lo_ok = r0 + g < KP, hi_ok = r0 + g + 8 < KP;  // padded rows (KP % 16 != 0) read as zero
   auto load_a = [&](const double* Ar, int ks, double (&a)[4]) {
-    a[0] = __ldg(Ar + 8 * ks);
-    a[1] = __ldg(Ar + 8 * KP + 8 * ks);
-    a[2] = __ldg(Ar + 8 * ks + 4);
-    a[3] = __ldg(Ar + 8 * KP + 8 * ks + 4);
+    a[0] = lo_ok ? __ldg(Ar + 8 * ks) : 0.0;
+    a[1] = hi_ok ? __ldg(Ar + 8 * KP + 8 * ks) : 0.0;
+    a[2] = lo_ok ? __ldg(Ar + 8 * ks + 4) : 0.0;
+    a[3] = hi_ok ? __ldg(Ar + 8 * KP + 8 * ks + 4) : 0.0;
   };
 
   int slot = 0;
@@ -1102,12 +1110,13 @@ static int sib_minb() {
 template <int KP, int MINB>
 int launch_sib16(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
   constexpr int NT = sq_nt(KP);
+  constexpr int NTH = Sib16Shape<KP>::NW * 32;
   const size_t smem = (size_t)NT * 2 * (KP + 4) * sizeof(double);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_sib16<KP, NT, MINB>, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_sib16<KP, NT, MINB>, NTH, smem);
   const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
   KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
-  k_m2l_sib16<KP, NT, MINB><<<grid, 256, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y,
+  k_m2l_sib16<KP, NT, MINB><<<grid, NTH, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y,
                                                      g.d_counter);
   return 0;
 }
@@ -1120,8 +1129,9 @@ static int sib16() {
 int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, const double* X, double* Y, cudaStream_t st) {
   if (g.ntiles == 0) return 0;
   ++g_launches;
-  if (sib16() && (kp == 32 || kp == 64)) {
+  if (sib16() && (kp == 32 || kp == 64 || (kp == 104 && sib16() != 2))) {
     if (kp == 32) launch_sib16<32, 3>(g, C, mvalid, X, Y, st);
+    else if (kp == 104) launch_sib16<104, 3>(g, C, mvalid, X, Y, st);
     else if (sib_minb() == 3) launch_sib16<64, 3>(g, C, mvalid, X, Y, st);
     else launch_sib16<64, 2>(g, C, mvalid, X, Y, st);
     KIFMM_CUDA(cudaGetLastError());
@@ -1182,6 +1192,7 @@ int kernels_init() {
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<32, sq_nt(32), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<104, sq_nt(104), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
 }
