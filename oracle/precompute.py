@@ -15,6 +15,9 @@ numpy.linalg.eigh.  "P:n" = /root/reference/PAPER.md line n.
   C_delta      P:216-223  K~ = U^T K R with R = U
   S', T'       P:341, P:351 (T~ = T U, typo reading Q16), fused with pinv (Q17)
   M~_o, L~_o
+  stage 2      P:248-312  per-offset truncated SVD of each compressed core:
+                          K~_0^(i) = U S Q^T, singular values < eps2 ||K_fat||_2 dropped
+                          (eq-lra); eps2 = C2 eps1 / p~ (eq-vareps2)
 """
 from __future__ import annotations
 
@@ -103,3 +106,35 @@ def build_tables(p: int, k: int, d: float = 0.1, rcond: float = 1e-10, k_exact: 
     L = np.stack([U.T @ kernel_matrix(octant_centre(o) + 0.5 * f_in * g, de) @ Ei_d @ U for o in range(8)])
     return dict(p=p, n=n, k=keff, d=d, rcond=rcond, U=U, C=C, S=S, T=T, M=M, L=L, sigma=sigma,
                 E_u=E_u, E_d=E_d, K=K)
+
+
+def stage1_eps1(tb: dict) -> float:
+    """The stage-1 truncation level actually applied: sigma_{k+1} / sigma_1 (the columns kept
+    are those with sigma >= eps1 ||K_fat||_2; with a fixed k, eps1 is the first
+    dropped singular value relative to the largest)."""
+    sig, k = tb["sigma"], tb["k"]
+    return float(sig[k] / sig[0]) if k < sig.size else 0.0
+
+
+def stage2(tb: dict, C2: float) -> dict:
+    """Stage 2 of the M2L compression, step by step in the paper's order:
+    eps2 = C2 * eps1 / p~ (eq-vareps2, p~ = k); for each of the 316 compressed cores
+    K~_0^(i) = U_0 S_0 Q_0^T (SVD), keep the singular values >= eps2 ||K_0,fat||_2
+    (||K_fat||_2 = sigma_1), U^ = the kept columns of U_0, V^ = S^ Q^^T (eq-lra).
+    Returns a copy of the tables whose cores are the products C_o = U^_o V^_o, with
+    the factors, the ranks and eps2.  C2 = 0 returns the tables unchanged."""
+    if C2 <= 0:
+        return dict(tb, ranks=np.full(316, tb["k"]), eps2=0.0)
+    k = tb["k"]
+    eps2 = C2 * stage1_eps1(tb) / k
+    cut = eps2 * tb["sigma"][0]
+    C = np.empty_like(tb["C"])
+    Uh, Vh, ranks = [], [], np.zeros(316, dtype=np.int64)
+    for o in range(316):
+        U0, S0, Q0t = np.linalg.svd(tb["C"][o])
+        r = int((S0 >= cut).sum())
+        ranks[o] = r
+        Uh.append(U0[:, :r].copy())
+        Vh.append(S0[:r, None] * Q0t[:r])
+        C[o] = Uh[o] @ Vh[o]
+    return dict(tb, C=C, Uhat=Uh, Vhat=Vh, ranks=ranks, eps2=eps2, C2=C2)

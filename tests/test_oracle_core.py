@@ -214,3 +214,43 @@ def test_compressed_l2l_reproduces_child_local_field():
     cc = pc.octant_centre(o)
     pd_child = _far_field(far, q, cc + 0.5 * (1 + d) * g)
     assert np.linalg.norm(t["U"] @ lhat_c - pd_child) / np.linalg.norm(pd_child) < 1e-5
+
+
+# ---------------------------------------------------------------- stage-2 low-rank M2L
+@pytest.mark.parametrize("p,k", [(4, 24), (6, 60)])
+def test_stage2_truncation_bound_and_ranks(p, k):
+    tb = pc.build_tables(p, k)
+    s1 = tb["sigma"][0]
+    for C2 in (1.0, 10.0):
+        t2 = pc.stage2(tb, C2)
+        assert t2["eps2"] == pytest.approx(C2 * (tb["sigma"][tb["k"]] / s1) / tb["k"])
+        for o in (0, 57, 158, 315):
+            # || K^_0^(i) - K~_0^(i) ||_2 <= eps2 || K_0,fat ||_2
+            err = np.linalg.norm(t2["C"][o] - tb["C"][o], 2)
+            assert err <= t2["eps2"] * s1 * (1 + 1e-9)
+            # the truncated core has exactly the kept rank
+            sv = np.linalg.svd(t2["C"][o], compute_uv=False)
+            r = t2["ranks"][o]
+            assert sv[r - 1] >= t2["eps2"] * s1 * (1 - 1e-9)
+            if r < sv.size:
+                assert sv[r] <= 1e-12 * s1
+            np.testing.assert_allclose(t2["Uhat"][o].T @ t2["Uhat"][o], np.eye(r), atol=1e-12)
+        assert 1 <= t2["ranks"].min() and t2["ranks"].max() < tb["k"]
+    # C2 -> 0: stage 2 off, the cores are unchanged
+    assert np.array_equal(pc.stage2(tb, 0.0)["C"], tb["C"])
+
+
+def test_stage2_ranks_lower_for_far_offsets():
+    # Fig. ranksM2L: the cores' numerical ranks are well below p~ and fall with
+    # the distance of the interacting cube (offsets with |delta|_inf = 3 vs 2)
+    tb = pc.build_tables(6, 60)
+    t2 = pc.stage2(tb, 1.0)
+    far = np.abs(pc.offsets()).max(1) == 3
+    assert t2["ranks"][far].mean() < t2["ranks"][~far].mean() < tb["k"]
+    # the symmetric partner offset -delta has the transposed core (K_-d = K_d^T for
+    # UE = DC, reading Q10), hence the same rank
+    offs = [tuple(o) for o in pc.offsets()]
+    for i, o in enumerate(offs[:40]):
+        j = offs.index(tuple(-np.array(o)))
+        assert t2["ranks"][i] == t2["ranks"][j]
+        np.testing.assert_allclose(tb["C"][j], tb["C"][i].T, atol=1e-14 * np.abs(tb["C"][i]).max())

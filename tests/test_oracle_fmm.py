@@ -105,3 +105,17 @@ def test_phase_outputs_sum_to_potential(c1):
     pot, ph = plan.matvec(tb, q, phases=True)
     perm = plan.tree()["perm"]
     np.testing.assert_array_equal(pot[perm], ph["near"] + ph["far"])
+
+
+def test_stage2_accuracy_vs_direct():
+    # the stage-2 error is of the order of eps1 when eps2 = C2 eps1 / p~; measured on
+    # C1 at p = 6: C2 = 1 leaves the error vs the direct sum unchanged (< 2% growth), and the
+    # error grows with C2 (the truncation is monotone in eps2)
+    pts, q, _ = synth_inputs.make("C1")
+    d = oracle.direct(pts, q)
+    tb = pc.build_tables(6, 60)
+    plan = oracle.Plan(pts, 64, tb["n"])
+    errs = [np.linalg.norm(plan.matvec(pc.stage2(tb, c2), q) - d) / np.linalg.norm(d) for c2 in (0.0, 1.0, 10.0, 100.0)]
+    assert errs[1] <= 1.02 * errs[0]
+    assert errs[0] <= errs[2] <= errs[3]
+    assert errs[3] < 1e-3
