@@ -54,6 +54,7 @@ typedef struct {
   int p, n, k;
   double d;
   const double *U, *C, *S, *T, *M, *L;
+  const double* sigma;  /* n singular values of K_fat, descending (needed by stage 2; may be NULL) */
 } fmm_tables_view;
 
 typedef struct {
@@ -87,6 +88,10 @@ typedef struct {
                          doubles each): a matvec then streams them from HBM instead of
                          evaluating n kernel values per point and operator.  -1 (default): each
                          while max(16 GB, 25% of the device) stays free; 0 off; 1 on. */
+  double m2l_c2;      /* stage 2 of the M2L compression: each core C_o is replaced
+                         by its SVD truncated at eps2 ||K_fat||_2 with eps2 = C2 eps1 / k
+                         (eq-vareps2; eps1 = sigma_{k+1} / sigma_1, the stage-1 truncation) and
+                         M2L runs as two skinny GEMMs (U^_o (V^_o q)).  0 (default) = off. */
 } fmm_options;
 
 typedef struct {
@@ -108,6 +113,10 @@ typedef struct {
   int64_t ghost_d_recv, ghost_d_send;  /* ghost densities per matvec (owned mode) */
   int64_t nV_local;           /* V pairs this rank's M2L applies (= nV on one rank) */
   int64_t leaf_op_bytes;      /* device bytes of the per-leaf operators (0: not used) */
+  double m2l_flops;           /* algorithmic M2L flops of one matvec on this rank:
+                                 sum over V pairs of 2 k^2 (dense cores) or 4 k r_o (stage 2) */
+  double m2l_eps2;            /* stage-2 threshold relative to ||K_fat||_2 (0: off) */
+  double m2l_rank_mean;       /* mean stage-2 rank over the 316 offsets (k when off) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

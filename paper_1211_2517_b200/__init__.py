@@ -26,7 +26,7 @@ class FmmError(RuntimeError):
 class TablesView(ctypes.Structure):
     _fields_ = [("p", ctypes.c_int), ("n", ctypes.c_int), ("k", ctypes.c_int), ("d", ctypes.c_double),
                 ("U", ctypes.c_void_p), ("C", ctypes.c_void_p), ("S", ctypes.c_void_p), ("T", ctypes.c_void_p),
-                ("M", ctypes.c_void_p), ("L", ctypes.c_void_p)]
+                ("M", ctypes.c_void_p), ("L", ctypes.c_void_p), ("sigma", ctypes.c_void_p)]
 
 
 class Options(ctypes.Structure):
@@ -34,7 +34,7 @@ class Options(ctypes.Structure):
                 ("pinv_rcond", ctypes.c_double), ("wx_direct_max", ctypes.c_int),
                 ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
-                ("leaf_ops", ctypes.c_int)]
+                ("leaf_ops", ctypes.c_int), ("m2l_c2", ctypes.c_double)]
 
 
 class Info(ctypes.Structure):
@@ -50,7 +50,8 @@ class Info(ctypes.Structure):
                 ("own_lo", ctypes.c_int64), ("own_hi", ctypes.c_int64), ("n_straddle", ctypes.c_int64),
                 ("ghost_q_recv", ctypes.c_int64), ("ghost_q_send", ctypes.c_int64),
                 ("ghost_d_recv", ctypes.c_int64), ("ghost_d_send", ctypes.c_int64), ("nV_local", ctypes.c_int64),
-                ("leaf_op_bytes", ctypes.c_int64)]
+                ("leaf_op_bytes", ctypes.c_int64), ("m2l_flops", ctypes.c_double), ("m2l_eps2", ctypes.c_double),
+                ("m2l_rank_mean", ctypes.c_double)]
 
 
 # phases of fmm_matvec (profile=True): the near field is evaluated in the "eval" pass together with
@@ -192,7 +193,7 @@ class Plan:
     def __init__(self, points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, d: float = 0.1,
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
                  split_phases: bool = False, stream=None, nranks: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None, leaf_ops: int = -1):
+                 nccl_id: bytes | None = None, leaf_ops: int = -1, m2l_c2: float = 0.0):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -202,7 +203,7 @@ class Plan:
         lib().fmm_default_options(ctypes.byref(opt))
         opt.p, opt.k, opt.leaf_size, opt.d, opt.pinv_rcond = p, k, leaf_size, d, rcond
         opt.wx_direct_max, opt.profile, opt.split_phases = wx_direct_max, int(profile), int(split_phases)
-        opt.nranks, opt.rank, opt.leaf_ops = nranks, rank, int(leaf_ops)
+        opt.nranks, opt.rank, opt.leaf_ops, opt.m2l_c2 = nranks, rank, int(leaf_ops), float(m2l_c2)
         self._keep = []
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -210,8 +211,11 @@ class Plan:
             opt.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
         if tables is not None:
             arrs = {x: np.ascontiguousarray(tables[x], dtype=np.float64) for x in "UCSTML"}
+            if tables.get("sigma") is not None:
+                arrs["sigma"] = np.ascontiguousarray(tables["sigma"], dtype=np.float64)
             self._keep.append(arrs)
-            tv = TablesView(tables["p"], tables["n"], tables["k"], tables["d"], *(arrs[x].ctypes.data for x in "UCSTML"))
+            tv = TablesView(tables["p"], tables["n"], tables["k"], tables["d"], *(arrs[x].ctypes.data for x in "UCSTML"),
+                            arrs["sigma"].ctypes.data if "sigma" in arrs else None)
             self._keep.append(tv)
             opt.tables = ctypes.pointer(tv)
         dens = None

@@ -86,6 +86,7 @@ void fmm_default_options(fmm_options* o) {
   o->rank = 0;
   o->nccl_id = nullptr;
   o->leaf_ops = -1;
+  o->m2l_c2 = 0.0;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -109,6 +110,7 @@ int fmm_tables_view_get(const fmm_tables* t, fmm_tables_view* v, const double** 
   const kifmm::HostTables& H = t->H;
   v->p = H.p; v->n = H.n; v->k = H.k; v->d = H.d;
   v->U = H.U.data(); v->C = H.C.data(); v->S = H.S.data(); v->T = H.T.data(); v->M = H.M.data(); v->L = H.L.data();
+  v->sigma = H.sigma.data();
   if (sigma) *sigma = H.sigma.data();
   return FMM_OK;
 }
@@ -172,6 +174,8 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     H.T.assign(v->T, v->T + n * k);
     H.M.assign(v->M, v->M + 8 * k * k);
     H.L.assign(v->L, v->L + 8 * k * k);
+    if (v->sigma) H.sigma.assign(v->sigma, v->sigma + n);
+    else H.sigma.clear();
     // surface grid (same enumeration as the precompute)
     H.surf.clear();
     const int pp = v->p;
@@ -187,6 +191,8 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     int rc = kifmm::build_tables(opt->p, opt->k, opt->d, opt->pinv_rcond, &P.tables);
     if (rc) return fail(rc);
   }
+  if (!(opt->m2l_c2 >= 0)) { set_error("fmm_setup: m2l_c2 must be >= 0"); return fail(FMM_EINVAL); }
+  if (int rc = kifmm::build_stage2(P.tables, opt->m2l_c2)) return fail(rc == -2 ? FMM_ECONFIG : rc);
   h->precompute_ms = ms_since(t0);
   P.p = P.tables.p;
   P.n = P.tables.n;
@@ -497,6 +503,13 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
   info->ghost_d_send = P.xd.nsend;
   info->nV_local = P.nV_local;
   info->leaf_op_bytes = P.leaf_op_bytes;
+  info->m2l_flops = P.m2l_flops;
+  info->m2l_eps2 = P.tables.eps2;
+  {
+    double rs = 0;
+    for (int r : P.tables.ranks) rs += r;
+    info->m2l_rank_mean = P.tables.ranks.empty() ? P.k : rs / P.tables.ranks.size();
+  }
   return FMM_OK;
 }
 

@@ -21,9 +21,15 @@ struct HostTables {
   std::vector<double> T;       // n x k
   std::vector<double> M;       // 8 x k x k
   std::vector<double> L;       // 8 x k x k
+  // stage 2: per-offset low-rank factors of C, empty when off
+  double eps2 = 0;
+  int rmax = 0;
+  std::vector<int> ranks;                 // 316
+  std::vector<std::vector<double>> Uh, Vh;  // k x r_o, r_o x k
 };
 
 int build_tables(int p, int k, double d, double rcond, HostTables* out);
+int build_stage2(HostTables& H, double C2);
 
 // One launch of the grouped gather-GEMM-scatter kernel: Y[tgt] (+)= scale * Op * X[src].
 struct GemmTile {
@@ -49,6 +55,16 @@ struct SibLaunch {
   int* d_cols = nullptr;
   int* d_classes = nullptr;
   int* d_counter = nullptr;  // dynamic tile scheduler (reset before every launch)
+};
+
+// Stage-2 low-rank M2L factors on the device (k_m2l_lr), zero padded: Uh[316][kp][rp],
+// Vh[316][rp][kp] with rp = max rank rounded up to 16; rank[316].
+struct LowRank {
+  bool on = false;
+  int rp = 0;
+  double* d_Uh = nullptr;
+  double* d_Vh = nullptr;
+  int* d_rank = nullptr;
 };
 
 struct Tree {
@@ -141,6 +157,8 @@ struct Plan {
   double* d_T = nullptr;    // n x kp    (T')
   double* d_Ue = nullptr;   // n x kp    (U)
   double* d_surf = nullptr; // n x 3 unit surface grid
+  LowRank lr;               // stage-2 M2L (fmm_options.m2l_c2 > 0)
+  double m2l_flops = 0;     // algorithmic M2L flops per matvec on this rank
   // work buffers
   double* d_qhat = nullptr;     // nboxes x kp (level-normalised q^')
   double* d_lhat = nullptr;     // nboxes x kp

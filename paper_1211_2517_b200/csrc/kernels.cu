@@ -1107,6 +1107,204 @@ static int sib_minb() {
   return v;
 }
 
+// ----------------------------------------------------------------------------
+// k_m2l_lr: the sibling-grouped M2L with the paper's stage-2 low-rank cores
+// (eq-lra): C_o ~= U^_o V^_o with rank r_o, so each operator step of a
+// tile is two skinny GEMMs instead of one k x k GEMM:
+//   phase A  T = V^_o Q        (r_o x NT, inner k)   -> shared memory (column-major)
+//   phase B  acc += U^_o T     (k x NT, inner r_o)   -> the per-(target, delta) accumulators
+// 4 k r_o instead of 2 k^2 flops per column.  Same tiles, classes, dynamic scheduler,
+// metadata ring and cp.async B-panel pipeline as k_m2l_sib16; m16n8k8 FP64 MMA in both
+// phases.  Factor tables (zero padded): Vh[o] RP x KP, Uh[o] KP x RP; rank[o] = r_o.
+// ----------------------------------------------------------------------------
+template <int KP, int NT, int RP, int MINB>
+__global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_lr(
+    const int4* __restrict__ tiles, int ntiles, const int* __restrict__ cols, const int* __restrict__ classes,
+    const double* __restrict__ Uh, const double* __restrict__ Vh, const int* __restrict__ rank, int mvalid,
+    const double* X, double* Y, int* __restrict__ counter) {
+  constexpr int RB = Sib16Shape<KP>::RB;
+  constexpr int CS = Sib16Shape<KP>::CS;
+  constexpr int NW = Sib16Shape<KP>::NW;
+  constexpr int NTH = NW * 32;
+  constexpr int SB = KP + 4;
+  constexpr int ST = RP + 4;         // T: column-major, stride ST
+  constexpr int K2 = KP / 2;
+  constexpr int CW = 9;
+  constexpr int NCW = NT / CS;
+  constexpr int NB = NCW / 8;
+  constexpr int NBT = NT / 8;        // n-blocks of a tile (phase A)
+  constexpr int KS8 = KP / 8;
+  extern __shared__ __align__(16) double sm[];
+  double* Ts = sm + 2 * NT * SB;
+  __shared__ int s_meta[3][NT * CW];
+  __shared__ int s_tile[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp % RB) * 16;
+  const int cbase = (warp / RB) * NCW;
+  const bool lo_ok = r0 + g < KP, hi_ok = r0 + g + 8 < KP;
+  int ti = blockIdx.x;
+  if (ti >= ntiles) return;
+
+  auto fetch_meta = [&](int tid, int slot) {
+    const int4 tl = tiles[tid];
+    for (int e = threadIdx.x; e < NT * CW; e += NTH) {
+      const int c = e / CW;
+      s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
+    }
+  };
+  auto gather = [&](int slot, int b, int buf) {
+    double* Bd = sm + buf * NT * SB;
+    for (int p = warp; p < NT; p += NW) {
+      const int src = s_meta[slot][p * CW + 1 + b];
+      for (int c = lane; c < K2; c += 32) {
+        double* dst = Bd + p * SB + 2 * c;
+        if (src >= 0) cp_async16(dst, X + (size_t)src * KP + 2 * c);
+        else { dst[0] = 0.0; dst[1] = 0.0; }
+      }
+    }
+  };
+
+  int slot = 0;
+  fetch_meta(ti, 0);
+  if (threadIdx.x == 0) s_tile[1] = gridDim.x + atomicAdd(counter, 1);
+  __syncthreads();
+  const int* cls = classes + tiles[ti].x * 17;
+  gather(0, cls[1], 0);
+  cp_async_commit();
+  int buf = 0;
+  double acc[NB][4];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+
+  while (true) {
+    const int nv = cls[0];
+    const int nslot = slot == 2 ? 0 : slot + 1;
+    const int tnext = s_tile[nslot];
+    for (int jb = 0; jb < nv; ++jb) {
+      const bool last = jb + 1 == nv;
+      if (jb == 0 && tnext < ntiles) {
+        fetch_meta(tnext, nslot);
+        if (threadIdx.x == 0) s_tile[nslot == 2 ? 0 : nslot + 1] = gridDim.x + atomicAdd(counter, 1);
+      }
+      cp_async_wait0();
+      __syncthreads();  // B panel of this step landed; T free; next metadata visible
+      if (!last) gather(slot, cls[2 + jb], buf ^ 1);
+      else if (tnext < ntiles) gather(nslot, classes[tiles[tnext].x * 17 + 1], buf ^ 1);
+      cp_async_commit();
+      const int op = cls[9 + jb];
+      const int r = rank[op];
+      const int ra = (r + 15) >> 4, rk8 = (r + 7) >> 3;
+      // ---- phase A: T = V^_o Q   (tiles (row block, n-block) over the warps)
+      {
+        const double* Vo = Vh + (size_t)op * RP * KP;
+        const double* B = sm + buf * NT * SB;
+        for (int tile = warp; tile < ra * NBT; tile += NW) {
+          const int rb = tile / NBT, nb = tile - rb * NBT;
+          const double* Ar = Vo + (size_t)(16 * rb + g) * KP + t;
+          const double* Bp = B + (size_t)(nb * 8 + g) * SB + t;
+          double c4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+          for (int ks = 0; ks < KS8; ++ks) {
+            double a[4];
+            a[0] = __ldg(Ar + 8 * ks);
+            a[1] = __ldg(Ar + 8 * KP + 8 * ks);
+            a[2] = __ldg(Ar + 8 * ks + 4);
+            a[3] = __ldg(Ar + 8 * KP + 8 * ks + 4);
+            dmma_16x8x8(c4, a, Bp[8 * ks], Bp[8 * ks + 4]);
+          }
+          // c0,c1: T[16 rb + g][nb 8 + 2t (+1)], c2,c3: row + 8
+          double* T0 = Ts + (size_t)(nb * 8 + 2 * t) * ST + 16 * rb + g;
+          T0[0] = c4[0];
+          T0[ST] = c4[1];
+          T0[8] = c4[2];
+          T0[ST + 8] = c4[3];
+        }
+      }
+      __syncthreads();  // T complete
+      // ---- phase B: acc += U^_o T   (warp: rows r0..r0+16, columns cbase..cbase+NCW)
+      {
+        const double* Ar = Uh + (size_t)op * KP * RP + (size_t)(r0 + g) * RP + t;
+        const double* Bp = Ts + (size_t)(cbase + g) * ST + t;
+        for (int ks = 0; ks < rk8; ++ks) {
+          double a[4];
+          a[0] = lo_ok ? __ldg(Ar + 8 * ks) : 0.0;
+          a[1] = hi_ok ? __ldg(Ar + 8 * RP + 8 * ks) : 0.0;
+          a[2] = lo_ok ? __ldg(Ar + 8 * ks + 4) : 0.0;
+          a[3] = hi_ok ? __ldg(Ar + 8 * RP + 8 * ks + 4) : 0.0;
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            const double* bp = Bp + (size_t)j * 8 * ST + 8 * ks;
+            dmma_16x8x8(acc[j], a, bp[0], bp[4]);
+          }
+        }
+      }
+      buf ^= 1;
+      if (last) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int tg = s_meta[slot][(cbase + j * 8 + 2 * t + c) * CW];
+            if (tg >= 0) {
+              if (r0 + g < mvalid) atomicAdd(Y + (size_t)tg * KP + r0 + g, acc[j][c]);
+              if (r0 + g + 8 < mvalid) atomicAdd(Y + (size_t)tg * KP + r0 + g + 8, acc[j][2 + c]);
+            }
+          }
+          acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+        }
+      }
+    }
+    if (tnext >= ntiles) break;
+    ti = tnext;
+    slot = nslot;
+    cls = classes + tiles[ti].x * 17;
+  }
+}
+
+template <int KP, int RP>
+int launch_lr(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
+  constexpr int NT = sq_nt(KP);
+  constexpr int NTH = Sib16Shape<KP>::NW * 32;
+  const size_t smem = ((size_t)NT * 2 * (KP + 4) + (size_t)NT * (RP + 4)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_lr<KP, NT, RP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_lr<KP, NT, RP, 2>, NTH, smem);
+  const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
+  KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
+  k_m2l_lr<KP, NT, RP, 2><<<grid, NTH, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, lr.d_Uh, lr.d_Vh,
+                                                   lr.d_rank, mvalid, X, Y, g.d_counter);
+  return 0;
+}
+
+template <int KP>
+int launch_lr_rp(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
+  switch (lr.rp) {
+    case 16: return launch_lr<KP, 16>(g, lr, mvalid, X, Y, st);
+    case 32: return launch_lr<KP, 32>(g, lr, mvalid, X, Y, st);
+    case 48: return launch_lr<KP, 48>(g, lr, mvalid, X, Y, st);
+    case 64: return launch_lr<KP, 64>(g, lr, mvalid, X, Y, st);
+    default: return launch_lr<KP, (KP + 15) / 16 * 16>(g, lr, mvalid, X, Y, st);
+  }
+}
+
+int launch_m2l_lowrank(const SibLaunch& g, const LowRank& lr, int kp, int mvalid, const double* X, double* Y,
+                       cudaStream_t st) {
+  if (g.ntiles == 0) return 0;
+  ++g_launches;
+  int rc = 0;
+  if (kp == 32) rc = launch_lr_rp<32>(g, lr, mvalid, X, Y, st);
+  else if (kp == 64) rc = launch_lr_rp<64>(g, lr, mvalid, X, Y, st);
+  else rc = launch_lr_rp<104>(g, lr, mvalid, X, Y, st);
+  if (rc) return rc;
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
+}
+
 template <int KP, int MINB>
 int launch_sib16(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
   constexpr int NT = sq_nt(KP);
@@ -1338,7 +1536,11 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       mark(4);
       // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
       //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
-      if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, st)) return -3;
+      if (P.lr.on) {
+        if (launch_m2l_lowrank(P.g_m2l_sib, P.lr, kp, k, P.d_qhat, P.d_lhat, st)) return -3;
+      } else if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, st)) {
+        return -3;
+      }
       if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, st)) return -3;
       mark(5);
       // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)

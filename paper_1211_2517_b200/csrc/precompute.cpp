@@ -138,6 +138,64 @@ Mat pinv_jacobi(const Mat& A, int n, double rcond) {
   return P;
 }
 
+// SVD of a square n x n A by one-sided (Hestenes) Jacobi: A = sum_c s_c u_c v_c^T,
+// s descending; u (n x n, column c = u_c, row-major), v (n x n, row c = v_c).
+void svd_jacobi(const Mat& A, int n, std::vector<double>& s, Mat& u, Mat& v) {
+  Mat W = transpose(A, n, n);  // row c of W = column c of A
+  Mat V((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    double off = 0;
+    for (int i = 0; i < n - 1; ++i)
+      for (int j = i + 1; j < n; ++j) {
+        double* wi = &W[(size_t)i * n];
+        double* wj = &W[(size_t)j * n];
+        double al = 0, be = 0, ga = 0;
+        for (int r = 0; r < n; ++r) { al += wi[r] * wi[r]; be += wj[r] * wj[r]; ga += wi[r] * wj[r]; }
+        if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+        const double rel = std::fabs(ga) / std::sqrt(al * be);
+        off = std::max(off, rel);
+        if (rel < 1e-15) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        for (int r = 0; r < n; ++r) {
+          const double x = wi[r], y = wj[r];
+          wi[r] = c * x - sn * y;
+          wj[r] = sn * x + c * y;
+        }
+        double* vi = &V[(size_t)i * n];
+        double* vj = &V[(size_t)j * n];
+        for (int r = 0; r < n; ++r) {
+          const double x = vi[r], y = vj[r];
+          vi[r] = c * x - sn * y;
+          vj[r] = sn * x + c * y;
+        }
+      }
+    if (off < 1e-15) break;
+  }
+  std::vector<double> sig(n);
+  for (int c = 0; c < n; ++c) {
+    double s2 = 0;
+    for (int r = 0; r < n; ++r) s2 += W[(size_t)c * n + r] * W[(size_t)c * n + r];
+    sig[c] = std::sqrt(s2);
+  }
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return sig[a] > sig[b]; });
+  s.resize(n);
+  u.assign((size_t)n * n, 0.0);
+  v.assign((size_t)n * n, 0.0);
+  for (int c = 0; c < n; ++c) {
+    const int k = idx[c];
+    s[c] = sig[k];
+    for (int r = 0; r < n; ++r) {
+      u[(size_t)r * n + c] = sig[k] > 0 ? W[(size_t)k * n + r] / sig[k] : 0.0;
+      v[(size_t)c * n + r] = V[(size_t)k * n + r];
+    }
+  }
+}
+
 // Cyclic Jacobi eigendecomposition of a symmetric n x n matrix. Returns
 // eigenvalues descending; column c of `vec` (row-major n x n) is eigenvector c.
 void jacobi_eig(Mat A, int n, std::vector<double>& val, Mat& vec) {
@@ -263,6 +321,56 @@ int build_tables(int p, int k, double d, double rcond, HostTables* out) {
     std::memcpy(&out->L[(size_t)o * kk * kk], Lo.data(), sizeof(double) * kk * kk);
   }
   out->surf = g;
+  return 0;
+}
+
+// Stage 2 of the M2L compression: eps2 = C2 eps1 / p~ (eq-vareps2) with
+// eps1 = sigma_{k+1} / sigma_1 (the stage-1 truncation applied) and p~ = k; each core
+// C_o = U_o S_o Q_o^T (SVD) keeps the singular values >= eps2 ||K_fat||_2 = eps2 sigma_1
+// (eq-lra): U^_o = the kept columns of U_o (k x r_o), V^_o = S^_o Q^_o^T (r_o x k).
+int build_stage2(HostTables& H, double C2) {
+  H.ranks.clear(); H.Uh.clear(); H.Vh.clear(); H.eps2 = 0; H.rmax = 0;
+  if (!(C2 > 0)) return 0;
+  const int k = H.k;
+  if (H.sigma.size() < (size_t)k + 1 || !(H.sigma[0] > 0)) {
+    set_error("stage 2 needs the singular values of K_fat (tables.sigma)");
+    return -2;
+  }
+  H.eps2 = C2 * (H.sigma[k] / H.sigma[0]) / k;
+  const double cut = H.eps2 * H.sigma[0];
+  std::vector<Mat> Us(kNumOffsets), Vs(kNumOffsets);
+  std::vector<std::vector<double>> Ss(kNumOffsets);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int o = 0; o < kNumOffsets; ++o) {
+    Mat A(H.C.begin() + (size_t)o * k * k, H.C.begin() + (size_t)(o + 1) * k * k);
+    svd_jacobi(A, k, Ss[o], Us[o], Vs[o]);
+  }
+  H.ranks.assign(kNumOffsets, 0);
+  for (int o = 0; o < kNumOffsets; ++o) {
+    int r = 0;
+    while (r < k && Ss[o][r] >= cut) ++r;
+    H.ranks[o] = r;
+    H.rmax = std::max(H.rmax, r);
+  }
+  // factors, unpadded: Uh[o] k x r_o (row-major), Vh[o] r_o x k
+  H.Uh.resize(kNumOffsets);
+  H.Vh.resize(kNumOffsets);
+  for (int o = 0; o < kNumOffsets; ++o) {
+    const int r = H.ranks[o];
+    H.Uh[o].assign((size_t)k * r, 0.0);
+    H.Vh[o].assign((size_t)r * k, 0.0);
+    for (int a = 0; a < k; ++a)
+      for (int c = 0; c < r; ++c) H.Uh[o][(size_t)a * r + c] = Us[o][(size_t)a * k + c];
+    for (int c = 0; c < r; ++c)
+      for (int b = 0; b < k; ++b) H.Vh[o][(size_t)c * k + b] = Ss[o][c] * Vs[o][(size_t)c * k + b];
+    // the truncated core U^_o V^_o replaces C_o (every M2L path applies the same operator)
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) {
+        double acc = 0;
+        for (int c = 0; c < r; ++c) acc += H.Uh[o][(size_t)a * r + c] * H.Vh[o][(size_t)c * k + b];
+        H.C[((size_t)o * k + a) * k + b] = acc;
+      }
+  }
   return 0;
 }
 

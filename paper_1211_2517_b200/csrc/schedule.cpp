@@ -331,6 +331,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
       const int e0 = vcnt[b], e1 = vcnt[b + 1];
       if (e0 == e1 || !inD(b)) continue;
       P.nV_local += e1 - e0;
+      for (int e = e0; e < e1; ++e)  // algorithmic flops: 2 k^2 (dense core) or 4 k r_o (stage 2)
+        P.m2l_flops += P.lr.on ? 4.0 * P.k * P.tables.ranks[vby[e].z] : 2.0 * P.k * P.k;
       anchor(T.parent[b], ap);
       const int a = (int)(T.key[b] & 7);
       // distinct source parents (<= 26)
@@ -480,6 +482,23 @@ int upload_tables(Plan& P) {
       upload(P, &P.d_Ut, Ut, st) || upload(P, &P.d_T, Tt, st) || upload(P, &P.d_Ue, Ue, st))
     return -3;
   if (upload(P, &P.d_surf, H.surf, st)) return -3;
+  // stage-2 factors, zero padded to kp x rp / rp x kp (rp = max rank rounded up to 16)
+  P.lr = LowRank();
+  if (!H.ranks.empty()) {
+    const int rp = std::max(16, (H.rmax + 15) / 16 * 16);
+    std::vector<double> Uh((size_t)316 * kp * rp, 0.0), Vh((size_t)316 * rp * kp, 0.0);
+    for (int o = 0; o < 316; ++o) {
+      const int r = H.ranks[o];
+      for (int a = 0; a < k; ++a)
+        for (int c = 0; c < r; ++c) Uh[((size_t)o * kp + a) * rp + c] = H.Uh[o][(size_t)a * r + c];
+      for (int c = 0; c < r; ++c)
+        for (int b = 0; b < k; ++b) Vh[((size_t)o * rp + c) * kp + b] = H.Vh[o][(size_t)c * k + b];
+    }
+    P.lr.on = true;
+    P.lr.rp = rp;
+    if (upload(P, &P.lr.d_Uh, Uh, st) || upload(P, &P.lr.d_Vh, Vh, st) || upload(P, &P.lr.d_rank, H.ranks, st))
+      return -3;
+  }
   KIFMM_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
