@@ -53,7 +53,9 @@ def lib():
         L.oracle_count.argtypes = [ctypes.c_void_p, ctypes.c_int]
         L.oracle_export_tree.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 8
         L.oracle_export_lists.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 4
-        L.oracle_matvec.argtypes = [ctypes.c_void_p, ctypes.POINTER(_Tables)] + [ctypes.c_void_p] * 6
+        L.oracle_matvec.argtypes = [ctypes.c_void_p, ctypes.POINTER(_Tables)] + [ctypes.c_void_p] * 7
+        L.oracle_direct_dl.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                       ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_direct.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                     ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
@@ -72,6 +74,18 @@ def direct(points, q, targets=None):
     tg = np.arange(N, dtype=np.int64) if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
     out = np.zeros(tg.size)
     lib().oracle_direct(N, _ptr(points), _ptr(q), tg.size, _ptr(tg), _ptr(out))
+    return out
+
+
+def direct_dl(points, normals, q, targets=None):
+    """Double layer: p_i = sum_{j: r_ij != 0} q_j (x_i - x_j).n_j / (4 pi r_ij^3)."""
+    points = np.ascontiguousarray(points, dtype=np.float64)
+    normals = np.ascontiguousarray(normals, dtype=np.float64)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    N = points.shape[0]
+    tg = np.arange(N, dtype=np.int64) if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
+    out = np.zeros(tg.size)
+    lib().oracle_direct_dl(N, _ptr(points), _ptr(normals), _ptr(q), tg.size, _ptr(tg), _ptr(out))
     return out
 
 
@@ -108,8 +122,10 @@ class Plan:
         lib().oracle_export_lists(self._h, _ptr(out["U"]), _ptr(out["V"]), _ptr(out["W"]), _ptr(out["X"]))
         return out
 
-    def matvec(self, tables: dict, q, phases: bool = False):
+    def matvec(self, tables: dict, q, phases: bool = False, normals=None):
+        """normals (N x 3, caller order): double-layer sources."""
         q = np.ascontiguousarray(q, dtype=np.float64)
+        nrm = None if normals is None else np.ascontiguousarray(normals, dtype=np.float64)
         keep = []
 
         def arr(name):
@@ -122,7 +138,7 @@ class Plan:
         pot = np.zeros(self.N)
         nb, k = self.counts["nboxes"], tables["k"]
         ph = dict(qhat=np.zeros((nb, k)), lhat=np.zeros((nb, k)), near=np.zeros(self.N), far=np.zeros(self.N)) if phases else {}
-        lib().oracle_matvec(self._h, ctypes.byref(tb), _ptr(q), _ptr(pot), _ptr(ph.get("qhat")),
+        lib().oracle_matvec(self._h, ctypes.byref(tb), _ptr(q), _ptr(nrm), _ptr(pot), _ptr(ph.get("qhat")),
                             _ptr(ph.get("lhat")), _ptr(ph.get("near")), _ptr(ph.get("far")))
         return (pot, ph) if phases else pot
 

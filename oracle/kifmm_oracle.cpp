@@ -9,6 +9,7 @@
 // Paper anchors ("P:n" = /root/reference/PAPER.md line n):
 //   eq_eval           P:65-77   p_i = sum_j G(x_i, y_j) q_j
 //   kernel            P:374     G(x, y) = 1 / (4 pi |x - y|)
+//   double layer      P:458-464 dG/dn(y) in S2T and the first S2M step (eq-doubles2m)
 //   octree            P:79-84   subdivide into 8 until <= s points per leaf
 //   near / far field  P:86-88   N^C: same-level cubes sharing a vertex; I^C = F^C \ F^B
 //   surfaces          P:109-113 UE, DC at (1+d) r; UC, DE at (3-2d) r
@@ -44,6 +45,15 @@ inline double G(double x0, double x1, double x2, double y0, double y1, double y2
   double r = std::sqrt(dx * dx + dy * dy + dz * dz);
   if (r == 0.0) return 0.0;
   return 1.0 / (4.0 * M_PI * r);
+}
+
+inline double Gdl(double x0, double x1, double x2, double y0, double y1, double y2, double n0, double n1, double n2) {
+  // double-layer kernel dG/dn(y) = (x - y) . n(y) / (4 pi |x - y|^3) (eq-doubles2m);
+  // pairs with r == 0 contribute 0 (reading Q1)
+  double dx = x0 - y0, dy = x1 - y1, dz = x2 - y2;
+  double r = std::sqrt(dx * dx + dy * dy + dz * dz);
+  if (r == 0.0) return 0.0;
+  return (dx * n0 + dy * n1 + dz * n2) / (4.0 * M_PI * r * r * r);
 }
 
 struct Box {
@@ -309,6 +319,19 @@ void oracle_direct(int64_t N, const double* pts, const double* q, int64_t ntgt, 
   }
 }
 
+// double-layer direct sum: out[t] = sum_j dG(x_{tgt[t]}, x_j)/dn(x_j) q_j (nrm: N x 3 normals)
+void oracle_direct_dl(int64_t N, const double* pts, const double* nrm, const double* q, int64_t ntgt, const int64_t* tgt,
+                      double* out) {
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < ntgt; ++t) {
+    const double* x = pts + 3 * tgt[t];
+    double acc = 0;
+    for (int64_t j = 0; j < N; ++j)
+      acc += Gdl(x[0], x[1], x[2], pts[3 * j], pts[3 * j + 1], pts[3 * j + 2], nrm[3 * j], nrm[3 * j + 1], nrm[3 * j + 2]) * q[j];
+    out[t] = acc;
+  }
+}
+
 void* oracle_plan(int64_t N, const double* pts, int s, int wx_direct_max) {
   Plan* P = new Plan();
   P->N = N; P->s = s; P->wx_direct_max = wx_direct_max;
@@ -382,7 +405,11 @@ void oracle_export_lists(void* h, int32_t* U, int32_t* V, int32_t* W, int32_t* X
 // operators of P:205-235 / P:315-355).  q and pot are in caller order.
 // Optional phase outputs (may be NULL): qhat [nboxes x k] (level-normalised
 // q^'), lhat [nboxes x k], pot_near / pot_far [N] in SORTED order.
-void oracle_matvec(void* h, const oracle_tables* tb, const double* q, double* pot,
+// nrm (may be NULL): N x 3 source normals in caller order -> double-layer sources: the kernel
+// of every evaluation whose source is an input point (S2M check potential, X check potential,
+// near field) is dG/dn(y) ("only the integral kernel function in S2T translation
+// and the first step in S2M translation should be replaced"); surfaces stay single layer.
+void oracle_matvec(void* h, const oracle_tables* tb, const double* q, const double* nrm, double* pot,
                    double* qhat_out, double* lhat_out, double* near_out, double* far_out) {
   Plan* P = (Plan*)h;
   const int64_t N = P->N;
@@ -394,6 +421,17 @@ void oracle_matvec(void* h, const oracle_tables* tb, const double* q, double* po
   std::vector<double> qs(N);
   for (int64_t i = 0; i < N; ++i) qs[i] = q[P->perm[i]];
   const double* xs = P->xs.data();
+  std::vector<double> ns;  // sorted normals (double layer)
+  if (nrm) {
+    ns.resize(3 * N);
+    for (int64_t i = 0; i < N; ++i)
+      for (int c = 0; c < 3; ++c) ns[3 * i + c] = nrm[3 * (int64_t)P->perm[i] + c];
+  }
+  // source-point kernel: single layer G, or double layer dG/dn(y) with the source's normal
+  auto Gsrc = [&](double x0, double x1, double x2, int j) {
+    return nrm ? Gdl(x0, x1, x2, xs[3 * j], xs[3 * j + 1], xs[3 * j + 2], ns[3 * j], ns[3 * j + 1], ns[3 * j + 2])
+               : G(x0, x1, x2, xs[3 * j], xs[3 * j + 1], xs[3 * j + 2]);
+  };
   std::vector<double> qhat((size_t)nb * k, 0.0), lhat((size_t)nb * k, 0.0);
   std::vector<double> pnear(N, 0.0), pfar(N, 0.0);
   auto npts = [&](int a) { return P->boxes[a].pend - P->boxes[a].pbeg; };
@@ -408,7 +446,7 @@ void oracle_matvec(void* h, const oracle_tables* tb, const double* q, double* po
     for (int i = 0; i < n; ++i) {
       double y0 = B.c[0] + B.r * f_out * g[3 * i], y1 = B.c[1] + B.r * f_out * g[3 * i + 1], y2 = B.c[2] + B.r * f_out * g[3 * i + 2];
       double acc = 0;
-      for (int j = B.pbeg; j < B.pend; ++j) acc += G(y0, y1, y2, xs[3 * j], xs[3 * j + 1], xs[3 * j + 2]) * qs[j];
+      for (int j = B.pbeg; j < B.pend; ++j) acc += Gsrc(y0, y1, y2, j) * qs[j];
       c[i] = acc;
     }
     for (int a = 0; a < k; ++a) {
@@ -460,7 +498,7 @@ void oracle_matvec(void* h, const oracle_tables* tb, const double* q, double* po
       for (int i = 0; i < n; ++i) {
         double y0 = B.c[0] + B.r * f_in * g[3 * i], y1 = B.c[1] + B.r * f_in * g[3 * i + 1], y2 = B.c[2] + B.r * f_in * g[3 * i + 2];
         double acc = 0;
-        for (int j = A.pbeg; j < A.pend; ++j) acc += G(y0, y1, y2, xs[3 * j], xs[3 * j + 1], xs[3 * j + 2]) * qs[j];
+        for (int j = A.pbeg; j < A.pend; ++j) acc += Gsrc(y0, y1, y2, j) * qs[j];
         c[i] = acc;
       }
       for (int r = 0; r < k; ++r) {
@@ -533,7 +571,7 @@ void oracle_matvec(void* h, const oracle_tables* tb, const double* q, double* po
     for (int i = B.pbeg; i < B.pend; ++i) {
       double acc = 0;
       for (auto& rg : ranges)
-        for (int j = rg.first; j < rg.second; ++j) acc += G(xs[3 * i], xs[3 * i + 1], xs[3 * i + 2], xs[3 * j], xs[3 * j + 1], xs[3 * j + 2]) * qs[j];
+        for (int j = rg.first; j < rg.second; ++j) acc += Gsrc(xs[3 * i], xs[3 * i + 1], xs[3 * i + 2], j) * qs[j];
       pnear[i] = acc;
     }
   }
