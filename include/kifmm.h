@@ -4,7 +4,8 @@
  * and its application to BEM"; "P:n" = /root/reference/PAPER.md line n).
  *
  * The library computes one FP64 matrix-vector product with the 3D Laplace
- * single-layer kernel G(x, y) = 1 / (4 pi |x - y|):
+ * single-layer kernel G(x, y) = 1 / (4 pi |x - y|) — or, with source
+ * normals, the double-layer kernel dG/dn(y):
  *
  *     p_i = sum_{j : x_j != x_i} G(x_i, x_j) q_j            (eq_eval)
  *
@@ -92,6 +93,11 @@ typedef struct {
                          by its SVD truncated at eps2 ||K_fat||_2 with eps2 = C2 eps1 / k
                          (eq-vareps2; eps1 = sigma_{k+1} / sigma_1, the stage-1 truncation) and
                          M2L runs as two skinny GEMMs (U^_o (V^_o q)).  0 (default) = off. */
+  const double* normals; /* device, N x 3 FP64, caller order, or NULL.  Non-NULL: double-layer
+                         sources (eq-doubles2m): every evaluation whose source is an
+                         input point (near field S2T, the S2M check potential, the X-list check
+                         potential) uses dG/dn(y) = (x - y).n(y) / (4 pi |x - y|^3); the
+                         translations between surfaces stay single layer.  Copied at setup. */
 } fmm_options;
 
 typedef struct {

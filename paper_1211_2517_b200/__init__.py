@@ -34,7 +34,7 @@ class Options(ctypes.Structure):
                 ("pinv_rcond", ctypes.c_double), ("wx_direct_max", ctypes.c_int),
                 ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
-                ("leaf_ops", ctypes.c_int), ("m2l_c2", ctypes.c_double)]
+                ("leaf_ops", ctypes.c_int), ("m2l_c2", ctypes.c_double), ("normals", ctypes.c_void_p)]
 
 
 class Info(ctypes.Structure):
@@ -193,7 +193,7 @@ class Plan:
     def __init__(self, points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, d: float = 0.1,
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
                  split_phases: bool = False, stream=None, nranks: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None, leaf_ops: int = -1, m2l_c2: float = 0.0):
+                 nccl_id: bytes | None = None, leaf_ops: int = -1, m2l_c2: float = 0.0, normals=None):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -204,6 +204,11 @@ class Plan:
         opt.p, opt.k, opt.leaf_size, opt.d, opt.pinv_rcond = p, k, leaf_size, d, rcond
         opt.wx_direct_max, opt.profile, opt.split_phases = wx_direct_max, int(profile), int(split_phases)
         opt.nranks, opt.rank, opt.leaf_ops, opt.m2l_c2 = nranks, rank, int(leaf_ops), float(m2l_c2)
+        if normals is not None:  # double-layer sources
+            if not (isinstance(normals, torch.Tensor) and normals.is_cuda and tuple(normals.shape) == (self.N, 3)):
+                raise TypeError("normals must be a CUDA tensor [N, 3]")
+            self.normals = normals.contiguous().to(torch.float64)
+            opt.normals = ctypes.c_void_p(self.normals.data_ptr())
         self._keep = []
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -87,6 +87,7 @@ void fmm_default_options(fmm_options* o) {
   o->nccl_id = nullptr;
   o->leaf_ops = -1;
   o->m2l_c2 = 0.0;
+  o->normals = nullptr;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -206,6 +207,10 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   t0 = std::chrono::steady_clock::now();
   if (kifmm::build_tree_device(P, points, st)) return fail(FMM_ECUDA);
   h->tree_ms = ms_since(t0);
+  if (opt->normals) {  // double-layer sources: no symmetric near-field pairs (dG/dn is not symmetric)
+    if (kifmm::sort_normals(P, opt->normals, st)) return fail(FMM_ECUDA);
+    P.sym_opt = 0;
+  }
   t0 = std::chrono::steady_clock::now();
   if (kifmm::build_lists_device(P, st)) return fail(FMM_ECUDA);
   h->lists_ms = ms_since(t0);

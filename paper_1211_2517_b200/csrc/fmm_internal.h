@@ -158,6 +158,7 @@ struct Plan {
   double* d_Ue = nullptr;   // n x kp    (U)
   double* d_surf = nullptr; // n x 3 unit surface grid
   LowRank lr;               // stage-2 M2L (fmm_options.m2l_c2 > 0)
+  double4* d_nrm = nullptr; // sorted source normals: double-layer sources, else NULL
   double m2l_flops = 0;     // algorithmic M2L flops per matvec on this rank
   // work buffers
   double* d_qhat = nullptr;     // nboxes x kp (level-normalised q^')
@@ -225,6 +226,7 @@ struct Plan {
 //                                                   -> allgather potentials (replicated mode)
 //   4 potential in caller order (replicated mode)
 int build_leaf_ops(Plan& P, cudaStream_t st);
+int sort_normals(Plan& P, const double* d_normals, cudaStream_t st);
 int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st);
 constexpr int kNumStages = 5;
 int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st);

@@ -546,26 +546,42 @@ struct EvalArgs {
   double* out;
   int ldo;
   int accumulate;        // k_eval: out += result (leaf-op mode: L2T already stored)
+  const double4* nrm;    // sorted source normals (double layer), else NULL
 };
 
-constexpr int EV_NT = 256;    // threads per target item (default variant)
-constexpr int EV_CH_MAX = 512;  // sources staged per chunk (max over variants)
+// Double-layer source term: q_j (x - y_j).n_j / r^3 with the source staged
+// as (y, q n_x) and (q n_y, q n_z); 1/(4 pi) applied once per sum.
+template <bool CHECK>
+__device__ __forceinline__ double dl_term(double dx, double dy, double dz, double wx, double wy, double wz) {
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const double ri = CHECK ? rinv_or_zero(r2) : rinv_nonzero(r2);
+  const double dot = fma(dz, wz, fma(dy, wy, dx * wx));
+  return dot * ri * (ri * ri);
+}
+
 constexpr int EV_SEG = 128;   // segments per batch (= 32 lanes x 4)
 constexpr int EV_TB = 4;      // targets per thread (register blocking)
 
 // Sum over sources sbuf[j0, j1) step G into TB accumulators; CHECK: pairs with
 // r^2 == 0 contribute 0 (reading Q1), else r > 0 is known.
-template <int TB, bool CHECK>
-__device__ __forceinline__ void eval_sources(const double4* sbuf, int j0, int j1, int G, const double (&x)[TB][3],
-                                             double (&acc)[TB]) {
+template <int TB, bool CHECK, bool DL = false>
+__device__ __forceinline__ void eval_sources(const double4* sbuf, const double2* sbufw, int j0, int j1, int G,
+                                             const double (&x)[TB][3], double (&acc)[TB]) {
 #pragma unroll 2
   for (int j = j0; j < j1; j += G) {
     const double4 sv = sbuf[j];
+    if (DL) {
+      const double2 sw = sbufw[j];
 #pragma unroll
-    for (int u = 0; u < TB; ++u) {
-      const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
-      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      acc[u] = fma(sv.w, CHECK ? rinv_or_zero(r2) : rinv_nonzero(r2), acc[u]);
+      for (int u = 0; u < TB; ++u)
+        acc[u] += dl_term<CHECK>(x[u][0] - sv.x, x[u][1] - sv.y, x[u][2] - sv.z, sv.w, sw.x, sw.y);
+    } else {
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        acc[u] = fma(sv.w, CHECK ? rinv_or_zero(r2) : rinv_nonzero(r2), acc[u]);
+      }
     }
   }
 }
@@ -576,9 +592,10 @@ __device__ __forceinline__ void eval_sources(const double4* sbuf, int j0, int j1
 // concatenated segments, staged EV_CH at a time into a double buffer (point sources
 // by cp.async, so chunk c + 1 lands while chunk c is evaluated); the first `nchk`
 // sources are tested for r = 0.
-template <int TB, int EV_CH>
+template <int TB, int EV_CH, bool DL>
 __device__ __forceinline__ void eval_pass(const EvalArgs& A, const int4& it, int tbeg, int t0, int mm, int sb, int se,
-                                          int nchk, double4 (*sbuf)[EV_CH], double* red, int* s_pref, int4* s_seg) {
+                                          int nchk, double4 (*sbuf)[EV_CH], double2 (*sbufw)[EV_CH], double* red,
+                                          int* s_pref, int4* s_seg) {
   const int NT = blockDim.x;
   const int lane = threadIdx.x & 31;
   const int mq = (mm + TB - 1) / TB;
@@ -608,7 +625,11 @@ __device__ __forceinline__ void eval_pass(const EvalArgs& A, const int4& it, int
       }
       const int4 sg = s_seg[lo];
       const int j = fi - s_pref[lo];
-      if (sg.x == 0) {
+      if (sg.x == 0 && DL) {  // double-layer source: (y, q n_x), (q n_y, q n_z)
+        const double4 p = A.pts[sg.y + j], nv = A.nrm[sg.y + j];
+        sbuf[b][f] = make_double4(p.x, p.y, p.z, p.w * nv.x);
+        sbufw[b][f] = make_double2(p.w * nv.y, p.w * nv.z);
+      } else if (sg.x == 0) {
         const double* src = reinterpret_cast<const double*>(A.pts + sg.y + j);
         double* dst = reinterpret_cast<double*>(&sbuf[b][f]);
         cp_async16(dst, src);
@@ -670,10 +691,10 @@ __device__ __forceinline__ void eval_pass(const EvalArgs& A, const int4& it, int
         const int j0 = gi;
         int jc = j0;
         if (split > 0) {
-          eval_sources<TB, true>(sbuf[b], j0, split, G, x, acc);
+          eval_sources<TB, true, DL>(sbuf[b], sbufw[b], j0, split, G, x, acc);
           jc = j0 + ((split - j0 + G - 1) / G) * G;  // first j >= split in this slice
         }
-        eval_sources<TB, false>(sbuf[b], jc, cn, G, x, acc);
+        eval_sources<TB, false, DL>(sbuf[b], sbufw[b], jc, cn, G, x, acc);
       }
       b ^= 1;
     }
@@ -797,9 +818,10 @@ __global__ void __launch_bounds__(SYM_WARPS * 32, 6) k_p2p_sym(const int2* __res
 //   kind 1: surface of box b, radius r_b * f_out, densities eqd1[a * ldq + m]   (L2T)
 //   kind 2: surface of box b, radius r_b * f_in,  densities eqd2[a * ldq + m]   (W)
 // chk_self: the first m_B sources are the leaf's own points (r = 0 possible).
-template <int NT, int CH>
+template <int NT, int CH, bool DL = false>
 __global__ void __launch_bounds__(NT) k_eval(EvalArgs A, int chk_self) {
   __shared__ __align__(16) double4 sbuf[2][CH];
+  __shared__ __align__(16) double2 sbufw[2][DL ? CH : 1];
   __shared__ double red[EV_TB * NT];
   __shared__ int s_pref[EV_SEG + 1];
   __shared__ int4 s_seg[EV_SEG];
@@ -809,8 +831,10 @@ __global__ void __launch_bounds__(NT) k_eval(EvalArgs A, int chk_self) {
   const int nchk = chk_self ? m : 0;
   for (int t0 = 0; t0 < m; t0 += EV_TB * NT) {
     const int mm = min(m - t0, EV_TB * NT);
-    if (mm >= 12) eval_pass<EV_TB, CH>(A, it, tbeg, t0, mm, sb, se, nchk, sbuf, red, s_pref, s_seg);
-    else eval_pass<2, CH>(A, it, tbeg, t0, mm, sb, se, nchk, sbuf, red, s_pref, s_seg);
+    // (single layer: the weight buffer is a 1-element placeholder, never indexed)
+    double2 (*sw)[CH] = reinterpret_cast<double2 (*)[CH]>(&sbufw[0][0]);
+    if (mm >= 12) eval_pass<EV_TB, CH, DL>(A, it, tbeg, t0, mm, sb, se, nchk, sbuf, sw, red, s_pref, s_seg);
+    else eval_pass<2, CH, DL>(A, it, tbeg, t0, mm, sb, se, nchk, sbuf, sw, red, s_pref, s_seg);
   }
 }
 
@@ -822,9 +846,10 @@ __global__ void __launch_bounds__(NT) k_eval(EvalArgs A, int chk_self) {
 // ----------------------------------------------------------------------------
 constexpr int CHK_WARPS = 8;
 
-template <int CHK_TB>
+template <int CHK_TB, bool DL = false>
 __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) {
   __shared__ double4 ssrc[CHK_WARPS][32];
+  __shared__ double2 ssrcw[CHK_WARPS][DL ? 32 : 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int item = blockIdx.x * CHK_WARPS + w;
   if (item >= nitems) return;
@@ -850,15 +875,31 @@ __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) 
     for (int c0 = 0; c0 < sg.w; c0 += 32) {
       const int cnt = min(32, sg.w - c0);
       __syncwarp();
-      if (lane < cnt) ssrc[w][lane] = A.pts[sg.y + c0 + lane];
+      if (lane < cnt) {
+        const double4 p = A.pts[sg.y + c0 + lane];
+        if (DL) {  // double-layer source: (y, q n_x), (q n_y, q n_z)
+          const double4 nv = A.nrm[sg.y + c0 + lane];
+          ssrc[w][lane] = make_double4(p.x, p.y, p.z, p.w * nv.x);
+          ssrcw[w][lane] = make_double2(p.w * nv.y, p.w * nv.z);
+        } else {
+          ssrc[w][lane] = p;
+        }
+      }
       __syncwarp();
       for (int j = 0; j < cnt; ++j) {
         const double4 sv = ssrc[w][j];
+        if (DL) {
+          const double2 sw = ssrcw[w][j];
 #pragma unroll
-        for (int u = 0; u < CHK_TB; ++u) {
-          const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
-          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-          acc[u] = fma(sv.w, rinv_or_zero(r2), acc[u]);
+          for (int u = 0; u < CHK_TB; ++u)
+            acc[u] += dl_term<true>(x[u][0] - sv.x, x[u][1] - sv.y, x[u][2] - sv.z, sv.w, sw.x, sw.y);
+        } else {
+#pragma unroll
+          for (int u = 0; u < CHK_TB; ++u) {
+            const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            acc[u] = fma(sv.w, rinv_or_zero(r2), acc[u]);
+          }
         }
       }
     }
@@ -886,12 +927,13 @@ __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) 
 // ----------------------------------------------------------------------------
 constexpr int LO_CH = 32;
 
-template <int MODE>
+template <int MODE, bool DL = false>
 __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ items, const double4* __restrict__ pts,
                                                       const double4* __restrict__ geom, const int* __restrict__ pbeg,
                                                       const int* __restrict__ pend, const double* __restrict__ surf,
                                                       int n, int kp, double f, const double* __restrict__ Op, int sa,
-                                                      int si, int own_lo, double* __restrict__ out) {
+                                                      int si, int own_lo, double* __restrict__ out,
+                                                      const double4* __restrict__ nrm = nullptr) {
   extern __shared__ double Gs[];  // n x (LO_CH + 1)
   const int b = items[blockIdx.x].x;
   const double4 gb = geom[b];
@@ -909,7 +951,12 @@ __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ i
         const double dx = gb.x + rad * surf[3 * i] - x.x;
         const double dy = gb.y + rad * surf[3 * i + 1] - x.y;
         const double dz = gb.z + rad * surf[3 * i + 2] - x.z;
-        v = kInv4Pi * rinv_nonzero(fma(dz, dz, fma(dy, dy, dx * dx)));  // surface outside the leaf: r > 0
+        if (DL) {  // S2M of double-layer sources (eq-doubles2m): dG/dn(x_j) at the check point
+          const double4 nv = nrm[p0 + c0 + jj];
+          v = kInv4Pi * dl_term<false>(dx, dy, dz, nv.x, nv.y, nv.z);
+        } else {
+          v = kInv4Pi * rinv_nonzero(fma(dz, dz, fma(dy, dy, dx * dx)));  // surface outside the leaf: r > 0
+        }
       }
       Gs[i * (LO_CH + 1) + jj] = v;
     }
@@ -1012,6 +1059,25 @@ __global__ void k_owned_output(const double* __restrict__ pnear, const double* _
                                double* __restrict__ pot) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < cnt) pot[i] = pfar ? pnear[lo + i] + pfar[lo + i] : pnear[lo + i];
+}
+
+// sorted normals: nrm[i] = (n[perm[i]], 0)
+__global__ void k_sort_normals(const double* __restrict__ n, const int32_t* __restrict__ perm, int64_t N,
+                               double4* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < N) {
+    const int64_t j = perm[i];
+    out[i] = make_double4(n[3 * j], n[3 * j + 1], n[3 * j + 2], 0.0);
+  }
+}
+
+int sort_normals(Plan& P, const double* d_normals, cudaStream_t st) {
+  const int64_t N = P.tree.N;
+  KIFMM_CUDA(cudaMalloc(&P.d_nrm, sizeof(double4) * N));
+  P.allocations.push_back(P.d_nrm);
+  k_sort_normals<<<(int)((N + 255) / 256), 256, 0, st>>>(d_normals, P.tree.d_perm, N, P.d_nrm);
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
 }
 
 __global__ void k_combine(double* __restrict__ pnear, const double* __restrict__ pfar, int lo, int cnt) {
@@ -1351,11 +1417,17 @@ int build_leaf_ops(Plan& P, cudaStream_t st) {
   const Tree& T = P.tree;
   const size_t smem = (size_t)P.n * (LO_CH + 1) * sizeof(double);
   KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const double f = 3.0 - 2.0 * P.d;  // UC and DE halfwidth factor
   if (P.leaf_s2m) {
-    k_leafop_build<0><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
-                                                  P.kp, f, P.d_S, P.np, 1, P.dist.own_lo, P.d_s2m_mat);
+    if (P.d_nrm)
+      k_leafop_build<0, true><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf,
+                                                          P.n, P.kp, f, P.d_S, P.np, 1, P.dist.own_lo, P.d_s2m_mat,
+                                                          P.d_nrm);
+    else
+      k_leafop_build<0><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
+                                                    P.kp, f, P.d_S, P.np, 1, P.dist.own_lo, P.d_s2m_mat);
     KIFMM_CUDA(cudaGetLastError());
   }
   if (P.leaf_l2t) {
@@ -1399,10 +1471,11 @@ int kernels_init() {
 // Evaluation work lists live in the plan; see build_schedules (schedule.cpp).
 // k_eval with 128 threads per target leaf (measured best of 128 / 256 threads and
 // a warp-per-leaf variant; KIFMM_EVAL_NT=256 selects the 256-thread kernel)
-static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st) {
+static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st, bool dl = false) {
   static const int nt = [] { const char* e = std::getenv("KIFMM_EVAL_NT"); return e ? std::atoi(e) : 128; }();
   a.items = P.d_tleaf_items;
-  if (nt == 256) k_eval<256, 512><<<P.n_tleaf, 256, 0, st>>>(a, chk_self);
+  if (dl) k_eval<128, 256, true><<<P.n_tleaf, 128, 0, st>>>(a, chk_self);
+  else if (nt == 256) k_eval<256, 512><<<P.n_tleaf, 256, 0, st>>>(a, chk_self);
   else k_eval<128, 256><<<P.n_tleaf, 128, 0, st>>>(a, chk_self);
 }
 
@@ -1413,7 +1486,7 @@ static int launch_near(const Plan& P, const EvalArgs& ea, cudaStream_t st) {
   if (P.n_tleaf > 0) {
     EvalArgs a = ea;
     a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
-    launch_eval(P, a, 1, st);
+    launch_eval(P, a, 1, st, P.d_nrm != nullptr);  // the near-field sources are input points
     ++g_launches;
     KIFMM_CUDA(cudaGetLastError());
   }
@@ -1433,6 +1506,16 @@ static int launch_sym(const Plan& P, cudaStream_t st) {
 void launch_chk(const EvalArgs& a, int nitems, int n, cudaStream_t st) {
   const int tb = n <= 160 ? (n + 31) / 32 : (n + 63) / 64;
   const int grid = (nitems + CHK_WARPS - 1) / CHK_WARPS, thr = CHK_WARPS * 32;
+  if (a.nrm) {  // double-layer sources
+    switch (std::min(5, std::max(1, tb))) {
+      case 1: k_chk<1, true><<<grid, thr, 0, st>>>(a, nitems); break;
+      case 2: k_chk<2, true><<<grid, thr, 0, st>>>(a, nitems); break;
+      case 3: k_chk<3, true><<<grid, thr, 0, st>>>(a, nitems); break;
+      case 4: k_chk<4, true><<<grid, thr, 0, st>>>(a, nitems); break;
+      default: k_chk<5, true><<<grid, thr, 0, st>>>(a, nitems); break;
+    }
+    return;
+  }
   switch (std::min(5, std::max(1, tb))) {
     case 1: k_chk<1><<<grid, thr, 0, st>>>(a, nitems); break;
     case 2: k_chk<2><<<grid, thr, 0, st>>>(a, nitems); break;
@@ -1473,6 +1556,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
   EvalArgs ea{};
   ea.pts = T.d_pts; ea.geom = T.d_geom; ea.pbeg = T.d_pbeg; ea.pend = T.d_pend;
   ea.surf = P.d_surf; ea.n = n; ea.f_in = 1.0 + P.d; ea.f_out = 3.0 - 2.0 * P.d; ea.ldq = np;
+  ea.nrm = P.d_nrm;  // S2M / X check potentials and the near field use it (double layer)
   // per-plan launch count across stages (plans of a loopback group interleave)
   struct LaunchCount {
     Plan& P;
@@ -1558,14 +1642,15 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       for (auto& g : P.g_l2l)
         if (launch_ggs(g, P.d_L, kp * kp, kp, kp, k, P.d_lhat, kp, P.d_lhat, kp, true, st)) return -3;
       mark(7);
-      // near field alone (split_phases: phase exports)
-      if (P.split_phases && launch_near(P, ea, st)) return -3;
+      // near field as its own pass (split_phases: phase exports; double layer: its own
+      // kernel) unless it runs on the overlapped near stream
+      const bool sep = P.split_phases || P.overlap || P.d_nrm;
+      if (sep && !P.overlap && launch_near(P, ea, st)) return -3;
       // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
       if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
       if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
       // far field of the targets into pot_far when the near field is separate (split or
       // overlapped on the near stream), else everything fused into pot_near
-      const bool sep = P.split_phases || P.overlap;
       double* far_out = sep ? P.d_pot_far : P.d_pot_near;
       // leaf-op mode: L2T as one GEMV per leaf, stored; the evaluation pass below adds to it
       if (P.leaf_l2t && P.n_tleaf > 0) {
@@ -1579,6 +1664,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         EvalArgs a = ea;
         a.items = P.d_tleaf_items;
         a.accumulate = P.leaf_l2t ? 1 : 0;
+        a.nrm = nullptr;  // far sources are equivalent surfaces: single layer
         if (sep) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; }
         else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; }
         a.out = far_out;
@@ -1588,8 +1674,8 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaGetLastError());
       }
       if (!sep && launch_sym(P, st)) return -3;
-      if (P.overlap) {  // join the near stream, then pot_near += pot_far on the owned points
-        KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_join, 0));
+      if (sep && !P.split_phases) {  // [join the near stream,] then pot_near += pot_far on the owned points
+        if (P.overlap) KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_join, 0));
         const int cnt = Dp.own_hi - Dp.own_lo;
         if (cnt > 0) {
           ++g_launches;

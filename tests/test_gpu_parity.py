@@ -226,3 +226,55 @@ def test_stage2_c2_full_size_and_accuracy():
     idx = np.random.default_rng(0).choice(pts.shape[0], 2048, replace=False)
     d = oracle.direct(pts, q, idx)
     assert rel(out[idx], d) <= 1.02 * rel(ref1[idx], d)
+
+
+def _normals_for(case, pts):
+    # outward normals of the sphere cases; seeded random unit normals elsewhere
+    if case in ("sphere6k_s16", "octa_sphere32k"):
+        return pts / np.linalg.norm(pts, axis=1, keepdims=True)
+    rng = np.random.default_rng(11)
+    g = rng.normal(size=pts.shape)
+    return g / np.linalg.norm(g, axis=1, keepdims=True)
+
+
+@pytest.mark.parametrize("case", ["C1", "sphere6k_s16", "clustered4k_s8", "octa_sphere32k", "torus50k"])
+@pytest.mark.parametrize("leaf_ops", [0, 1])
+def test_double_layer_parity(case, leaf_ops):
+    # double-layer sources: the GPU against the oracle's double-layer passes
+    pts, q, p, k, s = CASES[case]()
+    nrm = _normals_for(case, pts)
+    tb = tables(p, k)
+    op = oracle.Plan(pts, s, tb["n"])
+    ref, ph = op.matvec(tb, q, phases=True, normals=nrm)
+    dev = torch.device("cuda:0")
+    gp = K().Plan(torch.from_numpy(pts).to(dev), None, p=p, k=k, leaf_size=s, tables=tb, leaf_ops=leaf_ops,
+                  normals=torch.from_numpy(nrm).to(dev))
+    out = gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
+    assert rel(out, ref) <= TOL
+    gs = K().Plan(torch.from_numpy(pts).to(dev), None, p=p, k=k, leaf_size=s, tables=tb, leaf_ops=leaf_ops,
+                  normals=torch.from_numpy(nrm).to(dev), split_phases=True)
+    gs.matvec(torch.from_numpy(q).to(dev))
+    assert rel(gs.export_phase("near"), ph["near"]) <= TOL
+    amp = {4: 1.0, 6: 1.0, 8: 30.0}[p]
+    assert rel(gs.export_phase("qhat"), ph["qhat"]) <= amp * TOL
+
+
+def test_double_layer_gauss_and_loopback():
+    # Gauss closed form at the centre through the GPU FMM, and a 3-rank loopback partition
+    R = 0.5
+    rng = np.random.default_rng(8)
+    g = rng.normal(size=(8000, 3))
+    nrm = g / np.linalg.norm(g, axis=1, keepdims=True)
+    P = np.vstack([[0.0, 0.0, 0.0], R * nrm])
+    Nn = np.vstack([[0.0, 0.0, 1.0], nrm])
+    q = np.concatenate([[0.0], np.full(8000, 4 * np.pi * R * R / 8000)])
+    tb = tables(8, 100)
+    dev = torch.device("cuda:0")
+    Pt, Nt, Qt = (torch.from_numpy(x).to(dev) for x in (P, Nn, q))
+    out = K().Plan(Pt, None, p=8, k=100, leaf_size=64, tables=tb, normals=Nt).matvec(Qt).cpu().numpy()
+    assert out[0] == pytest.approx(-1.0, abs=5e-5)
+    ref = oracle.Plan(P, 64, tb["n"]).matvec(tb, q, normals=Nn)
+    assert rel(out, ref) <= TOL
+    plans = [K().Plan(Pt, None, p=8, k=100, leaf_size=64, tables=tb, normals=Nt, nranks=3, rank=r) for r in range(3)]
+    for pt in K().fmm_matvec_group(plans, [Qt] * 3, owned=False):
+        assert rel(pt.cpu().numpy(), ref) <= TOL
