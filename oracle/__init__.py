@@ -53,7 +53,11 @@ def lib():
         L.oracle_count.argtypes = [ctypes.c_void_p, ctypes.c_int]
         L.oracle_export_tree.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 8
         L.oracle_export_lists.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 4
-        L.oracle_matvec.argtypes = [ctypes.c_void_p, ctypes.POINTER(_Tables)] + [ctypes.c_void_p] * 7
+        L.oracle_matvec.argtypes = [ctypes.c_void_p, ctypes.POINTER(_Tables)] + [ctypes.c_void_p] * 8
+        L.oracle_tri_integral.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        L.oracle_tri_integral.restype = ctypes.c_double
+        L.oracle_direct_bem.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_direct_dl.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_direct.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
@@ -86,6 +90,25 @@ def direct_dl(points, normals, q, targets=None):
     tg = np.arange(N, dtype=np.int64) if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
     out = np.zeros(tg.size)
     lib().oracle_direct_dl(N, _ptr(points), _ptr(normals), _ptr(q), tg.size, _ptr(tg), _ptr(out))
+    return out
+
+
+def tri_integral(tri, x, self_term: bool = False) -> float:
+    """int_T G(x, y) dy over the flat triangle tri (3 x 3 vertices), reading R-BEM."""
+    t = np.ascontiguousarray(tri, dtype=np.float64).reshape(9)
+    xx = np.ascontiguousarray(x, dtype=np.float64).reshape(3)
+    return lib().oracle_tri_integral(_ptr(t), _ptr(xx), int(self_term))
+
+
+def direct_bem(centroids, tris, q, targets=None):
+    """Dense collocation BEM product: sum_j q_j int_Tj G(x_i, y) dy."""
+    c = np.ascontiguousarray(centroids, dtype=np.float64)
+    t = np.ascontiguousarray(tris, dtype=np.float64).reshape(-1, 9)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    N = c.shape[0]
+    tg = np.arange(N, dtype=np.int64) if targets is None else np.ascontiguousarray(targets, dtype=np.int64)
+    out = np.zeros(tg.size)
+    lib().oracle_direct_bem(N, _ptr(c), _ptr(t), _ptr(q), tg.size, _ptr(tg), _ptr(out))
     return out
 
 
@@ -122,10 +145,12 @@ class Plan:
         lib().oracle_export_lists(self._h, _ptr(out["U"]), _ptr(out["V"]), _ptr(out["W"]), _ptr(out["X"]))
         return out
 
-    def matvec(self, tables: dict, q, phases: bool = False, normals=None):
-        """normals (N x 3, caller order): double-layer sources."""
+    def matvec(self, tables: dict, q, phases: bool = False, normals=None, tris=None):
+        """normals (N x 3, caller order): double-layer sources; tris (N x 9):
+        BEM elements whose centroids are the plan's points."""
         q = np.ascontiguousarray(q, dtype=np.float64)
         nrm = None if normals is None else np.ascontiguousarray(normals, dtype=np.float64)
+        tri = None if tris is None else np.ascontiguousarray(tris, dtype=np.float64).reshape(-1, 9)
         keep = []
 
         def arr(name):
@@ -138,7 +163,7 @@ class Plan:
         pot = np.zeros(self.N)
         nb, k = self.counts["nboxes"], tables["k"]
         ph = dict(qhat=np.zeros((nb, k)), lhat=np.zeros((nb, k)), near=np.zeros(self.N), far=np.zeros(self.N)) if phases else {}
-        lib().oracle_matvec(self._h, ctypes.byref(tb), _ptr(q), _ptr(nrm), _ptr(pot), _ptr(ph.get("qhat")),
+        lib().oracle_matvec(self._h, ctypes.byref(tb), _ptr(q), _ptr(nrm), _ptr(tri), _ptr(pot), _ptr(ph.get("qhat")),
                             _ptr(ph.get("lhat")), _ptr(ph.get("near")), _ptr(ph.get("far")))
         return (pot, ph) if phases else pot
 

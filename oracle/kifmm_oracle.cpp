@@ -56,6 +56,100 @@ inline double Gdl(double x0, double x1, double x2, double y0, double y1, double 
   return (dx * n0 + dy * n1 + dz * n2) / (4.0 * M_PI * r * r * r);
 }
 
+// ---- BEM elements: flat triangles, piecewise-constant density, collocation at
+// centroids.  Element integral of the single-layer kernel, reading R-BEM (the
+// paper specifies no quadrature):
+//   self (x = the element's own collocation point): the analytic flat-triangle value
+//        int_T 1/|x - y| dA = sum over edges of  h_e ln((s2 + r2) / (s1 + r1))
+//        (x in the plane: h_e = distance from x to the edge line, s1, s2 the endpoints'
+//        coordinates along the edge measured from the foot of the perpendicular, r1, r2
+//        their distances to x), divided by 4 pi;
+//   else if |x - centroid| > 2 diam (diam = longest edge): Dunavant's 6-point degree-4 rule;
+//   else: split into 4 (edge midpoints) and recurse, at depth 8 the 6-point rule.
+struct Tri {
+  double v[3][3];
+};
+
+inline double tri_area(const Tri& T) {
+  double a[3], b[3];
+  for (int d = 0; d < 3; ++d) { a[d] = T.v[1][d] - T.v[0][d]; b[d] = T.v[2][d] - T.v[0][d]; }
+  double c0 = a[1] * b[2] - a[2] * b[1], c1 = a[2] * b[0] - a[0] * b[2], c2 = a[0] * b[1] - a[1] * b[0];
+  return 0.5 * std::sqrt(c0 * c0 + c1 * c1 + c2 * c2);
+}
+
+inline double tri_diam(const Tri& T) {
+  double m = 0;
+  for (int e = 0; e < 3; ++e) {
+    const double* p = T.v[e];
+    const double* q = T.v[(e + 1) % 3];
+    double dx = p[0] - q[0], dy = p[1] - q[1], dz = p[2] - q[2];
+    m = std::max(m, std::sqrt(dx * dx + dy * dy + dz * dz));
+  }
+  return m;
+}
+
+// Dunavant (1985) degree-4 rule: barycentric (a, a, 1 - 2a) and permutations
+double tri_rule6(const Tri& T, const double x[3]) {
+  static const double A[2] = {0.445948490915965, 0.091576213509771};
+  static const double W[2] = {0.223381589678011, 0.109951743655322};
+  double acc = 0;
+  for (int g = 0; g < 2; ++g)
+    for (int perm = 0; perm < 3; ++perm) {
+      double l[3] = {A[g], A[g], A[g]};
+      l[perm] = 1.0 - 2.0 * A[g];
+      double y[3];
+      for (int d = 0; d < 3; ++d) y[d] = l[0] * T.v[0][d] + l[1] * T.v[1][d] + l[2] * T.v[2][d];
+      acc += W[g] * G(x[0], x[1], x[2], y[0], y[1], y[2]);
+    }
+  return acc * tri_area(T);
+}
+
+double tri_self(const Tri& T, const double x[3]) {
+  double acc = 0;
+  for (int e = 0; e < 3; ++e) {
+    const double* p1 = T.v[e];
+    const double* p2 = T.v[(e + 1) % 3];
+    double t[3], L = 0;
+    for (int d = 0; d < 3; ++d) { t[d] = p2[d] - p1[d]; L += t[d] * t[d]; }
+    L = std::sqrt(L);
+    for (int d = 0; d < 3; ++d) t[d] /= L;
+    double s1 = 0, s2 = 0, r1 = 0, r2 = 0;
+    for (int d = 0; d < 3; ++d) {
+      s1 += (p1[d] - x[d]) * t[d];
+      s2 += (p2[d] - x[d]) * t[d];
+      r1 += (p1[d] - x[d]) * (p1[d] - x[d]);
+      r2 += (p2[d] - x[d]) * (p2[d] - x[d]);
+    }
+    r1 = std::sqrt(r1);
+    r2 = std::sqrt(r2);
+    const double h = std::sqrt(std::max(0.0, r1 * r1 - s1 * s1));
+    acc += h * std::log((s2 + r2) / (s1 + r1));
+  }
+  return acc / (4.0 * M_PI);
+}
+
+double tri_integral(const Tri& T, const double x[3], int depth) {
+  double c[3];
+  for (int d = 0; d < 3; ++d) c[d] = (T.v[0][d] + T.v[1][d] + T.v[2][d]) / 3.0;
+  double dx = x[0] - c[0], dy = x[1] - c[1], dz = x[2] - c[2];
+  const double dist = std::sqrt(dx * dx + dy * dy + dz * dz);
+  if (depth >= 8 || dist > 2.0 * tri_diam(T)) return tri_rule6(T, x);
+  double m[3][3];
+  for (int e = 0; e < 3; ++e)
+    for (int d = 0; d < 3; ++d) m[e][d] = 0.5 * (T.v[e][d] + T.v[(e + 1) % 3][d]);
+  // children: corner 0 (v0, m01, m20), corner 1 (m01, v1, m12), corner 2 (m20, m12, v2), centre (m01, m12, m20)
+  Tri ch[4];
+  for (int d = 0; d < 3; ++d) {
+    ch[0].v[0][d] = T.v[0][d]; ch[0].v[1][d] = m[0][d]; ch[0].v[2][d] = m[2][d];
+    ch[1].v[0][d] = m[0][d]; ch[1].v[1][d] = T.v[1][d]; ch[1].v[2][d] = m[1][d];
+    ch[2].v[0][d] = m[2][d]; ch[2].v[1][d] = m[1][d]; ch[2].v[2][d] = T.v[2][d];
+    ch[3].v[0][d] = m[0][d]; ch[3].v[1][d] = m[1][d]; ch[3].v[2][d] = m[2][d];
+  }
+  double acc = 0;
+  for (int i = 0; i < 4; ++i) acc += tri_integral(ch[i], x, depth + 1);
+  return acc;
+}
+
 struct Box {
   int level;
   uint64_t key;     // Morton prefix at `level` (3*level bits)
@@ -332,6 +426,27 @@ void oracle_direct_dl(int64_t N, const double* pts, const double* nrm, const dou
   }
 }
 
+// element integral of G over triangle tri (9 doubles) at x; self = 1: analytic (x = centroid)
+double oracle_tri_integral(const double* tri, const double* x, int self) {
+  Tri T;
+  for (int e = 0; e < 3; ++e)
+    for (int d = 0; d < 3; ++d) T.v[e][d] = tri[3 * e + d];
+  return self ? tri_self(T, x) : tri_integral(T, x, 0);
+}
+
+// dense BEM collocation product: out[t] = sum_j A_{tgt[t], j} q_j with
+// A_ij = int_Tj G(x_i, y) dy (analytic self term for j = i); x_i = pts (centroids)
+void oracle_direct_bem(int64_t N, const double* pts, const double* tri, const double* q, int64_t ntgt,
+                       const int64_t* tgt, double* out) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < ntgt; ++t) {
+    const int64_t i = tgt[t];
+    double acc = 0;
+    for (int64_t j = 0; j < N; ++j) acc += oracle_tri_integral(tri + 9 * j, pts + 3 * i, j == i) * q[j];
+    out[t] = acc;
+  }
+}
+
 void* oracle_plan(int64_t N, const double* pts, int s, int wx_direct_max) {
   Plan* P = new Plan();
   P->N = N; P->s = s; P->wx_direct_max = wx_direct_max;
@@ -409,7 +524,11 @@ void oracle_export_lists(void* h, int32_t* U, int32_t* V, int32_t* W, int32_t* X
 // of every evaluation whose source is an input point (S2M check potential, X check potential,
 // near field) is dG/dn(y) ("only the integral kernel function in S2T translation
 // and the first step in S2M translation should be replaced"); surfaces stay single layer.
-void oracle_matvec(void* h, const oracle_tables* tb, const double* q, const double* nrm, double* pot,
+// tri (may be NULL): N x 9 triangle vertices in caller order -> BEM elements:
+// the points are the elements' centroids (collocation points) and every evaluation whose
+// source is an element integrates G over it (reading R-BEM): S2T, the S2M check
+// potential and the X check potential.
+void oracle_matvec(void* h, const oracle_tables* tb, const double* q, const double* nrm, const double* tri, double* pot,
                    double* qhat_out, double* lhat_out, double* near_out, double* far_out) {
   Plan* P = (Plan*)h;
   const int64_t N = P->N;
@@ -427,11 +546,24 @@ void oracle_matvec(void* h, const oracle_tables* tb, const double* q, const doub
     for (int64_t i = 0; i < N; ++i)
       for (int c = 0; c < 3; ++c) ns[3 * i + c] = nrm[3 * (int64_t)P->perm[i] + c];
   }
-  // source-point kernel: single layer G, or double layer dG/dn(y) with the source's normal
-  auto Gsrc = [&](double x0, double x1, double x2, int j) {
+  std::vector<Tri> ts;  // sorted triangles (BEM)
+  if (tri) {
+    ts.resize(N);
+    for (int64_t i = 0; i < N; ++i)
+      for (int e = 0; e < 3; ++e)
+        for (int c = 0; c < 3; ++c) ts[i].v[e][c] = tri[9 * (int64_t)P->perm[i] + 3 * e + c];
+  }
+  // source kernel: single layer G, double layer dG/dn(y), or (BEM) the element integral;
+  // self = the target is source j's own collocation point
+  auto Gsrc_t = [&](double x0, double x1, double x2, int j, bool self) {
+    if (tri) {
+      const double x[3] = {x0, x1, x2};
+      return self ? tri_self(ts[j], x) : tri_integral(ts[j], x, 0);
+    }
     return nrm ? Gdl(x0, x1, x2, xs[3 * j], xs[3 * j + 1], xs[3 * j + 2], ns[3 * j], ns[3 * j + 1], ns[3 * j + 2])
                : G(x0, x1, x2, xs[3 * j], xs[3 * j + 1], xs[3 * j + 2]);
   };
+  auto Gsrc = [&](double x0, double x1, double x2, int j) { return Gsrc_t(x0, x1, x2, j, false); };
   std::vector<double> qhat((size_t)nb * k, 0.0), lhat((size_t)nb * k, 0.0);
   std::vector<double> pnear(N, 0.0), pfar(N, 0.0);
   auto npts = [&](int a) { return P->boxes[a].pend - P->boxes[a].pbeg; };
@@ -571,7 +703,7 @@ void oracle_matvec(void* h, const oracle_tables* tb, const double* q, const doub
     for (int i = B.pbeg; i < B.pend; ++i) {
       double acc = 0;
       for (auto& rg : ranges)
-        for (int j = rg.first; j < rg.second; ++j) acc += Gsrc(xs[3 * i], xs[3 * i + 1], xs[3 * i + 2], j) * qs[j];
+        for (int j = rg.first; j < rg.second; ++j) acc += Gsrc_t(xs[3 * i], xs[3 * i + 1], xs[3 * i + 2], j, j == i) * qs[j];
       pnear[i] = acc;
     }
   }

@@ -38,6 +38,38 @@ def uniform_cube(n: int, seed: int = 0):
     return pts, q
 
 
+def octahedron_mesh(levels: int) -> np.ndarray:
+    """Triangles (F x 3 x 3) of an octahedron whose 8 faces are each split into 4^levels
+    triangles (midpoint subdivision), vertices projected to the unit sphere; outward
+    orientation (counter-clockwise seen from outside)."""
+    v = np.array([[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]], float)
+    faces = np.array([[0, 2, 4], [2, 1, 4], [1, 3, 4], [3, 0, 4],
+                      [2, 0, 5], [1, 2, 5], [3, 1, 5], [0, 3, 5]])
+    tri = v[faces]  # (F, 3, 3)
+    for _ in range(levels):
+        a, b, c = tri[:, 0], tri[:, 1], tri[:, 2]
+        ab, bc, ca = a + b, b + c, c + a
+        ab /= np.linalg.norm(ab, axis=1, keepdims=True)
+        bc /= np.linalg.norm(bc, axis=1, keepdims=True)
+        ca /= np.linalg.norm(ca, axis=1, keepdims=True)
+        tri = np.concatenate([np.stack([a, ab, ca], 1), np.stack([ab, b, bc], 1),
+                              np.stack([ca, bc, c], 1), np.stack([ab, bc, ca], 1)], 0)
+    return tri
+
+
+def sphere_bem(levels: int, radius: float = 1.0, seed: int = 0):
+    """BEM input: flat triangles of the refined octahedron scaled to `radius`
+    (N x 9, caller order), their centroids (the collocation points) and densities
+    q = cos(3 theta) + N(0, 0.1) (the C3 recipe, without jitter: the points must be the
+    elements' centroids)."""
+    rng = np.random.default_rng(seed)
+    tri = radius * octahedron_mesh(levels)
+    cen = tri.mean(axis=1)
+    theta = np.arccos(np.clip(cen[:, 2] / np.linalg.norm(cen, axis=1), -1.0, 1.0))
+    q = np.cos(3.0 * theta) + rng.normal(0.0, 0.1, cen.shape[0])
+    return np.ascontiguousarray(tri.reshape(-1, 9)), np.ascontiguousarray(cen), q
+
+
 def _octahedron_centroids(levels: int) -> np.ndarray:
     """Centroids of an octahedron whose 8 faces are each split into 4^levels
     triangles (midpoint subdivision), vertices projected to the unit sphere."""
