@@ -98,6 +98,16 @@ typedef struct {
                          input point (near field S2T, the S2M check potential, the X-list check
                          potential) uses dG/dn(y) = (x - y).n(y) / (4 pi |x - y|^3); the
                          translations between surfaces stay single layer.  Copied at setup. */
+  const double* triangles; /* device, N x 9 FP64 (3 vertices), caller order, or NULL.  Non-NULL:
+                         BEM collocation: source j is the flat triangle j with
+                         piecewise-constant density, the points passed to setup are the
+                         triangles' centroids (collocation points), and every evaluation whose
+                         source is an element integrates G over it (analytic self term, 6-point
+                         rule, subdivision: reading R-BEM).  Use d = C_d / sqrt(s);
+                         the overhang of elements beyond their leaves is reported in
+                         fmm_info.bem_extrusion, setup fails (FMM_EINVAL) if an element reaches
+                         its leaf's upward check surface.  The near-field matrix is built at setup
+                         (FMM_ENOMEM if it does not fit).  Single GPU. */
 } fmm_options;
 
 typedef struct {
@@ -123,6 +133,9 @@ typedef struct {
                                  sum over V pairs of 2 k^2 (dense cores) or 4 k r_o (stage 2) */
   double m2l_eps2;            /* stage-2 threshold relative to ||K_fat||_2 (0: off) */
   double m2l_rank_mean;       /* mean stage-2 rank over the 316 offsets (k when off) */
+  int64_t bem_near_bytes;     /* BEM near-field matrix bytes (0: point sources) */
+  double bem_extrusion;       /* BEM: largest element overhang beyond a leaf, in leaf halfwidths
+                                 (the surface condition of P:389-411 asks for < d) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

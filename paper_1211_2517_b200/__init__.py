@@ -34,7 +34,8 @@ class Options(ctypes.Structure):
                 ("pinv_rcond", ctypes.c_double), ("wx_direct_max", ctypes.c_int),
                 ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
-                ("leaf_ops", ctypes.c_int), ("m2l_c2", ctypes.c_double), ("normals", ctypes.c_void_p)]
+                ("leaf_ops", ctypes.c_int), ("m2l_c2", ctypes.c_double), ("normals", ctypes.c_void_p),
+                ("triangles", ctypes.c_void_p)]
 
 
 class Info(ctypes.Structure):
@@ -51,7 +52,8 @@ class Info(ctypes.Structure):
                 ("ghost_q_recv", ctypes.c_int64), ("ghost_q_send", ctypes.c_int64),
                 ("ghost_d_recv", ctypes.c_int64), ("ghost_d_send", ctypes.c_int64), ("nV_local", ctypes.c_int64),
                 ("leaf_op_bytes", ctypes.c_int64), ("m2l_flops", ctypes.c_double), ("m2l_eps2", ctypes.c_double),
-                ("m2l_rank_mean", ctypes.c_double)]
+                ("m2l_rank_mean", ctypes.c_double), ("bem_near_bytes", ctypes.c_int64),
+                ("bem_extrusion", ctypes.c_double)]
 
 
 # phases of fmm_matvec (profile=True): the near field is evaluated in the "eval" pass together with
@@ -193,7 +195,8 @@ class Plan:
     def __init__(self, points, densities=None, p: int = 6, k: int = 60, leaf_size: int = 128, d: float = 0.1,
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
                  split_phases: bool = False, stream=None, nranks: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None, leaf_ops: int = -1, m2l_c2: float = 0.0, normals=None):
+                 nccl_id: bytes | None = None, leaf_ops: int = -1, m2l_c2: float = 0.0, normals=None,
+                 triangles=None):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -209,6 +212,12 @@ class Plan:
                 raise TypeError("normals must be a CUDA tensor [N, 3]")
             self.normals = normals.contiguous().to(torch.float64)
             opt.normals = ctypes.c_void_p(self.normals.data_ptr())
+        if triangles is not None:  # BEM elements; points = their centroids
+            if not (isinstance(triangles, torch.Tensor) and triangles.is_cuda and triangles.shape[0] == self.N
+                    and triangles.numel() == 9 * self.N):
+                raise TypeError("triangles must be a CUDA tensor [N, 9] (or [N, 3, 3])")
+            self.triangles = triangles.contiguous().to(torch.float64)
+            opt.triangles = ctypes.c_void_p(self.triangles.data_ptr())
         self._keep = []
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

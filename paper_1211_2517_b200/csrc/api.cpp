@@ -88,6 +88,7 @@ void fmm_default_options(fmm_options* o) {
   o->leaf_ops = -1;
   o->m2l_c2 = 0.0;
   o->normals = nullptr;
+  o->triangles = nullptr;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -207,15 +208,29 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   t0 = std::chrono::steady_clock::now();
   if (kifmm::build_tree_device(P, points, st)) return fail(FMM_ECUDA);
   h->tree_ms = ms_since(t0);
+  if (opt->normals && opt->triangles) {
+    set_error("fmm_setup: normals (double layer) and triangles (BEM) are exclusive");
+    return fail(FMM_EINVAL);
+  }
   if (opt->normals) {  // double-layer sources: no symmetric near-field pairs (dG/dn is not symmetric)
     if (kifmm::sort_normals(P, opt->normals, st)) return fail(FMM_ECUDA);
     P.sym_opt = 0;
+  }
+  if (opt->triangles) {  // BEM elements: collocation at the points (= centroids), element integrals
+    if (opt->nranks > 1 || P.overlap) {
+      set_error("fmm_setup: BEM elements are single-GPU in this build");
+      return fail(FMM_EINVAL);
+    }
+    P.bem = true;
+    P.sym_opt = 0;
+    if (kifmm::bem_sort_triangles(P, opt->triangles, st)) return fail(FMM_ECUDA);
+    if (int rc = kifmm::bem_check_enclosure(P, st)) return fail(rc == -1 ? FMM_EINVAL : FMM_ECUDA);
   }
   t0 = std::chrono::steady_clock::now();
   if (kifmm::build_lists_device(P, st)) return fail(FMM_ECUDA);
   h->lists_ms = ms_since(t0);
   t0 = std::chrono::steady_clock::now();
-  if (kifmm::build_schedules(P, st)) return fail(FMM_ECUDA);
+  if (int rc = kifmm::build_schedules(P, st)) return fail(rc == -4 ? FMM_ENOMEM : FMM_ECUDA);
   h->schedule_ms = ms_since(t0);
   h->part.view(&P.dist);
   if (opt->nccl_id) {  // (a one-rank communicator is allowed: it exercises the transport setup)
@@ -508,6 +523,8 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
   info->ghost_d_send = P.xd.nsend;
   info->nV_local = P.nV_local;
   info->leaf_op_bytes = P.leaf_op_bytes;
+  info->bem_near_bytes = P.bem_near_bytes;
+  info->bem_extrusion = P.bem_extrusion;
   info->m2l_flops = P.m2l_flops;
   info->m2l_eps2 = P.tables.eps2;
   {

@@ -159,6 +159,13 @@ struct Plan {
   double* d_surf = nullptr; // n x 3 unit surface grid
   LowRank lr;               // stage-2 M2L (fmm_options.m2l_c2 > 0)
   double4* d_nrm = nullptr; // sorted source normals: double-layer sources, else NULL
+  // BEM elements: sorted triangles (3 x double4 each), near-field block matrix
+  bool bem = false;
+  double4* d_tri = nullptr;
+  double* d_bem_A = nullptr;
+  int64_t* d_bem_moff = nullptr;  // matrix offset per near segment
+  int64_t bem_near_bytes = 0;
+  double bem_extrusion = 0;       // max over leaves of (vertex distance / r) - 1 (surface condition)
   double m2l_flops = 0;     // algorithmic M2L flops per matvec on this rank
   // work buffers
   double* d_qhat = nullptr;     // nboxes x kp (level-normalised q^')
@@ -227,6 +234,10 @@ struct Plan {
 //   4 potential in caller order (replicated mode)
 int build_leaf_ops(Plan& P, cudaStream_t st);
 int sort_normals(Plan& P, const double* d_normals, cudaStream_t st);
+int bem_sort_triangles(Plan& P, const double* d_tri_caller, cudaStream_t st);
+int bem_check_enclosure(Plan& P, cudaStream_t st);
+int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st);
+int bem_near_matvec(const Plan& P, cudaStream_t st);
 int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st);
 constexpr int kNumStages = 5;
 int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st);

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "bem.cuh"
 #include "common.cuh"
 #include "fmm_internal.h"
 
@@ -547,6 +548,7 @@ struct EvalArgs {
   int ldo;
   int accumulate;        // k_eval: out += result (leaf-op mode: L2T already stored)
   const double4* nrm;    // sorted source normals (double layer), else NULL
+  const double4* tri;    // sorted triangles (BEM elements), else NULL
 };
 
 // Double-layer source term: q_j (x - y_j).n_j / r^3 with the source staged
@@ -846,6 +848,29 @@ __global__ void __launch_bounds__(NT) k_eval(EvalArgs A, int chk_self) {
 // ----------------------------------------------------------------------------
 constexpr int CHK_WARPS = 8;
 
+// BEM X-list check potentials (P:445-456 restated for S2L): one warp per item, each lane
+// CHK_TB check points, the source elements' integrals by bem_integral
+template <int CHK_TB>
+__global__ void __launch_bounds__(CHK_WARPS * 32) k_chk_bem(EvalArgs A, int nitems) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int item = blockIdx.x * CHK_WARPS + w;
+  if (item >= nitems) return;
+  const int4 it = A.items[item];
+  const double4 gb = A.geom[it.x];
+  const int4 sg = A.segs[A.seg_off[item]];
+  const double rad = gb.w * A.tgt_f;
+  for (int r0 = 0; r0 < A.n; r0 += 32 * CHK_TB)
+    for (int u = 0; u < CHK_TB; ++u) {
+      const int i = r0 + lane + 32 * u;
+      if (i >= A.n) continue;
+      const double x[3] = {gb.x + rad * A.surf[3 * i], gb.y + rad * A.surf[3 * i + 1], gb.z + rad * A.surf[3 * i + 2]};
+      double acc = 0.0;
+      for (int j = 0; j < sg.w; ++j)
+        acc += bem_integral(load_tri(A.tri + 3 * (int64_t)(sg.y + j)), x, false) * A.pts[sg.y + j].w;
+      A.out[(size_t)it.y * A.ldo + i] = acc;
+    }
+}
+
 template <int CHK_TB, bool DL = false>
 __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) {
   __shared__ double4 ssrc[CHK_WARPS][32];
@@ -927,13 +952,14 @@ __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) 
 // ----------------------------------------------------------------------------
 constexpr int LO_CH = 32;
 
-template <int MODE, bool DL = false>
+template <int MODE, bool DL = false, bool BEM = false>
 __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ items, const double4* __restrict__ pts,
                                                       const double4* __restrict__ geom, const int* __restrict__ pbeg,
                                                       const int* __restrict__ pend, const double* __restrict__ surf,
                                                       int n, int kp, double f, const double* __restrict__ Op, int sa,
                                                       int si, int own_lo, double* __restrict__ out,
-                                                      const double4* __restrict__ nrm = nullptr) {
+                                                      const double4* __restrict__ nrm = nullptr,
+                                                      const double4* __restrict__ tri = nullptr) {
   extern __shared__ double Gs[];  // n x (LO_CH + 1)
   const int b = items[blockIdx.x].x;
   const double4 gb = geom[b];
@@ -951,7 +977,10 @@ __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ i
         const double dx = gb.x + rad * surf[3 * i] - x.x;
         const double dy = gb.y + rad * surf[3 * i + 1] - x.y;
         const double dz = gb.z + rad * surf[3 * i + 2] - x.z;
-        if (DL) {  // S2M of double-layer sources (eq-doubles2m): dG/dn(x_j) at the check point
+        if (BEM) {  // S2M by element integration (eq s2meval)
+          const double cx[3] = {gb.x + rad * surf[3 * i], gb.y + rad * surf[3 * i + 1], gb.z + rad * surf[3 * i + 2]};
+          v = bem_integral(load_tri(tri + 3 * (int64_t)(p0 + c0 + jj)), cx, false);
+        } else if (DL) {  // S2M of double-layer sources (eq-doubles2m): dG/dn(x_j) at the check point
           const double4 nv = nrm[p0 + c0 + jj];
           v = kInv4Pi * dl_term<false>(dx, dy, dz, nv.x, nv.y, nv.z);
         } else {
@@ -1418,10 +1447,15 @@ int build_leaf_ops(Plan& P, cudaStream_t st) {
   const size_t smem = (size_t)P.n * (LO_CH + 1) * sizeof(double);
   KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const double f = 3.0 - 2.0 * P.d;  // UC and DE halfwidth factor
   if (P.leaf_s2m) {
-    if (P.d_nrm)
+    if (P.bem)
+      k_leafop_build<0, false, true><<<P.n_s2m, 256, smem, st>>>(
+          P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n, P.kp, f, P.d_S, P.np, 1, P.dist.own_lo,
+          P.d_s2m_mat, nullptr, P.d_tri);
+    else if (P.d_nrm)
       k_leafop_build<0, true><<<P.n_s2m, 256, smem, st>>>(P.d_s2m_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf,
                                                           P.n, P.kp, f, P.d_S, P.np, 1, P.dist.own_lo, P.d_s2m_mat,
                                                           P.d_nrm);
@@ -1506,6 +1540,10 @@ static int launch_sym(const Plan& P, cudaStream_t st) {
 void launch_chk(const EvalArgs& a, int nitems, int n, cudaStream_t st) {
   const int tb = n <= 160 ? (n + 31) / 32 : (n + 63) / 64;
   const int grid = (nitems + CHK_WARPS - 1) / CHK_WARPS, thr = CHK_WARPS * 32;
+  if (a.tri) {  // BEM elements: element integrals
+    k_chk_bem<2><<<grid, thr, 0, st>>>(a, nitems);
+    return;
+  }
   if (a.nrm) {  // double-layer sources
     switch (std::min(5, std::max(1, tb))) {
       case 1: k_chk<1, true><<<grid, thr, 0, st>>>(a, nitems); break;
@@ -1557,6 +1595,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
   ea.pts = T.d_pts; ea.geom = T.d_geom; ea.pbeg = T.d_pbeg; ea.pend = T.d_pend;
   ea.surf = P.d_surf; ea.n = n; ea.f_in = 1.0 + P.d; ea.f_out = 3.0 - 2.0 * P.d; ea.ldq = np;
   ea.nrm = P.d_nrm;  // S2M / X check potentials and the near field use it (double layer)
+  ea.tri = P.d_tri;  // BEM: X check potentials by element integration
   // per-plan launch count across stages (plans of a loopback group interleave)
   struct LaunchCount {
     Plan& P;
@@ -1644,8 +1683,13 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       mark(7);
       // near field as its own pass (split_phases: phase exports; double layer: its own
       // kernel) unless it runs on the overlapped near stream
-      const bool sep = P.split_phases || P.overlap || P.d_nrm;
-      if (sep && !P.overlap && launch_near(P, ea, st)) return -3;
+      const bool sep = P.split_phases || P.overlap || P.d_nrm || P.bem;
+      if (P.bem) {  // BEM near field: the precomputed element-integral blocks
+        ++g_launches;
+        if (bem_near_matvec(P, st)) return -3;
+      } else if (sep && !P.overlap && launch_near(P, ea, st)) {
+        return -3;
+      }
       // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
       if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
       if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
@@ -1665,6 +1709,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         a.items = P.d_tleaf_items;
         a.accumulate = P.leaf_l2t ? 1 : 0;
         a.nrm = nullptr;  // far sources are equivalent surfaces: single layer
+        a.tri = nullptr;
         if (sep) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; }
         else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; }
         a.out = far_out;

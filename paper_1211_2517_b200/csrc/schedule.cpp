@@ -114,7 +114,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
     const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot);
     const bool on = P.leaf_ops_opt > 0, au = P.leaf_ops_opt < 0;
-    P.leaf_s2m = on || (au && one <= budget);
+    P.leaf_s2m = on || P.bem || (au && one <= budget);  // BEM: S2M by element integration, always an operator
     P.leaf_l2t = on || (au && one * (P.leaf_s2m ? 2 : 1) <= budget);
   }
 
@@ -233,9 +233,21 @@ int build_schedules(Plan& P, cudaStream_t st) {
   if (upload(P, &P.d_sym, sympairs, st)) return -3;
 
   P.n_near_seg = (int)near_seg.size();
+  if (P.bem) {  // near-field block matrix (S2T by element integration)
+    std::vector<int4> blocks;
+    blocks.reserve(near_seg.size());
+    for (int i = 0; i < nt; ++i) {
+      const int b = titems[i].x;
+      for (int s = near_off[i]; s < near_off[i + 1]; ++s)
+        blocks.push_back(make_int4(T.pbeg[b], npts(b), near_seg[s].y, near_seg[s].w));
+    }
+    if (upload(P, &P.d_near_seg, near_seg, st) || upload(P, &P.d_near_off, near_off, st)) return -3;
+    if (int rc = bem_build_near(P, blocks, st)) return rc;
+  }
   P.n_far_seg = (int)far_seg.size();
-  if (upload(P, &P.d_tleaf_items, titems, st) || upload(P, &P.d_near_off, near_off, st) ||
-      upload(P, &P.d_near_seg, near_seg, st) || upload(P, &P.d_far_off, far_off, st) ||
+  if (upload(P, &P.d_tleaf_items, titems, st) ||
+      (!P.bem && (upload(P, &P.d_near_off, near_off, st) || upload(P, &P.d_near_seg, near_seg, st))) ||
+      upload(P, &P.d_far_off, far_off, st) ||
       upload(P, &P.d_far_seg, far_seg, st) || upload(P, &P.d_all_off, all_off, st) ||
       upload(P, &P.d_all_seg, all_seg, st))
     return -3;
