@@ -47,8 +47,8 @@ __global__ void k_enclosure(const int* __restrict__ leaves, int nleaves, const d
   if (lane == 0) ratio[w] = m / g.w;
 }
 
-// one CTA per near block (target leaf t, source range [a, a + len)): row-major entries
-// A[off + i * len + j] = int_{T_{a+j}} G(x_{tb+i}, y) dy, analytic when tb + i == a + j
+// one CTA per near block (target leaf t, source range [a, a + len)): column-major entries
+// A[off + j * m + i] = int_{T_{a+j}} G(x_{tb+i}, y) dy, analytic when tb + i == a + j
 __global__ void __launch_bounds__(128) k_bem_near_build(const int4* __restrict__ blocks, const int64_t* __restrict__ off,
                                                         int nblocks, const double4* __restrict__ pts,
                                                         const double4* __restrict__ tri, double* __restrict__ A) {
@@ -58,36 +58,55 @@ __global__ void __launch_bounds__(128) k_bem_near_build(const int4* __restrict__
   const int64_t o = off[bi];
   const int64_t cnt = (int64_t)bk.y * bk.w;
   for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
-    const int i = (int)(e / bk.w), j = (int)(e - (int64_t)i * bk.w);
+    const int j = (int)(e / bk.y), i = (int)(e - (int64_t)j * bk.y);
     const double4 p = pts[bk.x + i];
     const double x[3] = {p.x, p.y, p.z};
     A[o + e] = bem_integral(load_tri(tri + 3 * (int64_t)(bk.z + j)), x, bk.x + i == bk.z + j);
   }
 }
 
-// near field: pot[tb + i] = sum over the leaf's blocks of A[i][:] . q[a : a + len]; one CTA
-// (4 warps) per target leaf, a warp per row, lanes over the columns (coalesced A rows)
-constexpr int BN_WARPS = 4;
-__global__ void __launch_bounds__(BN_WARPS * 32) k_bem_near(const int4* __restrict__ items, const int* __restrict__ pbeg,
-                                                           const int* __restrict__ pend, const int* __restrict__ seg_off,
-                                                           const int4* __restrict__ segs, const int64_t* __restrict__ moff,
-                                                           const double4* __restrict__ pts, const double* __restrict__ A,
-                                                           double* __restrict__ pot) {
+// near field: pot[tb + i] = sum over the leaf's blocks of A[:, i] . q[a : a + len]; one CTA
+// per target leaf; thread (ti, gi) owns target t0 + ti and the source slice j = gi (mod G),
+// so a warp reads contiguous runs of a column-major block; slices summed in shared memory
+constexpr int BN_NT = 128;
+__global__ void __launch_bounds__(BN_NT) k_bem_near(const int4* __restrict__ items, const int* __restrict__ pbeg,
+                                                    const int* __restrict__ pend, const int* __restrict__ seg_off,
+                                                    const int4* __restrict__ segs, const int64_t* __restrict__ moff,
+                                                    const double4* __restrict__ pts, const double* __restrict__ A,
+                                                    double* __restrict__ pot) {
+  __shared__ double red[BN_NT];
   const int item = blockIdx.x;
   const int b = items[item].x;
   const int tb = pbeg[b], m = pend[b] - tb;
   const int s0 = seg_off[item], s1 = seg_off[item + 1];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = w; i < m; i += BN_WARPS) {
+  for (int t0 = 0; t0 < m; t0 += BN_NT) {
+    const int mm = min(BN_NT, m - t0);
+    const int G = BN_NT / mm;
+    const int ti = threadIdx.x % mm, gi = threadIdx.x / mm;
     double acc = 0.0;
-    for (int s = s0; s < s1; ++s) {
-      const int4 sg = segs[s];
-      const double* row = A + moff[s] + (int64_t)i * sg.w;
-      for (int j = lane; j < sg.w; j += 32) acc = fma(__ldcs(row + j), pts[sg.y + j].w, acc);
+    if (gi < G) {
+      for (int s = s0; s < s1; ++s) {
+        const int4 sg = segs[s];
+        const double* col = A + moff[s] + t0 + ti;
+        double acc2 = 0.0;
+        int j = gi;
+#pragma unroll 4
+        for (; j + G < sg.w; j += 2 * G) {  // two independent chains
+          acc = fma(__ldcs(col + (int64_t)j * m), pts[sg.y + j].w, acc);
+          acc2 = fma(__ldcs(col + (int64_t)(j + G) * m), pts[sg.y + j + G].w, acc2);
+        }
+        if (j < sg.w) acc = fma(__ldcs(col + (int64_t)j * m), pts[sg.y + j].w, acc);
+        acc += acc2;
+      }
     }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) pot[tb + i] = acc;
+    __syncthreads();
+    red[threadIdx.x] = gi < G ? acc : 0.0;
+    __syncthreads();
+    if (threadIdx.x < mm) {
+      double sum = 0.0;
+      for (int g = 0; g < G; ++g) sum += red[g * mm + threadIdx.x];
+      pot[tb + t0 + threadIdx.x] = sum;
+    }
   }
 }
 
@@ -170,7 +189,7 @@ int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
 
 int bem_near_matvec(const Plan& P, cudaStream_t st) {
   if (P.n_tleaf == 0) return 0;
-  k_bem_near<<<P.n_tleaf, BN_WARPS * 32, 0, st>>>(P.d_tleaf_items, P.tree.d_pbeg, P.tree.d_pend, P.d_near_off,
+  k_bem_near<<<P.n_tleaf, BN_NT, 0, st>>>(P.d_tleaf_items, P.tree.d_pbeg, P.tree.d_pend, P.d_near_off,
                                                   P.d_near_seg, P.d_bem_moff, P.tree.d_pts, P.d_bem_A, P.d_pot_near);
   KIFMM_CUDA(cudaGetLastError());
   return 0;

@@ -191,6 +191,13 @@ struct Plan {
   // (kp-major within a leaf block); both indexed by sorted point - own_lo
   int leaf_ops_opt = -1;      // -1 auto, 0 off, 1 on
   bool leaf_s2m = false, leaf_l2t = false;  // which of the two operators are used
+  // X-list operators (same budget): per non-direct X pair (target B, source leaf A) the
+  // k x m_A matrix U^T G_src(DC_B, sources of A), point-major rows of kp at x_moff[row]
+  bool leaf_x = false;
+  double* d_x_mat = nullptr;
+  int64_t* d_x_moff = nullptr;
+  int n_xt = 0;
+  int4* d_xt_items = nullptr;   // (target box, first row, end row, 0)
   double* d_s2m_mat = nullptr;
   double* d_l2t_mat = nullptr;
   int64_t leaf_op_bytes = 0;
@@ -233,6 +240,7 @@ struct Plan {
 //                                                   -> allgather potentials (replicated mode)
 //   4 potential in caller order (replicated mode)
 int build_leaf_ops(Plan& P, cudaStream_t st);
+int build_x_ops(Plan& P, cudaStream_t st);
 int sort_normals(Plan& P, const double* d_normals, cudaStream_t st);
 int bem_sort_triangles(Plan& P, const double* d_tri_caller, cudaStream_t st);
 int bem_check_enclosure(Plan& P, cudaStream_t st);

@@ -959,11 +959,16 @@ __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ i
                                                       int n, int kp, double f, const double* __restrict__ Op, int sa,
                                                       int si, int own_lo, double* __restrict__ out,
                                                       const double4* __restrict__ nrm = nullptr,
-                                                      const double4* __restrict__ tri = nullptr) {
+                                                      const double4* __restrict__ tri = nullptr,
+                                                      const int4* __restrict__ xsegs = nullptr,
+                                                      const int64_t* __restrict__ xmoff = nullptr) {
   extern __shared__ double Gs[];  // n x (LO_CH + 1)
+  // MODE 0/1: the check surface and the sources are the leaf's; MODE 2 (X operator of row
+  // blockIdx.x): the check surface is the target box's, the sources the X source leaf's
   const int b = items[blockIdx.x].x;
   const double4 gb = geom[b];
-  const int p0 = pbeg[b], m = pend[b] - p0;
+  const int p0 = MODE == 2 ? xsegs[blockIdx.x].y : pbeg[b];
+  const int m = MODE == 2 ? xsegs[blockIdx.x].w : pend[b] - p0;
   const double rad = gb.w * f;
   const double scale = MODE == 1 ? gb.w : 1.0;
   for (int c0 = 0; c0 < m; c0 += LO_CH) {
@@ -999,6 +1004,7 @@ __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ i
       acc *= scale;
       const int j = c0 + jj;
       if (MODE == 0) out[(size_t)(p0 + j - own_lo) * kp + a] = acc;
+      else if (MODE == 2) out[xmoff[blockIdx.x] + (size_t)j * kp + a] = acc;
       else out[(size_t)(p0 - own_lo) * kp + (size_t)a * m + j] = acc;
     }
   }
@@ -1016,19 +1022,59 @@ __global__ void __launch_bounds__(256) k_s2m_leafop(const int4* __restrict__ ite
   const int p0 = pbeg[b], m = pend[b] - p0;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const double* row = S + (size_t)(p0 - own_lo) * kp;
+  for (int j0 = 0; j0 < m; j0 += 32) {  // densities 32 at a time, broadcast by shuffle
+    const double qv = j0 + lane < m ? pts[p0 + j0 + lane].w : 0.0;
+    const int jn = min(32, m - j0);
 #pragma unroll 4
-  for (int j = 0; j < m; ++j) {
-    const double q = pts[p0 + j].w;
+    for (int jj = 0; jj < jn; ++jj) {
+      const double q = __shfl_sync(0xffffffffu, qv, jj);
+      const double* rj = row + (size_t)(j0 + jj) * kp;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int a = lane + 32 * c;
-      if (a < kp) acc[c] = fma(q, __ldcs(row + (size_t)j * kp + a), acc[c]);
+      for (int c = 0; c < 4; ++c) {
+        const int a = lane + 32 * c;
+        if (a < kp) acc[c] = fma(q, __ldcs(rj + a), acc[c]);
+      }
     }
   }
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const int a = lane + 32 * c;
     if (a < kp) qhat[(size_t)b * kp + a] = acc[c];
+  }
+}
+
+// X list with its operators: l^_B[a] += sum over B's X rows, sum_j q_j X_row[j][a]; one warp
+// per target box (its rows are contiguous), rows of kp doubles read coalesced; M2L into l^
+// finished earlier on the stream and a target belongs to one warp: plain read-add-write
+__global__ void __launch_bounds__(256) k_x_gemv(const int4* __restrict__ xt, int nxt, const int4* __restrict__ xsegs,
+                                                const int64_t* __restrict__ xmoff, const double4* __restrict__ pts,
+                                                const double* __restrict__ X, int kp, double* __restrict__ lhat) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nxt) return;
+  const int4 t = xt[w];
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int r = t.y; r < t.z; ++r) {
+    const int4 sg = xsegs[r];
+    const double* row = X + xmoff[r];
+    for (int j0 = 0; j0 < sg.w; j0 += 32) {  // densities 32 at a time, broadcast by shuffle
+      const double qv = j0 + lane < sg.w ? pts[sg.y + j0 + lane].w : 0.0;
+      const int jn = min(32, sg.w - j0);
+#pragma unroll 4
+      for (int jj = 0; jj < jn; ++jj) {
+        const double q = __shfl_sync(0xffffffffu, qv, jj);
+        const double* rj = row + (size_t)(j0 + jj) * kp;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int a = lane + 32 * c;
+          if (a < kp) acc[c] = fma(q, __ldcs(rj + a), acc[c]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int a = lane + 32 * c;
+    if (a < kp) lhat[(size_t)t.x * kp + a] += acc[c];
   }
 }
 
@@ -1472,6 +1518,32 @@ int build_leaf_ops(Plan& P, cudaStream_t st) {
   return 0;
 }
 
+// X operators: row r = (target B, source leaf A): U^T G_src(c_B + r_B (1 + d) e, sources of A)
+int build_x_ops(Plan& P, cudaStream_t st) {
+  if (P.n_xnd == 0) return 0;
+  const Tree& T = P.tree;
+  const size_t smem = (size_t)P.n * (LO_CH + 1) * sizeof(double);
+  const double f = 1.0 + P.d;  // DC halfwidth factor
+  if (P.bem) {
+    KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leafop_build<2, false, true><<<P.n_xnd, 256, smem, st>>>(P.d_x_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend,
+                                                               P.d_surf, P.n, P.kp, f, P.d_Ut, P.np, 1, 0, P.d_x_mat,
+                                                               nullptr, P.d_tri, P.d_x_seg, P.d_x_moff);
+  } else if (P.d_nrm) {
+    KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leafop_build<2, true><<<P.n_xnd, 256, smem, st>>>(P.d_x_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf,
+                                                        P.n, P.kp, f, P.d_Ut, P.np, 1, 0, P.d_x_mat, P.d_nrm, nullptr,
+                                                        P.d_x_seg, P.d_x_moff);
+  } else {
+    KIFMM_CUDA(cudaFuncSetAttribute(k_leafop_build<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leafop_build<2><<<P.n_xnd, 256, smem, st>>>(P.d_x_items, T.d_pts, T.d_geom, T.d_pbeg, T.d_pend, P.d_surf, P.n,
+                                                  P.kp, f, P.d_Ut, P.np, 1, 0, P.d_x_mat, nullptr, nullptr, P.d_x_seg,
+                                                  P.d_x_moff);
+  }
+  KIFMM_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int sib_tile_width(int kp) { return sq_nt(kp); }
 
 int ggs_tile_width(int M, int K) {
@@ -1667,7 +1739,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, st)) return -3;
       mark(5);
       // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
-      if (P.n_xnd > 0) {
+      if (P.leaf_x && P.n_xt > 0) {
+        ++g_launches;
+        k_x_gemv<<<(P.n_xt + 7) / 8, 256, 0, st>>>(P.d_xt_items, P.n_xt, P.d_x_seg, P.d_x_moff, T.d_pts, P.d_x_mat, kp,
+                                                   P.d_lhat);
+        KIFMM_CUDA(cudaGetLastError());
+      } else if (P.n_xnd > 0) {
         EvalArgs a = ea;
         a.items = P.d_x_items; a.seg_off = P.d_x_off; a.segs = P.d_x_seg; a.tgt_f = 1.0 + P.d;
         a.out = P.d_chk_x; a.ldo = np;

@@ -433,7 +433,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     return 0;
   };
   if (zalloc(&P.d_qhat, (size_t)nb * kp) || zalloc(&P.d_lhat, (size_t)nb * kp) ||
-      zalloc(&P.d_chk_s2m, P.leaf_s2m ? 1 : (size_t)P.n_s2m * np) || zalloc(&P.d_chk_x, (size_t)P.n_xnd * np) ||
+      zalloc(&P.d_chk_s2m, P.leaf_s2m ? 1 : (size_t)P.n_s2m * np) || zalloc(&P.d_chk_x, P.leaf_x ? 1 : (size_t)P.n_xnd * np) ||
       zalloc(&P.d_eqd_l2t, (size_t)n_l2t * np) || zalloc(&P.d_eqd_w, (size_t)n_wnd * np) ||
       zalloc(&P.d_pot_near, T.N) || zalloc(&P.d_pot_far, T.N) || zalloc(&P.d_io, 2 * T.N))
     return -3;
@@ -457,11 +457,39 @@ int build_schedules(Plan& P, cudaStream_t st) {
     std::vector<int> sl = Dp.nranks > 1 ? Dp.straddle : std::vector<int>();
     if (upload(P, &P.d_straddle, sl, st) || zalloc(&P.d_straddle_buf, (size_t)P.n_straddle * kp)) return -3;
   }
+  // X-list operators (after S2M / L2T, same reserve; BEM: always, its runtime integrals are slow)
+  {
+    int64_t xcnt = 0;
+    std::vector<int64_t> xo(xitems.size() + 1, 0);
+    for (size_t r = 0; r < xitems.size(); ++r) xo[r + 1] = xo[r] + (int64_t)xsegs[r].w * kp;
+    xcnt = xo.back();
+    size_t fr = 0, tot = 0;
+    KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
+    const double used = (P.leaf_s2m ? 1.0 : 0.0) + (P.leaf_l2t ? 1.0 : 0.0);
+    const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot) -
+                          used * (double)(Dp.own_hi - Dp.own_lo) * kp * sizeof(double);
+    P.leaf_x = !xitems.empty() && (P.leaf_ops_opt > 0 || P.bem ||
+                                   (P.leaf_ops_opt < 0 && (double)xcnt * sizeof(double) <= budget));
+    if (P.leaf_x) {
+      if (zalloc(&P.d_x_mat, (size_t)xcnt) || upload(P, &P.d_x_moff, xo, st)) return -3;
+      P.leaf_op_bytes += xcnt * (int64_t)sizeof(double);
+      std::vector<int4> xt;  // rows are grouped by target (X list order (tgt, src))
+      for (size_t r = 0; r < xitems.size();) {
+        size_t e = r;
+        while (e < xitems.size() && xitems[e].x == xitems[r].x) ++e;
+        xt.push_back(make_int4(xitems[r].x, (int)r, (int)e, 0));
+        r = e;
+      }
+      P.n_xt = (int)xt.size();
+      if (upload(P, &P.d_xt_items, xt, st)) return -3;
+    }
+  }
+  if (P.leaf_x && build_x_ops(P, st)) return -3;
   if (P.leaf_s2m || P.leaf_l2t) {
     const size_t cnt = (size_t)(Dp.own_hi - Dp.own_lo) * kp;
     if (P.leaf_s2m && zalloc(&P.d_s2m_mat, cnt)) return -3;
     if (P.leaf_l2t && zalloc(&P.d_l2t_mat, cnt)) return -3;
-    P.leaf_op_bytes = (int64_t)((P.leaf_s2m ? 1 : 0) + (P.leaf_l2t ? 1 : 0)) * cnt * sizeof(double);
+    P.leaf_op_bytes += (int64_t)((P.leaf_s2m ? 1 : 0) + (P.leaf_l2t ? 1 : 0)) * cnt * sizeof(double);
     if (build_leaf_ops(P, st)) return -3;
   }
   KIFMM_CUDA(cudaStreamSynchronize(st));
