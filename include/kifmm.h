@@ -175,6 +175,17 @@ int fmm_matvec_owned(fmm_plan* plan, const double* density_owned, double* potent
 /* Same with HOST buffers (copies inside; returns after the stream synchronised). */
 int fmm_matvec_owned_host(fmm_plan* plan, const double* h_density_owned, double* h_potential_owned, void* stream);
 
+/* Solve A x = rhs with restarted GMRES(restart) (the paper's solver,
+ * P:528, tolerance 1e-6 at P:539), A = the plan's matvec (single-GPU plans; with BEM
+ * triangles, the collocation operator).  Device vectors in caller order; x holds the
+ * initial guess on entry and the solution on return.  Stops when ||rhs - A x|| <=
+ * tol ||rhs|| or after maxit iterations.  Arnoldi by classical Gram-Schmidt applied twice
+ * on the device; Givens rotations on the host.  Outputs: *iters iterations (= matvecs
+ * in the Krylov loop), *relres the final true relative residual, *t_matvec_ms (may be
+ * NULL) the mean matvec time.  Synchronises `stream` before returning. */
+int fmm_gmres(fmm_plan* plan, const double* rhs, double* x, int restart, int maxit, double tol, void* stream, int* iters,
+              double* relres, double* t_matvec_ms);
+
 /* Owned sorted-point range [*begin, *end) of the plan's rank. */
 int fmm_owned_range(const fmm_plan* plan, int64_t* begin, int64_t* end);
 

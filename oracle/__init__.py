@@ -58,6 +58,7 @@ def lib():
         L.oracle_tri_integral.restype = ctypes.c_double
         L.oracle_direct_bem.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_bem_matrix.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_direct_dl.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_direct.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
@@ -110,6 +111,15 @@ def direct_bem(centroids, tris, q, targets=None):
     out = np.zeros(tg.size)
     lib().oracle_direct_bem(N, _ptr(c), _ptr(t), _ptr(q), tg.size, _ptr(tg), _ptr(out))
     return out
+
+
+def bem_matrix(centroids, tris):
+    """Dense collocation matrix A_ij = int_Tj G(x_i, y) dy, N x N."""
+    c = np.ascontiguousarray(centroids, dtype=np.float64)
+    t = np.ascontiguousarray(tris, dtype=np.float64).reshape(-1, 9)
+    A = np.zeros((c.shape[0], c.shape[0]))
+    lib().oracle_bem_matrix(c.shape[0], _ptr(c), _ptr(t), _ptr(A))
+    return A
 
 
 class Plan:

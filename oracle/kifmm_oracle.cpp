@@ -447,6 +447,13 @@ void oracle_direct_bem(int64_t N, const double* pts, const double* tri, const do
   }
 }
 
+// dense collocation matrix A (N x N, row-major): A_ij = int_Tj G(x_i, y) dy
+void oracle_bem_matrix(int64_t N, const double* pts, const double* tri, double* A) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < N; ++i)
+    for (int64_t j = 0; j < N; ++j) A[i * N + j] = oracle_tri_integral(tri + 9 * j, pts + 3 * i, j == i);
+}
+
 void* oracle_plan(int64_t N, const double* pts, int s, int wx_direct_max) {
   Plan* P = new Plan();
   P->N = N; P->s = s; P->wx_direct_max = wx_direct_max;

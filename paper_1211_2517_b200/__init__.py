@@ -69,7 +69,7 @@ EXPORTS = ("fmm_default_options", "fmm_setup", "fmm_setup_ex", "fmm_matvec", "fm
            "fmm_info", "fmm_export_tree", "fmm_export_lists", "fmm_export_phase", "fmm_tables_build",
            "fmm_tables_view_get", "fmm_tables_free", "fmm_last_error", "fmm_matvec_owned", "fmm_matvec_owned_host",
            "fmm_owned_range", "fmm_nccl_unique_id", "fmm_matvec_group", "fmm_partition_host", "fmm_partition_get",
-           "fmm_partition_free", "fmm_plan_partition")
+           "fmm_partition_free", "fmm_plan_partition", "fmm_gmres")
 
 _lib = None
 
@@ -112,6 +112,8 @@ def lib():
         L.fmm_partition_free.restype = None
         L.fmm_plan_partition.argtypes = [vp]
         L.fmm_plan_partition.restype = vp
+        L.fmm_gmres.argtypes = [vp, vp, vp, ci, ci, ctypes.c_double, vp, ctypes.POINTER(ci),
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         _lib = L
     return _lib
 
@@ -307,6 +309,19 @@ class Plan:
         _check(lib().fmm_matvec_owned_host(self._h, density_owned.ctypes.data, out.ctypes.data, _stream_ptr(stream)),
                "fmm_matvec_owned_host")
         return out
+
+    def gmres(self, rhs, x0=None, restart: int = 50, maxit: int = 500, tol: float = 1e-6, stream=None):
+        """Solve (this plan's operator) x = rhs by restarted GMRES on the device (fmm_gmres).
+        Returns (x, info) with info = {iters, relres, t_matvec_ms}."""
+        import torch
+        if not (rhs.is_cuda and rhs.dtype == torch.float64 and rhs.is_contiguous() and rhs.numel() == self.N):
+            raise TypeError("rhs must be a contiguous CUDA float64 tensor of length N")
+        x = torch.zeros_like(rhs) if x0 is None else x0.clone().contiguous()
+        it, rr, tm = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        _check(lib().fmm_gmres(self._h, ctypes.c_void_p(rhs.data_ptr()), ctypes.c_void_p(x.data_ptr()), restart,
+                               maxit, tol, _stream_ptr(stream), ctypes.byref(it), ctypes.byref(rr), ctypes.byref(tm)),
+               "fmm_gmres")
+        return x, dict(iters=it.value, relres=rr.value, t_matvec_ms=tm.value)
 
     def partition(self) -> dict:
         return _partition_dict(lib().fmm_plan_partition(self._h))

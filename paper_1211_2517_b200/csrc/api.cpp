@@ -311,6 +311,17 @@ int fmm_matvec_owned_host(fmm_plan* h, const double* h_density, double* h_potent
   return FMM_OK;
 }
 
+int fmm_gmres(fmm_plan* h, const double* rhs, double* x, int restart, int maxit, double tol, void* stream, int* iters,
+              double* relres, double* t_matvec_ms) {
+  if (!h || !rhs || !x || !iters || !relres || restart < 1 || maxit < 0 || !(tol >= 0)) {
+    set_error("fmm_gmres: invalid argument");
+    return FMM_EINVAL;
+  }
+  if (h->P.dist.nranks > 1) { set_error("fmm_gmres: single-GPU plans only"); return FMM_EINVAL; }
+  int rc = kifmm::gmres_solve(h->P, rhs, x, restart, maxit, tol, (cudaStream_t)stream, iters, relres, t_matvec_ms);
+  return rc ? FMM_ECUDA : FMM_OK;
+}
+
 int fmm_owned_range(const fmm_plan* h, int64_t* begin, int64_t* end) {
   if (!h || !begin || !end) { set_error("fmm_owned_range: null argument"); return FMM_EINVAL; }
   *begin = h->P.dist.own_lo;

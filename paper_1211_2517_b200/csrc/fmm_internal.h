@@ -246,6 +246,8 @@ int bem_sort_triangles(Plan& P, const double* d_tri_caller, cudaStream_t st);
 int bem_check_enclosure(Plan& P, cudaStream_t st);
 int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st);
 int bem_near_matvec(const Plan& P, cudaStream_t st);
+int gmres_solve(Plan& P, const double* b, double* x, int m, int maxit, double tol, cudaStream_t st, int* iters,
+                double* relres, double* t_matvec_ms);
 int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st);
 constexpr int kNumStages = 5;
 int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st);

@@ -73,3 +73,50 @@ def test_bem_unit_sphere_and_enclosure_check():
     with pytest.raises(K().FmmError, match="surface condition"):
         K().Plan(torch.from_numpy(cen2).to(dev), None, p=4, k=24, leaf_size=1, d=0.1,
                  triangles=torch.from_numpy(tri2).to(dev))
+
+
+def test_gmres_bem_dirichlet_sphere():
+    # NEXT(4): GMRES on the device with the FMM-BEM operator (tol 1e-6 at P:539) —
+    # f = 1 on the unit sphere; against the dense direct solve of the oracle's matrix
+    tri, cen, _ = synth_inputs.sphere_bem(4)
+    s = 16
+    d = 0.5 / math.sqrt(s)
+    dev = torch.device("cuda:0")
+    gp = K().Plan(torch.from_numpy(cen).to(dev), None, p=6, k=60, leaf_size=s, d=d, tables=tables(6, 60, d),
+                  triangles=torch.from_numpy(tri).to(dev))
+    f = torch.ones(cen.shape[0], dtype=torch.float64, device=dev)
+    x, info = gp.gmres(f, restart=30, maxit=200, tol=1e-10)
+    assert info["relres"] <= 1e-10 and 0 < info["iters"] < 200
+    xs = x.cpu().numpy()
+    # the same operator solved on the CPU: scipy GMRES around the oracle's FMM-BEM matvec
+    from scipy.sparse.linalg import LinearOperator, gmres
+    tb = tables(6, 60, d)
+    op = oracle.Plan(cen, s, tb["n"])
+    Aop = LinearOperator((cen.shape[0], cen.shape[0]), matvec=lambda v: op.matvec(tb, np.asarray(v).ravel(), tris=tri))
+    xo, flag = gmres(Aop, np.ones(cen.shape[0]), rtol=1e-12, restart=60, maxiter=20)
+    assert flag == 0
+    assert rel(xs, xo) < 1e-8
+    # and the dense direct solve, within the p = 6 FMM operator error (x conditioning)
+    ref = np.linalg.solve(oracle.bem_matrix(cen, tri), np.ones(cen.shape[0]))
+    assert rel(xs, ref) < 5e-4
+    assert abs(xs.mean() - 1.0) < 0.02
+    # tolerance 1e-6 (the paper's) stops earlier; zero rhs returns zero at once
+    x6, i6 = gp.gmres(f, tol=1e-6)
+    assert i6["relres"] <= 1e-6 and i6["iters"] < info["iters"]
+    z, iz = gp.gmres(torch.zeros_like(f))
+    assert iz["iters"] == 0 and float(z.abs().max()) == 0.0
+
+
+def test_gmres_restarts_true_residual():
+    # GMRES(5) with many restarts on the BEM operator: the final TRUE residual meets the tolerance
+    tri, cen, q = synth_inputs.sphere_bem(4)
+    s = 16
+    d = 0.5 / math.sqrt(s)
+    dev = torch.device("cuda:0")
+    gp = K().Plan(torch.from_numpy(cen).to(dev), None, p=6, k=60, leaf_size=s, d=d, tables=tables(6, 60, d),
+                  triangles=torch.from_numpy(tri).to(dev))
+    b = torch.from_numpy(q).to(dev)
+    x, info = gp.gmres(b, restart=5, maxit=500, tol=1e-8)
+    assert info["relres"] <= 1e-8 and info["iters"] > 5
+    r = b - gp.matvec(x)
+    assert float(torch.linalg.norm(r) / torch.linalg.norm(b)) <= 1e-8

@@ -92,3 +92,13 @@ def test_bem_fmm_matches_dense():
     tb = pc.build_tables(4, 24, d=d_bem)
     out = oracle.Plan(cen2, 16, tb["n"]).matvec(tb, q2, tris=tri2)
     np.testing.assert_allclose(out, oracle.direct_bem(cen2, tri2, q2), rtol=1e-14)
+
+
+def test_dense_matrix_is_the_product_and_sphere_solve():
+    # the dense matrix reproduces direct_bem, and the Dirichlet problem f = 1 on the unit
+    # sphere has the density ~ 1 (continuum: q = 1/R)
+    tri, cen, q = synth_inputs.sphere_bem(3)
+    A = oracle.bem_matrix(cen, tri)
+    np.testing.assert_allclose(A @ q, oracle.direct_bem(cen, tri, q), rtol=1e-12)
+    sol = np.linalg.solve(A, np.ones(cen.shape[0]))
+    assert abs(sol.mean() - 1.0) < 0.02 and sol.std() < 0.02

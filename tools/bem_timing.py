@@ -45,3 +45,17 @@ print(json.dumps(dict(workload=f"BEM sphere octa-{lv}", N=N, leaf=s, p=p, k=inf[
                       near_gb=inf["bem_near_bytes"] / 1e9, leafop_gb=inf["leaf_op_bytes"] / 1e9,
                       near_hbm_tbs=inf["bem_near_bytes"] / (inf["phase_ms"]["eval"] * 1e-3) / 1e12,
                       extrusion=inf["bem_extrusion"], unit_density_potential_maxdev=float(np.abs(ones - 1).max()))))
+
+# GMRES (tolerance 1e-6 as P:539) on the Dirichlet problem with the structured data
+# f = cos(3 theta) + N(0, 0.1) of the C3 recipe: the paper's T_it = solve time / iterations
+f = Q.clone()
+pl.gmres(f, restart=50, maxit=20, tol=1e-6)  # warm-up (workspace allocation)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+x, gi = pl.gmres(f, restart=50, maxit=500, tol=1e-6)
+wall = time.perf_counter() - t0
+r = f - pl.matvec(x)
+print(json.dumps(dict(workload=f"BEM GMRES sphere octa-{lv}", N=N, p=p, k=inf["k"], tol=1e-6, restart=50,
+                      iters=gi["iters"], relres=gi["relres"],
+                      true_relres=float(torch.linalg.norm(r) / torch.linalg.norm(f)), solve_s=wall,
+                      T_it_ms=wall / max(1, gi["iters"]) * 1e3, matvec_ms=gi["t_matvec_ms"])))
