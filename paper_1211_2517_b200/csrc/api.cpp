@@ -60,8 +60,10 @@ void free_plan_memory(fmm_plan* h) {
   if (P.ev_fork) cudaEventDestroy(P.ev_fork);
   if (P.ev_join) cudaEventDestroy(P.ev_join);
   if (P.stream_near) cudaStreamDestroy(P.stream_near);
-  P.ev_fork = P.ev_join = nullptr;
-  P.stream_near = nullptr;
+  if (P.stream_m2l) cudaStreamDestroy(P.stream_m2l);
+  if (P.ev_m2l) cudaEventDestroy(P.ev_m2l);
+  P.ev_fork = P.ev_join = P.ev_m2l = nullptr;
+  P.stream_near = P.stream_m2l = nullptr;
   kifmm::nccl_comm_destroy(P);
 }
 
@@ -217,7 +219,7 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     P.sym_opt = 0;
   }
   if (opt->triangles) {  // BEM elements: collocation at the points (= centroids), element integrals
-    if (opt->nranks > 1 || P.overlap) {
+    if (opt->nranks > 1) {
       set_error("fmm_setup: BEM elements are single-GPU in this build");
       return fail(FMM_EINVAL);
     }
@@ -249,10 +251,14 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   // near-field CTAs take the SMs first (measured C2 -1%, C3 +3.5%, C4 +5%)
   {
     const char* e = std::getenv("KIFMM_OVERLAP");
-    P.overlap = !P.split_phases && e && std::atoi(e) != 0;
+    P.overlap = (!P.split_phases && !P.bem && e) ? std::atoi(e) : 0;
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if (P.overlap &&
-        (cudaStreamCreateWithFlags(&P.stream_near, cudaStreamNonBlocking) != cudaSuccess ||
+        (cudaStreamCreateWithPriority(&P.stream_near, cudaStreamNonBlocking, lo_prio) != cudaSuccess ||
+         cudaStreamCreateWithPriority(&P.stream_m2l, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
          cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&P.ev_m2l, cudaEventDisableTiming) != cudaSuccess ||
          cudaEventCreateWithFlags(&P.ev_join, cudaEventDisableTiming) != cudaSuccess)) {
       set_error("fmm_setup: creating the near-field stream failed");
       return fail(FMM_ECUDA);

@@ -214,8 +214,10 @@ struct Plan {
   // timing of the last matvec (ms per phase), filled when profiling is on
   std::vector<float> phase_ms;
   cudaStream_t stream = nullptr;
-  bool overlap = false;               // near field on stream_near, concurrent with the far field
+  int overlap = 0;                    // near field on stream_near: 1 from the upward pass, 2 beside M2L
   cudaStream_t stream_near = nullptr;
+  cudaStream_t stream_m2l = nullptr;  // overlap 2: high-priority stream of the M2L kernel
+  cudaEvent_t ev_m2l = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_phase;
   bool profile = false;

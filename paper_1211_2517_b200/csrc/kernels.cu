@@ -1690,7 +1690,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
     }
     case 1: {  // upward pass (partial multipoles of straddling boxes)
       if (owned && unpack(pts_w, 4, P.xd.d_recv_idx, P.xd.nrecv, 1, P.xd.d_recv, st)) return -3;
-      if (P.overlap) {  // near field on its own stream, concurrent with the far field
+      if (P.overlap == 1) {  // near field on its own stream, concurrent with the far field
         KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
         KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
         if (launch_near(P, ea, P.stream_near)) return -3;
@@ -1731,12 +1731,27 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       mark(4);
       // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
       //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
+      // overlap mode 2: M2L on the plan's high-priority stream (its persistent CTAs are
+      // dispatched first), the near field on the low-priority near stream filling the rest
+      cudaStream_t sm2l = st;
+      if (P.overlap == 2) {
+        KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_m2l, P.ev_fork, 0));
+        sm2l = P.stream_m2l;
+      }
       if (P.lr.on) {
-        if (launch_m2l_lowrank(P.g_m2l_sib, P.lr, kp, k, P.d_qhat, P.d_lhat, st)) return -3;
-      } else if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, st)) {
+        if (launch_m2l_lowrank(P.g_m2l_sib, P.lr, kp, k, P.d_qhat, P.d_lhat, sm2l)) return -3;
+      } else if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, sm2l)) {
         return -3;
       }
-      if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, st)) return -3;
+      if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, sm2l)) return -3;
+      if (P.overlap == 2) {
+        KIFMM_CUDA(cudaEventRecord(P.ev_m2l, P.stream_m2l));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
+        if (launch_near(P, ea, P.stream_near)) return -3;
+        KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
+        KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_m2l, 0));
+      }
       mark(5);
       // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
       if (P.leaf_x && P.n_xt > 0) {
