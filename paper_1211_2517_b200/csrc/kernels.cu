@@ -787,7 +787,8 @@ __device__ __forceinline__ void p2p_sym_pass(const double4* __restrict__ pts, in
   }
 }
 
-__global__ void __launch_bounds__(SYM_WARPS * 32, 6) k_p2p_sym(const int2* __restrict__ pairs, int npairs,
+template <int MINB>
+__global__ void __launch_bounds__(SYM_WARPS * 32, MINB) k_p2p_sym(const int2* __restrict__ pairs, int npairs,
                                                               const double4* __restrict__ pts,
                                                               const int* __restrict__ pbeg, const int* __restrict__ pend,
                                                               double* __restrict__ pot) {
@@ -1602,8 +1603,14 @@ static int launch_near(const Plan& P, const EvalArgs& ea, cudaStream_t st) {
 static int launch_sym(const Plan& P, cudaStream_t st) {
   if (P.n_sym == 0) return 0;
   ++g_launches;
-  k_p2p_sym<<<(P.n_sym + SYM_WARPS - 1) / SYM_WARPS, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts,
-                                                                            P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
+  static const int minb = [] { const char* e = std::getenv("KIFMM_SYM_MINB"); return e ? std::atoi(e) : 5; }();
+  const int grid = (P.n_sym + SYM_WARPS - 1) / SYM_WARPS;
+  if (minb == 8)
+    k_p2p_sym<8><<<grid, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts, P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
+  else if (minb == 5)
+    k_p2p_sym<5><<<grid, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts, P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
+  else
+    k_p2p_sym<6><<<grid, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts, P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
   KIFMM_CUDA(cudaGetLastError());
   return 0;
 }
