@@ -283,6 +283,6 @@ int build_schedules(Plan& P, cudaStream_t st);
 int upload_tables(Plan& P);
 int kernels_init();
 int ggs_tile_width(int M, int K);
-int sib_tile_width(int kp);
+int sib_tile_width(int kp, bool lowrank = false);
 
 }  // namespace kifmm

@@ -1404,6 +1404,204 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_lr(
   }
 }
 
+// ----------------------------------------------------------------------------
+// k_m2l_lr2: stage-2 sibling M2L, factors staged in shared memory (kp <= 64).
+// All 8 warps step through the same tile (64 columns, warp w owns columns 8w..8w+7).
+// Per operator step the B panel AND the factors V^_o (r8 x kp) and U^_o (kp x r8) are
+// copied with cp.async one step ahead into double buffers, so every MMA operand comes
+// from shared memory.  Phase A computes T^T (8 columns x r8) = Q^T V^_o^T with
+// DMMA.8x8x4 (operands: panel, V^); phase B accumulates acc (kp x 8) += U^_o T with the
+// m16n8k8 MMA, its B fragments moved out of phase A's accumulators by 4 shuffles per
+// k8-step (no shared T, one barrier per step).
+// ----------------------------------------------------------------------------
+template <int KP, int RP, int NT_ = 128>
+struct Lr2Smem {
+  static constexpr int NT = NT_;
+  static constexpr int SB = KP + 4;  // panel row (column-major panel)
+  static constexpr int SV = KP + 4;  // V^ row
+  static constexpr int SU = RP + 4;  // U^ row
+  static constexpr int PANEL = NT * SB, VS = RP * SV, US = KP * SU;
+  static constexpr int BUF = PANEL + VS + US;  // doubles per buffer
+};
+
+template <int KP, int RP, int NTC>
+__global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
+    const int4* __restrict__ tiles, int ntiles, const int* __restrict__ cols, const int* __restrict__ classes,
+    const double* __restrict__ Uh, const double* __restrict__ Vh, const int* __restrict__ rank, int mvalid,
+    const double* X, double* Y, int* __restrict__ counter) {
+  using S = Lr2Smem<KP, RP, NTC>;
+  constexpr int NT = S::NT, NW = NT / 8, NTH = NW * 32, CW = 9, K2 = KP / 2, KS4 = KP / 4;
+  constexpr int RB = KP / 16;          // output row blocks (m16)
+  constexpr int NRB = RP / 8;          // max rank blocks of 8
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_meta[3][NT * CW];
+  __shared__ int s_tile[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  int ti = blockIdx.x;
+  if (ti >= ntiles) return;
+
+  auto fetch_meta = [&](int tid, int slot) {
+    const int4 tl = tiles[tid];
+    for (int e = threadIdx.x; e < NT * CW; e += NTH) {
+      const int c = e / CW;
+      s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
+    }
+  };
+  // stage step (child b of the columns in meta slot, operator op) into buffer buf
+  auto stage = [&](int slot, int b, int op, int buf) {
+    double* base = sm + (size_t)buf * S::BUF;
+    double* Bd = base;
+    for (int p = warp; p < NT; p += NW) {
+      const int src = s_meta[slot][p * CW + 1 + b];
+      for (int c = lane; c < K2; c += 32) {
+        double* dst = Bd + p * S::SB + 2 * c;
+        if (src >= 0) cp_async16(dst, X + (size_t)src * KP + 2 * c);
+        else { dst[0] = 0.0; dst[1] = 0.0; }
+      }
+    }
+    const int r8 = (rank[op] + 7) & ~7;
+    double* Vd = base + S::PANEL;
+    const double* Vg = Vh + (size_t)op * RP * KP;
+    for (int e = threadIdx.x; e < r8 * K2; e += NTH) {
+      const int row = e / K2, c = e - row * K2;
+      cp_async16(Vd + row * S::SV + 2 * c, Vg + (size_t)row * KP + 2 * c);
+    }
+    double* Ud = base + S::PANEL + S::VS;
+    const double* Ug = Uh + (size_t)op * KP * RP;
+    const int r2 = r8 / 2;
+    for (int e = threadIdx.x; e < KP * r2; e += NTH) {
+      const int row = e / r2, c = e - row * r2;
+      cp_async16(Ud + row * S::SU + 2 * c, Ug + (size_t)row * RP + 2 * c);
+    }
+  };
+
+  int slot = 0;
+  fetch_meta(ti, 0);
+  if (threadIdx.x == 0) s_tile[1] = gridDim.x + atomicAdd(counter, 1);
+  __syncthreads();
+  const int* cls = classes + tiles[ti].x * 17;
+  stage(0, cls[1], cls[9], 0);
+  cp_async_commit();
+  int buf = 0;
+  double acc[RB][4];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+
+  while (true) {
+    const int nv = cls[0];
+    const int nslot = slot == 2 ? 0 : slot + 1;
+    const int tnext = s_tile[nslot];
+    for (int jb = 0; jb < nv; ++jb) {
+      const bool last = jb + 1 == nv;
+      if (jb == 0 && tnext < ntiles) {
+        fetch_meta(tnext, nslot);
+        if (threadIdx.x == 0) s_tile[nslot == 2 ? 0 : nslot + 1] = gridDim.x + atomicAdd(counter, 1);
+      }
+      cp_async_wait0();
+      __syncthreads();  // this step's panel + factors landed; the other buffer is free
+      if (!last) stage(slot, cls[2 + jb], cls[9 + jb + 1], buf ^ 1);
+      else if (tnext < ntiles) {
+        const int* ncls = classes + tiles[tnext].x * 17;
+        stage(nslot, ncls[1], ncls[9], buf ^ 1);
+      }
+      cp_async_commit();
+      const double* base = sm + (size_t)buf * S::BUF;
+      const int op = cls[9 + jb];
+      const int nrb = (rank[op] + 7) >> 3;
+      // phase A: T^T[col 8w + g][rank 8 rb + 2t (+1)] in d[rb] (two interleaved chains per block)
+      double d[NRB][2];
+      {
+        const double* Pa = base + (size_t)(8 * warp + g) * S::SB + t;       // a = panel[col][4s + t]
+        const double* Vb = base + S::PANEL + (size_t)g * S::SV + t;          // b = V^[8 rb + g][4s + t]
+#pragma unroll
+        for (int rb = 0; rb < NRB; ++rb) {
+          d[rb][0] = d[rb][1] = 0.0;
+          if (rb < nrb) {
+            double e0 = 0.0, e1 = 0.0;
+            const double* vb = Vb + (size_t)8 * rb * S::SV;
+#pragma unroll
+            for (int s4 = 0; s4 < KS4; s4 += 2) {
+              dmma_8x8x4(d[rb][0], d[rb][1], Pa[4 * s4], vb[4 * s4]);
+              dmma_8x8x4(e0, e1, Pa[4 * s4 + 4], vb[4 * s4 + 4]);
+            }
+            d[rb][0] += e0;
+            d[rb][1] += e1;
+          }
+        }
+      }
+      // phase B: acc += U^ (KP x 8 nrb) T (8 nrb x 8); b0 = T[8ks + t][g], b1 = T[8ks + t + 4][g]
+      {
+        const double* Ua = base + S::PANEL + S::VS + (size_t)g * S::SU + t;
+        const int src0 = 4 * g + (t >> 1), src1 = src0 + 2;
+        const bool odd = t & 1;
+#pragma unroll
+        for (int ks = 0; ks < NRB; ++ks) {
+          if (ks < nrb) {
+            const double x0 = __shfl_sync(FULL, d[ks][0], src0), x1 = __shfl_sync(FULL, d[ks][1], src0);
+            const double y0 = __shfl_sync(FULL, d[ks][0], src1), y1 = __shfl_sync(FULL, d[ks][1], src1);
+            const double b0 = odd ? x1 : x0, b1 = odd ? y1 : y0;
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+              const double* ua = Ua + (size_t)16 * rb * S::SU + 8 * ks;
+              double a[4];
+              a[0] = ua[0];
+              a[1] = ua[8 * S::SU];
+              a[2] = ua[4];
+              a[3] = ua[8 * S::SU + 4];
+              dmma_16x8x8(acc[rb], a, b0, b1);
+            }
+          }
+        }
+      }
+      buf ^= 1;
+      if (last) {
+        // acc[rb]: rows 16 rb + g (c0, c1) and + 8 (c2, c3) of the warp's columns 2t, 2t + 1
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int tg = s_meta[slot][(8 * warp + 2 * t + c) * CW];
+          if (tg >= 0) {
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+              const int row = 16 * rb + g;
+              if (row < mvalid) atomicAdd(Y + (size_t)tg * KP + row, acc[rb][c]);
+              if (row + 8 < mvalid) atomicAdd(Y + (size_t)tg * KP + row + 8, acc[rb][2 + c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < RB; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+      }
+    }
+    if (tnext >= ntiles) break;
+    ti = tnext;
+    slot = nslot;
+    cls = classes + tiles[ti].x * 17;
+  }
+}
+
+constexpr int kLr2Cols = 128;  // columns per stage-2 sibling tile (kp <= 64)
+
+template <int KP, int RP>
+int launch_lr2(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
+  using S = Lr2Smem<KP, RP, kLr2Cols>;
+  const size_t smem = (size_t)2 * S::BUF * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_lr2<KP, RP, kLr2Cols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    attr = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_lr2<KP, RP, kLr2Cols>, kLr2Cols * 4, smem);
+  const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
+  KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
+  k_m2l_lr2<KP, RP, kLr2Cols><<<grid, kLr2Cols * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, lr.d_Uh,
+                                                                 lr.d_Vh, lr.d_rank, mvalid, X, Y, g.d_counter);
+  return 0;
+}
+
 template <int KP, int RP>
 int launch_lr(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
   constexpr int NT = sq_nt(KP);
@@ -1439,6 +1637,19 @@ int launch_m2l_lowrank(const SibLaunch& g, const LowRank& lr, int kp, int mvalid
   if (g.ntiles == 0) return 0;
   ++g_launches;
   int rc = 0;
+  static const int v2 = [] { const char* e = std::getenv("KIFMM_LR2"); return e ? std::atoi(e) : 1; }();
+  if (v2 && kp == 64 && (lr.rp == 16 || lr.rp == 32)) {
+    rc = lr.rp == 16 ? launch_lr2<64, 16>(g, lr, mvalid, X, Y, st) : launch_lr2<64, 32>(g, lr, mvalid, X, Y, st);
+    if (rc) return rc;
+    KIFMM_CUDA(cudaGetLastError());
+    return 0;
+  }
+  if (v2 && kp == 32 && (lr.rp == 16 || lr.rp == 32)) {
+    rc = lr.rp == 16 ? launch_lr2<32, 16>(g, lr, mvalid, X, Y, st) : launch_lr2<32, 32>(g, lr, mvalid, X, Y, st);
+    if (rc) return rc;
+    KIFMM_CUDA(cudaGetLastError());
+    return 0;
+  }
   if (kp == 32) rc = launch_lr_rp<32>(g, lr, mvalid, X, Y, st);
   else if (kp == 64) rc = launch_lr_rp<64>(g, lr, mvalid, X, Y, st);
   else rc = launch_lr_rp<104>(g, lr, mvalid, X, Y, st);
@@ -1545,7 +1756,10 @@ int build_x_ops(Plan& P, cudaStream_t st) {
   return 0;
 }
 
-int sib_tile_width(int kp) { return sq_nt(kp); }
+int sib_tile_width(int kp, bool lowrank) {
+  static const int v2 = [] { const char* e = std::getenv("KIFMM_LR2"); return e ? std::atoi(e) : 1; }();
+  return lowrank && v2 && kp <= 64 ? kLr2Cols : sq_nt(kp);
+}
 
 int ggs_tile_width(int M, int K) {
   if (M == K && (K == 32 || K == 64 || K == 104)) return sq_nt(K);

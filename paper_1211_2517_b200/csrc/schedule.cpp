@@ -386,7 +386,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     }
     if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
     // sibling tiles: per class, columns in target order, NT columns per tile
-    const int NTs = sib_tile_width(kp);
+    const int NTs = sib_tile_width(kp, P.lr.on && P.lr.rp <= 32);  // (k_m2l_lr2 takes rp 16 / 32)
     std::vector<int> cols;
     std::vector<int4> tiles;
     for (int cls = 0; cls < kCls; ++cls) {
@@ -397,10 +397,13 @@ int build_schedules(Plan& P, cudaStream_t st) {
       for (int c = 0; c < ncol; c += NTs) tiles.push_back(make_int4(cls, base + c, std::min(NTs, ncol - c), 0));
     }
     // longest tiles first (the kernel hands tiles out dynamically: LPT order balances the SMs;
-    // a Morton-window order for L2 locality measured no better on C2 / C3 / C5)
-    std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
-      return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
-    });
+    // a Morton-window order for L2 locality measured no better on C2 / C3 / C5).  Stage 2
+    // with KIFMM_LR_ORDER=1: class-major (all SMs share one class's operator factors)
+    static const int lr_order = [] { const char* e = std::getenv("KIFMM_LR_ORDER"); return e ? std::atoi(e) : 0; }();
+    if (!(P.lr.on && lr_order == 1))
+      std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
+        return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
+      });
     P.g_m2l_sib.ntiles = (int)tiles.size();
     P.g_m2l_sib.ncols = (int)cols.size() / 9;
     if (upload(P, &P.g_m2l_sib.d_tiles, tiles, st) || upload(P, &P.g_m2l_sib.d_cols, cols, st) ||
