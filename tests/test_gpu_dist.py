@@ -168,3 +168,15 @@ def test_nccl_transport_one_rank():
     out[perm] = po
     assert rel(out, ref) <= TOL
     assert rel(pl.matvec_owned_host(q[perm])[np.argsort(perm)], ref) <= TOL
+
+
+@pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k"])
+def test_loopback_stage2(case):
+    # stage-2 low-rank cores through a 3-rank partition
+    pts, q, p, k, s = CASES[case]()
+    tb = pc.stage2(tables(p, k), 1.0)
+    ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q)
+    dev = torch.device("cuda:0")
+    P = torch.from_numpy(pts).to(dev)
+    plans = [K().Plan(P, None, p=p, k=k, leaf_size=s, tables=tb, m2l_c2=1.0, nranks=3, rank=r) for r in range(3)]
+    assert rel(run_owned(plans, q), ref) <= TOL
