@@ -8,7 +8,8 @@ unit cube (seed 0), densities U[-1,1], p = 6 (n = 152), k = 60 (k_eff 61), leaf
 128.  A step is one whole fmm_matvec (permute, S2M, M2M, M2L, X, L2L, L2T, W,
 P2P, unpermute) with the inputs resident in HBM; L2 is flushed (a 256 MiB write)
 between timed steps, outside the timed events.  Multi-GPU (torchrun, N ranks):
-weak scaling, ONE problem of N x 2^20 points (same recipe) partitioned over the
+weak scaling, ONE problem of N unit cubes tiled (2, 2x2, 2x2x2) with 2^20 points each
+(C2's density, so every rank's Morton share has C2's leaf occupancy) partitioned over the
 ranks by Morton ranges (OWNED mode: each rank's owned densities in, owned
 potentials out), ghost multipoles / densities exchanged over NCCL inside every
 step; `value` = all points / max-over-ranks step time.  `--impl reference` times
@@ -254,7 +255,7 @@ def run_ours(args):
         cpu = {"value": N / ts[0], "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"one full {args.config} matvec (N={N}), oracle/ C++ -O2 OpenMP, {ts[0]:.2f} s"}
     value = N / (ms * 1e-3)
-    config = {"workload": args.config if ws == 1 else f"{args.config} x{ws} (weak)", "N": N,
+    config = {"workload": args.config if ws == 1 else f"{args.config} x{ws} (weak: {ws} tiled unit cubes)", "N": N,
               "N_per_gpu": N // ws, "p": cfg["p"], "k": cfg["k"], "k_eff": k, "leaf_size": cfg["leaf"],
               "kind": cfg["kind"], "parallelism": "single" if ws == 1 else f"morton-partition{ws} (NCCL ghosts)",
               "l2": "flushed (256 MiB write) between timed steps"}

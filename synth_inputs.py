@@ -31,6 +31,22 @@ CONFIGS = {
 }
 
 
+def tiled_cubes(per: int, count: int, seed: int = 0):
+    """`count` unit cubes (2 -> 2x1x1, 4 -> 2x2x1, 8 -> 2x2x2, else a row), `per` uniform
+    points and U[-1, 1] densities each; cube 0 is uniform_cube(per, seed) itself."""
+    shape = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(count, (count, 1, 1))
+    pts, qs = [], []
+    c = 0
+    for z in range(shape[2]):
+        for y in range(shape[1]):
+            for x in range(shape[0]):
+                p, q = uniform_cube(per, seed + c)
+                pts.append(p + np.array([x, y, z], dtype=float))
+                qs.append(q)
+                c += 1
+    return np.concatenate(pts), np.concatenate(qs)
+
+
 def uniform_cube(n: int, seed: int = 0):
     rng = np.random.default_rng(seed)
     pts = rng.random((n, 3))
@@ -134,6 +150,13 @@ def make(name: str, seed: int = 0, n: int | None = None, scale: int = 1):
     multiplies N (weak-scaling multi-GPU runs: the same recipe, scale x the points)."""
     cfg = dict(CONFIGS[name])
     kind = cfg["kind"]
+    if kind == "cube" and scale > 1 and n is None:
+        # weak scaling: `scale` unit cubes tiled (2, 2x2, 2x2x2, or a row), each with the
+        # workload's point density, so every GPU's share has the same leaf occupancy
+        pts, q = tiled_cubes(cfg["N"], scale, seed)
+        cfg["N"] = pts.shape[0]
+        cfg["tiling"] = scale
+        return np.ascontiguousarray(pts), np.ascontiguousarray(q), cfg
     if scale > 1 and n is None:
         n = cfg["N"] * scale
     if kind == "cube":
