@@ -1424,13 +1424,14 @@ struct Lr2Smem {
   static constexpr int BUF = PANEL + VS + US;  // doubles per buffer
 };
 
-template <int KP, int RP, int NTC>
-__global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
+template <int KP, int RP, int NTC, int CB>
+__global__ void __launch_bounds__(NTC * 4 / CB, 1) k_m2l_lr2(
     const int4* __restrict__ tiles, int ntiles, const int* __restrict__ cols, const int* __restrict__ classes,
     const double* __restrict__ Uh, const double* __restrict__ Vh, const int* __restrict__ rank, int mvalid,
     const double* X, double* Y, int* __restrict__ counter) {
+  // warp w owns CB column blocks of 8: columns 8 CB w .. 8 CB w + 8 CB - 1
   using S = Lr2Smem<KP, RP, NTC>;
-  constexpr int NT = S::NT, NW = NT / 8, NTH = NW * 32, CW = 9, K2 = KP / 2, KS4 = KP / 4;
+  constexpr int NT = S::NT, NW = NT / (8 * CB), NTH = NW * 32, CW = 9, K2 = KP / 2, KS4 = KP / 4;
   constexpr int RB = KP / 16;          // output row blocks (m16)
   constexpr int NRB = RP / 8;          // max rank blocks of 8
   constexpr unsigned FULL = 0xffffffffu;
@@ -1439,6 +1440,7 @@ __global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
   __shared__ int s_tile[3];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
+  const int col0 = 8 * CB * warp;
   int ti = blockIdx.x;
   if (ti >= ntiles) return;
 
@@ -1485,9 +1487,11 @@ __global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
   stage(0, cls[1], cls[9], 0);
   cp_async_commit();
   int buf = 0;
-  double acc[RB][4];
+  double acc[RB][CB][4];
 #pragma unroll
-  for (int i = 0; i < RB; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+  for (int i = 0; i < RB; ++i)
+#pragma unroll
+    for (int c = 0; c < CB; ++c) acc[i][c][0] = acc[i][c][1] = acc[i][c][2] = acc[i][c][3] = 0.0;
 
   while (true) {
     const int nv = cls[0];
@@ -1510,28 +1514,28 @@ __global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
       const double* base = sm + (size_t)buf * S::BUF;
       const int op = cls[9 + jb];
       const int nrb = (rank[op] + 7) >> 3;
-      // phase A: T^T[col 8w + g][rank 8 rb + 2t (+1)] in d[rb] (two interleaved chains per block)
-      double d[NRB][2];
+      // phase A: T^T[col][rank 8 rb + 2t (+1)] of column block cb in d[rb][cb]; each V^
+      // fragment feeds the CB column blocks
+      double d[NRB][CB][2];
       {
-        const double* Pa = base + (size_t)(8 * warp + g) * S::SB + t;       // a = panel[col][4s + t]
-        const double* Vb = base + S::PANEL + (size_t)g * S::SV + t;          // b = V^[8 rb + g][4s + t]
+        const double* Pa = base + (size_t)(col0 + g) * S::SB + t;   // a = panel[col][4s + t]
+        const double* Vb = base + S::PANEL + (size_t)g * S::SV + t;  // b = V^[8 rb + g][4s + t]
 #pragma unroll
         for (int rb = 0; rb < NRB; ++rb) {
-          d[rb][0] = d[rb][1] = 0.0;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) d[rb][c][0] = d[rb][c][1] = 0.0;
           if (rb < nrb) {
-            double e0 = 0.0, e1 = 0.0;
             const double* vb = Vb + (size_t)8 * rb * S::SV;
 #pragma unroll
-            for (int s4 = 0; s4 < KS4; s4 += 2) {
-              dmma_8x8x4(d[rb][0], d[rb][1], Pa[4 * s4], vb[4 * s4]);
-              dmma_8x8x4(e0, e1, Pa[4 * s4 + 4], vb[4 * s4 + 4]);
+            for (int s4 = 0; s4 < KS4; ++s4) {
+              const double bv = vb[4 * s4];
+#pragma unroll
+              for (int c = 0; c < CB; ++c) dmma_8x8x4(d[rb][c][0], d[rb][c][1], Pa[(size_t)8 * c * S::SB + 4 * s4], bv);
             }
-            d[rb][0] += e0;
-            d[rb][1] += e1;
           }
         }
       }
-      // phase B: acc += U^ (KP x 8 nrb) T (8 nrb x 8); b0 = T[8ks + t][g], b1 = T[8ks + t + 4][g]
+      // phase B: acc += U^ T; each U^ fragment feeds the CB column blocks
       {
         const double* Ua = base + S::PANEL + S::VS + (size_t)g * S::SU + t;
         const int src0 = 4 * g + (t >> 1), src1 = src0 + 2;
@@ -1539,9 +1543,14 @@ __global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
 #pragma unroll
         for (int ks = 0; ks < NRB; ++ks) {
           if (ks < nrb) {
-            const double x0 = __shfl_sync(FULL, d[ks][0], src0), x1 = __shfl_sync(FULL, d[ks][1], src0);
-            const double y0 = __shfl_sync(FULL, d[ks][0], src1), y1 = __shfl_sync(FULL, d[ks][1], src1);
-            const double b0 = odd ? x1 : x0, b1 = odd ? y1 : y0;
+            double b0[CB], b1[CB];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+              const double x0 = __shfl_sync(FULL, d[ks][c][0], src0), x1 = __shfl_sync(FULL, d[ks][c][1], src0);
+              const double y0 = __shfl_sync(FULL, d[ks][c][0], src1), y1 = __shfl_sync(FULL, d[ks][c][1], src1);
+              b0[c] = odd ? x1 : x0;
+              b1[c] = odd ? y1 : y0;
+            }
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb) {
               const double* ua = Ua + (size_t)16 * rb * S::SU + 8 * ks;
@@ -1550,28 +1559,32 @@ __global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
               a[1] = ua[8 * S::SU];
               a[2] = ua[4];
               a[3] = ua[8 * S::SU + 4];
-              dmma_16x8x8(acc[rb], a, b0, b1);
+#pragma unroll
+              for (int c = 0; c < CB; ++c) dmma_16x8x8(acc[rb][c], a, b0[c], b1[c]);
             }
           }
         }
       }
       buf ^= 1;
       if (last) {
-        // acc[rb]: rows 16 rb + g (c0, c1) and + 8 (c2, c3) of the warp's columns 2t, 2t + 1
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int tg = s_meta[slot][(8 * warp + 2 * t + c) * CW];
-          if (tg >= 0) {
+        for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
-            for (int rb = 0; rb < RB; ++rb) {
-              const int row = 16 * rb + g;
-              if (row < mvalid) atomicAdd(Y + (size_t)tg * KP + row, acc[rb][c]);
-              if (row + 8 < mvalid) atomicAdd(Y + (size_t)tg * KP + row + 8, acc[rb][2 + c]);
+          for (int c = 0; c < 2; ++c) {
+            const int tg = s_meta[slot][(col0 + 8 * cb + 2 * t + c) * CW];
+            if (tg >= 0) {
+#pragma unroll
+              for (int rb = 0; rb < RB; ++rb) {
+                const int row = 16 * rb + g;
+                if (row < mvalid) atomicAdd(Y + (size_t)tg * KP + row, acc[rb][cb][c]);
+                if (row + 8 < mvalid) atomicAdd(Y + (size_t)tg * KP + row + 8, acc[rb][cb][2 + c]);
+              }
             }
           }
-        }
 #pragma unroll
-        for (int i = 0; i < RB; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+        for (int i = 0; i < RB; ++i)
+#pragma unroll
+          for (int c = 0; c < CB; ++c) acc[i][c][0] = acc[i][c][1] = acc[i][c][2] = acc[i][c][3] = 0.0;
       }
     }
     if (tnext >= ntiles) break;
@@ -1583,23 +1596,30 @@ __global__ void __launch_bounds__(NTC * 4, 1) k_m2l_lr2(
 
 constexpr int kLr2Cols = 128;  // columns per stage-2 sibling tile (kp <= 64)
 
-template <int KP, int RP>
-int launch_lr2(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
+template <int KP, int RP, int CB>
+int launch_lr2_cb(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
   using S = Lr2Smem<KP, RP, kLr2Cols>;
+  constexpr int NTH = kLr2Cols * 4 / CB;
   const size_t smem = (size_t)2 * S::BUF * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_lr2<KP, RP, kLr2Cols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_lr2<KP, RP, kLr2Cols, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
     attr = true;
   }
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_lr2<KP, RP, kLr2Cols>, kLr2Cols * 4, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_lr2<KP, RP, kLr2Cols, CB>, NTH, smem);
   const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
   KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
-  k_m2l_lr2<KP, RP, kLr2Cols><<<grid, kLr2Cols * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, lr.d_Uh,
-                                                                 lr.d_Vh, lr.d_rank, mvalid, X, Y, g.d_counter);
+  k_m2l_lr2<KP, RP, kLr2Cols, CB><<<grid, NTH, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, lr.d_Uh,
+                                                           lr.d_Vh, lr.d_rank, mvalid, X, Y, g.d_counter);
   return 0;
+}
+
+template <int KP, int RP>
+int launch_lr2(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
+  static const int cb = [] { const char* e = std::getenv("KIFMM_LR2_CB"); return e ? std::atoi(e) : 1; }();
+  return cb == 1 ? launch_lr2_cb<KP, RP, 1>(g, lr, mvalid, X, Y, st) : launch_lr2_cb<KP, RP, 2>(g, lr, mvalid, X, Y, st);
 }
 
 template <int KP, int RP>
