@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "bem.cuh"
 #include "common.cuh"
 #include "fmm_internal.h"
@@ -1909,6 +1911,13 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
   ea.surf = P.d_surf; ea.n = n; ea.f_in = 1.0 + P.d; ea.f_out = 3.0 - 2.0 * P.d; ea.ldq = np;
   ea.nrm = P.d_nrm;  // S2M / X check potentials and the near field use it (double layer)
   ea.tri = P.d_tri;  // BEM: X check potentials by element integration
+  // NVTX range per stage (tracing; free without an attached tool)
+  static const char* const kStageName[kNumStages] = {"fmm/density", "fmm/upward", "fmm/ghosts", "fmm/downward",
+                                                     "fmm/output"};
+  struct NvtxRange {
+    explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+  } nvtx_range(stage >= 0 && stage < kNumStages ? kStageName[stage] : "fmm/stage");
   // per-plan launch count across stages (plans of a loopback group interleave)
   struct LaunchCount {
     Plan& P;
