@@ -136,6 +136,9 @@ typedef struct {
   int64_t bem_near_bytes;     /* BEM near-field matrix bytes (0: point sources) */
   double bem_extrusion;       /* BEM: largest element overhang beyond a leaf, in leaf halfwidths
                                  (the surface condition of P:389-411 asks for < d) */
+  int64_t near_mutual_leaves; /* target leaves evaluating symmetric (mutual) leaf pairs */
+  int64_t near_mutual_pairs;  /* unordered near-field point pairs evaluated once for both sides */
+  int64_t near_sym_pairs;     /* leaf pairs of the warp-pair symmetric kernel (KIFMM_SYM=2) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

@@ -542,6 +542,9 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
   info->leaf_op_bytes = P.leaf_op_bytes;
   info->bem_near_bytes = P.bem_near_bytes;
   info->bem_extrusion = P.bem_extrusion;
+  info->near_mutual_leaves = P.n_tleaf_mut;
+  info->near_mutual_pairs = P.n_mut_pairs;
+  info->near_sym_pairs = P.n_sym;
   info->m2l_flops = P.m2l_flops;
   info->m2l_eps2 = P.tables.eps2;
   {

@@ -181,7 +181,20 @@ struct Plan {
   int np = 0;                                  // n rounded up to a multiple of 8
   int n_tleaf = 0; int4* d_tleaf_items = nullptr;
   int n_sym = 0; int2* d_sym = nullptr;   // symmetric near-field leaf pairs (both owned), k_p2p_sym
-  int sym_opt = -1;                        // -1 / 1 on, 0 off (all near pairs one-sided)
+  int sym_opt = -1;                        // -1 / 1 mutual segments (k_evalm), 2 warp pairs (k_p2p_sym), 0 off
+  // near field by k_near (near.cu; mutual leaf pairs, sym_opt -1 / 1): per target leaf
+  // (first point, m, chunk begin, chunk end), grouped by pass shape; chunks (first
+  // source slot, n | nchk << 10 | ml << 20, mh, 0); source slots (point indices)
+  bool nr_on = false;
+  int nr_table = 0;                        // k_near shape table (KIFMM_NEAR_TAB)
+  int n_tleaf_mut = 0;                     // target leaves with mutual segments
+  int64_t n_mut_pairs = 0;                 // unordered point pairs of the mutual segments
+  int4* d_nr_items = nullptr;
+  int4* d_nr_chunks = nullptr;
+  int* d_nr_src = nullptr;
+  int* d_nr_counters = nullptr;            // one work counter per k_near launch
+  int64_t nr_src_bytes = 0;
+  std::vector<int3> nr_groups;             // (pass shape, first item, count) per k_near launch
   int* d_near_off = nullptr; int4* d_near_seg = nullptr; int n_near_seg = 0;
   int* d_far_off = nullptr;  int4* d_far_seg = nullptr;  int n_far_seg = 0;
   int* d_all_off = nullptr;  int4* d_all_seg = nullptr;  // near + far segments (fused pass)
@@ -279,6 +292,12 @@ const char* last_error();
 // setup stages (tree.cu, lists.cu) and matvec launches (kernels.cu)
 int build_tree_device(Plan& P, const double* d_points_caller, cudaStream_t st);
 int build_lists_device(Plan& P, cudaStream_t st);
+constexpr int NR_CH = 256;               // k_near sources per chunk
+int near_shape_count(int tab);           // k_near pass shapes of table tab, by capacity
+int near_shape_cap(int tab, int shape);  // TB x MQ targets per pass
+extern int g_num_sms;
+extern int g_launches;
+int near_launch(const Plan& P, double* out, cudaStream_t st);
 int build_schedules(Plan& P, cudaStream_t st);
 int upload_tables(Plan& P);
 int kernels_init();

@@ -1184,13 +1184,14 @@ __global__ void k_unpack_rows(double* __restrict__ dst, int ld, const int* __res
 // ----------------------------------------------------------------------------
 // host-side launch helpers
 // ----------------------------------------------------------------------------
+int g_num_sms = 148;  // set at setup (cudaDevAttrMultiProcessorCount)
+int g_launches = 0;   // kernels launched by the current matvec (fmm_info.gpu_launches)
+
 namespace {
 
 inline int nblk(int64_t n, int t = 256) { return std::max(1, (int)((n + t - 1) / t)); }
 
 int ggs_nt(int M, int K) { return (size_t)(K + 4 + M + 2) * 64 * 8 <= 116 * 1024 ? 64 : 32; }
-
-int g_num_sms = 148;
 
 constexpr int sq_nt(int kp) { return kp <= 64 ? 64 : 32; }
 size_t sq_smem(int kp) { return (size_t)sq_nt(kp) * 2 * (kp + 4) * sizeof(double); }
@@ -1206,8 +1207,6 @@ int launch_sq(const GemmLaunch& g, const double* ops, int mvalid, const double* 
   k_ggs_sq<KP, NT><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_pairs, ops, mvalid, X, Y, atomic);
   return 0;
 }
-
-int g_launches = 0;
 
 int launch_ggs(const GemmLaunch& g, const double* ops, int op_stride, int M, int K, int mvalid, const double* X,
                int ldx, double* Y, int ldy, bool atomic, cudaStream_t st) {
@@ -1826,6 +1825,10 @@ static int launch_sym(const Plan& P, cudaStream_t st);
 
 // near field into pot_near: one-sided segments (own leaf first, U, direct W/X) + symmetric pairs
 static int launch_near(const Plan& P, const EvalArgs& ea, cudaStream_t st) {
+  if (P.nr_on) {  // mutual leaf pairs (near.cu): every result added with RED
+    KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * P.tree.N, st));
+    return near_launch(P, P.d_pot_near, st);
+  }
   if (P.n_tleaf > 0) {
     EvalArgs a = ea;
     a.seg_off = P.d_near_off; a.segs = P.d_near_seg; a.out = P.d_pot_near;
@@ -2045,18 +2048,25 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
             P.d_tleaf_items, P.n_tleaf, T.d_level, T.d_pbeg, T.d_pend, P.d_l2t_mat, P.d_lhat, kp, Dp.own_lo, far_out);
         KIFMM_CUDA(cudaGetLastError());
       }
+      // mutual near field fused into pot_near: after the stored L2T (else on zeros), before
+      // the far segments (k_eval below adds to the result)
+      const bool nr_fused = P.nr_on && !sep;
+      if (nr_fused) {
+        if (!P.leaf_l2t) KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, st));
+        if (near_launch(P, P.d_pot_near, st)) return -3;
+      }
       // L2T + W stage 2 (and, fused, the near field): potentials at the targets of each leaf
-      if (P.n_tleaf > 0 && !(sep && P.leaf_l2t && P.n_far_seg == 0)) {
+      if (P.n_tleaf > 0 && !(sep && P.leaf_l2t && P.n_far_seg == 0) && !(nr_fused && P.n_far_seg == 0)) {
         EvalArgs a = ea;
         a.items = P.d_tleaf_items;
-        a.accumulate = P.leaf_l2t ? 1 : 0;
+        a.accumulate = P.leaf_l2t || nr_fused ? 1 : 0;
         a.nrm = nullptr;  // far sources are equivalent surfaces: single layer
         a.tri = nullptr;
-        if (sep) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; }
+        if (sep || nr_fused) { a.seg_off = P.d_far_off; a.segs = P.d_far_seg; }
         else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; }
         a.out = far_out;
         a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
-        launch_eval(P, a, sep ? 0 : 1, st);
+        launch_eval(P, a, sep || nr_fused ? 0 : 1, st);
         ++g_launches;
         KIFMM_CUDA(cudaGetLastError());
       }

@@ -132,13 +132,29 @@ int build_schedules(Plan& P, cudaStream_t st) {
     const int b = titems[i].x;
     near[i].push_back(make_int4(0, T.pbeg[b], 0, npts(b)));
   }
-  // symmetric pairs (k_p2p_sym): U pairs and direct W pairs with a leaf source (whose
-  // mirror is the direct X pair), both leaves owned; evaluated once for both sides
-  // A pair goes symmetric when k_p2p_sym's padding (targets in passes of 32 TB lanes,
-  // sources in batches of 16) wastes little: its cost per useful pair is then ~13 FP64
-  // ops for both directions against 2 x 12 one-sided (measured: a win for C5's
-  // 88-point leaves, a loss for C2/C4's ~33-point ones without this filter).
-  const bool sym = P.sym_opt != 0;
+  // Symmetric near field: U pairs and direct W pairs with a leaf source (whose mirror is
+  // the direct X pair), both leaves owned, evaluated once for both sides.
+  //  * mutual mode (default): the pair becomes a mutual source segment of ONE of its
+  //    leaves, evaluated by k_near (near.cu: ~13 FP64 ops per unordered pair against
+  //    2 x 12 one-sided); the target side is the leaf whose k_near pass pads least
+  //    (TB x MQ slots), ties split by index parity;
+  //  * warp-pair mode (KIFMM_SYM=2): k_p2p_sym, one warp per pair, chosen per pair when
+  //    its padding (targets in passes of 32 TB lanes, sources in batches of 16) is small.
+  bool mutual = P.sym_opt == -1 || P.sym_opt == 1;
+  const bool sym = P.sym_opt == 2;
+  if (mutual) {  // k_near's source-slot table (4 B per near-field source) must fit the budget
+    int64_t slots = 0;
+    for (auto& u : U)
+      if (inD(u.x)) slots += npts(u.y);
+    for (auto& w : W)
+      if (inD(w.x) && w.z) slots += npts(w.y);
+    for (auto& x : X)
+      if (inD(x.x) && x.z) slots += npts(x.y);
+    size_t fr = 0, tot = 0;
+    KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
+    const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot);
+    if (4.0 * (double)slots > budget) mutual = false;
+  }
   static const double sym_r = [] { const char* e = std::getenv("KIFMM_SYM_R"); return e ? std::atof(e) : 1.4; }();
   auto pass_slots = [](int m) { int full = m / 96, rem = m - 96 * full; return 96 * full + 32 * ((rem + 31) / 32); };
   auto pad_ratio = [&](int mt, int ms) {
@@ -151,10 +167,36 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (std::min(r1, r2) > sym_r) return 0;
     return r1 <= r2 ? 1 : 2;
   };
+  // k_near pass shape of an m-point leaf (the least padding; passes of the largest beyond it)
+  static const int nr_tab = [] { const char* e = std::getenv("KIFMM_NEAR_TAB"); return e ? std::atoi(e) : 0; }();
+  P.nr_table = nr_tab;
+  const int kNearShapes = near_shape_count(nr_tab);
+  auto nr_shape = [&](int m) {
+    for (int c = 0; c < kNearShapes; ++c)
+      if (m <= near_shape_cap(nr_tab, c)) return c;
+    return kNearShapes - 1;
+  };
+  auto nr_slots = [&](int m) {
+    const int cap = near_shape_cap(nr_tab, nr_shape(m));
+    return (m + cap - 1) / cap * cap;
+  };
+  // target side of a mutual pair {a, b}, or -1 (not both owned)
+  static const bool mut_off = std::getenv("KIFMM_MUT_OFF") != nullptr;  // diagnostics: k_near one-sided only
+  auto mut_target = [&](int a, int b) {
+    if (!mutual || mut_off || !inD(a) || !inD(b)) return -1;
+    const int64_t ca = (int64_t)nr_slots(npts(a)) * npts(b), cb = (int64_t)nr_slots(npts(b)) * npts(a);
+    if (ca != cb) return ca < cb ? a : b;
+    return ((a ^ b) & 1) ? std::min(a, b) : std::max(a, b);
+  };
+  std::vector<std::vector<int4>> mnear(nt);
   std::vector<int2> sympairs;
   auto add_sym = [&](int a, int b, int c) { sympairs.push_back(c == 1 ? make_int2(a, b) : make_int2(b, a)); };
   for (auto& u : U) {
     if (!inD(u.x) || u.y == u.x) continue;
+    if (int t = mut_target(u.x, u.y); t >= 0) {
+      if (t == u.x) mnear[leaf_row[u.x]].push_back(make_int4(3, T.pbeg[u.y], 0, npts(u.y)));
+      continue;
+    }
     if (int c = sym_choice(u.x, u.y)) {
       if (u.x < u.y) add_sym(u.x, u.y, c);
       continue;
@@ -168,6 +210,11 @@ int build_schedules(Plan& P, cudaStream_t st) {
   for (auto& w : W) {
     if (!inD(w.x)) continue;
     if (w.z && T.leaf[w.y]) {
+      if (int t = mut_target(w.x, w.y); t >= 0) {
+        const int o = t == w.x ? w.y : w.x;
+        mnear[leaf_row[t]].push_back(make_int4(3, T.pbeg[o], 0, npts(o)));
+        continue;
+      }
       if (int c = sym_choice(w.x, w.y)) {
         add_sym(w.x, w.y, c);
         continue;
@@ -189,7 +236,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   std::vector<PairGroup> xgroup{PairGroup{0, 1.0, {}}};
   for (auto& x : X) {
     if (!inD(x.x)) continue;
-    if (x.z && sym_choice(x.x, x.y)) continue;  // mirror of a symmetric W pair
+    if (x.z && (mut_target(x.x, x.y) >= 0 || sym_choice(x.x, x.y))) continue;  // mirror of a symmetric W pair
     if (x.z) {
       near[leaf_row[x.x]].push_back(make_int4(0, T.pbeg[x.y], 0, npts(x.y)));
     } else {
@@ -212,6 +259,72 @@ int build_schedules(Plan& P, cudaStream_t st) {
     lgroups[llevel[lv]].pairs.push_back(make_int2(b, n_l2t));
     far[i].insert(far[i].begin(), make_int4(1, n_l2t, b, n));
     ++n_l2t;
+  }
+  // k_near tables (mutual mode): per target leaf its source list — own points (checked),
+  // mutual segments, one-sided point segments — cut into chunks of NR_CH source slots;
+  // leaves grouped by pass shape (groups under kMinGroup leaves join the next larger
+  // shape), Morton order within a group
+  P.nr_on = mutual;
+  P.n_tleaf_mut = 0;
+  P.n_mut_pairs = 0;
+  P.nr_groups.clear();
+  if (mutual && nt > 0) {
+    constexpr int kMinGroup = 256;
+    std::vector<int> shp(nt), cnt(kNearShapes, 0);
+    for (int i = 0; i < nt; ++i) ++cnt[shp[i] = nr_shape(npts(titems[i].x))];
+    int cmax = 0;
+    for (int c = 0; c < kNearShapes; ++c)
+      if (cnt[c]) cmax = c;
+    std::vector<int> remap(kNearShapes);
+    for (int c = 0, carry = 0; c < kNearShapes; ++c) {
+      remap[c] = c;
+      if (c < cmax && cnt[c] + carry < kMinGroup) { carry += cnt[c]; remap[c] = -1; }
+      else carry = 0;
+    }
+    for (int c = cmax - 1; c >= 0; --c)
+      if (remap[c] < 0) remap[c] = remap[c + 1];
+    std::vector<int4> nitems, nchunks;
+    std::vector<int> nsrc;
+    for (int c = 0; c < kNearShapes; ++c) {
+      const int first = (int)nitems.size();
+      for (int i = 0; i < nt; ++i) {
+        if (remap[shp[i]] != c) continue;
+        const int b = titems[i].x;
+        if (!mnear[i].empty()) ++P.n_tleaf_mut;
+        for (auto& sg : mnear[i]) P.n_mut_pairs += (int64_t)npts(b) * sg.w;
+        const int cb = (int)nchunks.size();
+        int n = 0, nchk = 0, ml = -1, mh = -1;
+        auto flush = [&]() {
+          if (n == 0) return;
+          if (ml < 0) ml = mh = n;
+          nchunks.push_back(make_int4((int)(nsrc.size() - n), n | (nchk << 10) | (ml << 20), mh, 0));
+          n = nchk = 0;
+          ml = mh = -1;
+        };
+        auto add = [&](int kind, int a, int len) {  // kind 0 one-sided, 1 own points, 3 mutual
+          for (int off = 0; off < len;) {
+            const int take = std::min(len - off, NR_CH - n);
+            if (kind == 1) nchk = n + take;
+            if (kind == 3) { if (ml < 0) ml = n; mh = n + take; }
+            for (int t = 0; t < take; ++t) nsrc.push_back(a + off + t);
+            n += take;
+            off += take;
+            if (n == NR_CH) flush();
+          }
+        };
+        add(1, T.pbeg[b], npts(b));
+        for (auto& sg : mnear[i]) add(3, sg.y, sg.w);
+        for (size_t k = 1; k < near[i].size(); ++k) add(0, near[i][k].y, near[i][k].w);
+        flush();
+        nitems.push_back(make_int4(T.pbeg[b], npts(b), cb, (int)nchunks.size()));
+      }
+      if ((int)nitems.size() > first) P.nr_groups.push_back(make_int3(c, first, (int)nitems.size() - first));
+    }
+    P.nr_src_bytes = (int64_t)nsrc.size() * sizeof(int);
+    std::vector<int> counters(P.nr_groups.size(), 0);
+    if (upload(P, &P.d_nr_items, nitems, st) || upload(P, &P.d_nr_chunks, nchunks, st) ||
+        upload(P, &P.d_nr_src, nsrc, st) || upload(P, &P.d_nr_counters, counters, st))
+      return -3;
   }
   std::vector<int> near_off{0}, far_off{0}, all_off{0};
   std::vector<int4> near_seg, far_seg, all_seg;

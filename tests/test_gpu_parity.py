@@ -278,3 +278,35 @@ def test_double_layer_gauss_and_loopback():
     plans = [K().Plan(Pt, None, p=8, k=100, leaf_size=64, tables=tb, normals=Nt, nranks=3, rank=r) for r in range(3)]
     for pt in K().fmm_matvec_group(plans, [Qt] * 3, owned=False):
         assert rel(pt.cpu().numpy(), ref) <= TOL
+
+
+NEAR_CASES = {
+    "sphere6k_s16": lambda: sphere(6000, 1) + (6, 60, 16),
+    "clustered4k_s8": lambda: clustered(4000, 2) + (4, 24, 8),
+    "torus50k": lambda: synth_inputs.torus(50000) + (6, 60, 128),
+    # leaves up to 400 points: several k_near passes per leaf, chunks split inside leaves
+    "sphere20k_s400": lambda: sphere(20000, 5) + (4, 24, 400),
+}
+
+
+@pytest.mark.parametrize("case", list(NEAR_CASES))
+@pytest.mark.parametrize("mode", ["1", "2", "0"])
+def test_near_field_modes(case, mode, monkeypatch):
+    """Mutual leaf pairs (k_near, default), warp-pair symmetric (k_p2p_sym) and all
+    one-sided (k_eval) give the oracle's result; fused and split passes."""
+    pts, q, p, k, s = NEAR_CASES[case]()
+    tb = tables(p, k)
+    op = oracle.Plan(pts, s, tb["n"])
+    ref, ph = op.matvec(tb, q, phases=True)
+    monkeypatch.setenv("KIFMM_SYM", mode)
+    for split in (False, True):
+        gp = gpu_plan(pts, p, k, s, tb=tb, split_phases=split)
+        inf = gp.info
+        if mode == "1":
+            assert inf["near_mutual_leaves"] > 0 and inf["near_mutual_pairs"] > 0 and inf["near_sym_pairs"] == 0
+        else:
+            assert inf["near_mutual_leaves"] == 0
+        out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+        assert rel(out, ref) <= TOL, (mode, split)
+        if split:
+            assert rel(gp.export_phase("near"), ph["near"]) <= TOL
