@@ -45,7 +45,7 @@ constexpr int NR_NT = 128;
 constexpr int NR_PER = NR_CH / NR_NT;  // sources staged per thread and chunk
 
 struct NearArgs {
-  const int4* items;    // (first target point, m, chunk begin, chunk end)
+  const int4* items;    // work units: (first target point, targets <= TB MQ, chunk begin, chunk end)
   int nitems;
   const int4* chunks;   // (first source slot, n | nchk << 10 | ml << 20, mh, 0)
   const int* src;       // per chunk: the point index of each source slot
@@ -136,12 +136,12 @@ __device__ __forceinline__ void nr_mutual(const double4* sbuf, const int* sidx, 
   if (s0 < nsteps) nr_mutual_batch<TB, MQ, 1, true>(sbuf, sidx, j0, j1, G, s0, x, q, acc, out);
 }
 
-// the CTA's work sequence: item blockIdx.x, then items taken from a global counter
-// (dynamic: leaves differ in cost), two ahead of use through a 4-slot ring in shared
-// memory; per item its passes of CAP targets; per pass the item's chunks
+// the CTA's work sequence: unit blockIdx.x, then units taken from a global counter
+// (dynamic: units differ in cost; the host orders them longest first), two ahead of use
+// through a 4-slot ring in shared memory; per unit its chunks
 struct Cursor {
-  int item, pass, chunk;
-  int4 rec;    // this item's record
+  int item, chunk;
+  int4 rec;  // this unit's record
 };
 
 template <int TB, int MQ>
@@ -162,11 +162,9 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
 
   auto advance = [&](Cursor c) {
     if (++c.chunk < c.rec.w) return c;
-    if ((++c.pass) * CAP < c.rec.y) { c.chunk = c.rec.z; return c; }
     c.item = s_ring[ring & 3];
     if (tid == 0) s_ring[(ring + 2) & 3] = (int)gridDim.x + atomicAdd(A.counter, 1);
     ++ring;
-    c.pass = 0;
     if (c.item < A.nitems) {
       c.rec = A.items[c.item];
       c.chunk = c.rec.z;
@@ -189,9 +187,8 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
       }
     }
     if (c.chunk == c.rec.z) {
-      const int t0 = c.pass * CAP, mm = min(CAP, c.rec.y - t0);
-      for (int i = tid; i < mm; i += NT) {
-        const double* src = reinterpret_cast<const double*>(A.pts + c.rec.x + t0 + i);
+      for (int i = tid; i < c.rec.y; i += NT) {
+        const double* src = reinterpret_cast<const double*>(A.pts + c.rec.x + i);
         double* dst = reinterpret_cast<double*>(&tbuf[b][i]);
         nr_cp16(dst, src);
         nr_cp16(dst + 2, src + 2);
@@ -215,7 +212,6 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
   __syncthreads();
   Cursor cur;
   cur.item = blockIdx.x;
-  cur.pass = 0;
   cur.rec = A.items[cur.item];
   cur.chunk = cur.rec.z;
   // prologue: stage chunk 0; chunk 1's record and indices in registers
@@ -248,8 +244,8 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
         load_idx(ck_nn, idx);
       }
     }
-    if (cur.chunk == cur.rec.z) {  // first chunk of a pass: its targets
-      mm = min(CAP, cur.rec.y - cur.pass * CAP);
+    if (cur.chunk == cur.rec.z) {  // first chunk of a unit: its targets
+      mm = cur.rec.y;
 #pragma unroll
       for (int u = 0; u < TB; ++u) {
         const int i = ti + u * MQ;
@@ -272,16 +268,15 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
       if (mh > ml) nr_mutual<TB, MQ>(sbuf[b], sidx[b], ml, first(ml), mh, G, x, q, acc, A.out);
       if (n > mh) nr_onesided<TB, false>(sbuf[b], first(mh), n, G, x, acc);
     }
-    if (cur.chunk + 1 == cur.rec.w) {  // last chunk of the pass: sum the slices, RED into p
+    if (cur.chunk + 1 == cur.rec.w) {  // last chunk of the unit: sum the slices, RED into p
 #pragma unroll
       for (int u = 0; u < TB; ++u) red[u * NT + tid] = acc[u];
       __syncthreads();
-      const int t0 = cur.pass * CAP;
       for (int i = tid; i < mm; i += NT) {
         const int u = i / MQ, tl = i - u * MQ;
         double sum = 0.0;
         for (int g = 0; g < G; ++g) sum += red[u * NT + g * MQ + tl];
-        atomicAdd(A.out + cur.rec.x + t0 + i, sum * kInv4Pi);
+        atomicAdd(A.out + cur.rec.x + i, sum * kInv4Pi);
       }
     }
     if (!more) break;

@@ -262,16 +262,58 @@ int build_schedules(Plan& P, cudaStream_t st) {
   }
   // k_near tables (mutual mode): per target leaf its source list — own points (checked),
   // mutual segments, one-sided point segments — cut into chunks of NR_CH source slots;
-  // leaves grouped by pass shape (groups under kMinGroup leaves join the next larger
-  // shape), Morton order within a group
+  // work units = (pass of <= TB x MQ targets, <= kUnitChunks chunks), grouped by pass
+  // shape (groups under kMinGroup units join the next larger shape), longest first
   P.nr_on = mutual;
   P.n_tleaf_mut = 0;
   P.n_mut_pairs = 0;
   P.nr_groups.clear();
   if (mutual && nt > 0) {
-    constexpr int kMinGroup = 256;
+    static const int kMinGroup = [] { const char* e = std::getenv("KIFMM_NEAR_MINGROUP"); return e ? std::atoi(e) : 2048; }();
+    static const int kUnitChunks = [] { const char* e = std::getenv("KIFMM_NEAR_UNIT"); return e ? std::atoi(e) : 4; }();
     std::vector<int> shp(nt), cnt(kNearShapes, 0);
-    for (int i = 0; i < nt; ++i) ++cnt[shp[i] = nr_shape(npts(titems[i].x))];
+    for (int i = 0; i < nt; ++i) shp[i] = nr_shape(npts(titems[i].x));
+    std::vector<int4> nchunks;
+    std::vector<int> nsrc;
+    std::vector<std::vector<std::pair<int64_t, int4>>> units(kNearShapes);  // (cost, unit) per shape
+    for (int i = 0; i < nt; ++i) {
+      const int b = titems[i].x;
+      if (!mnear[i].empty()) ++P.n_tleaf_mut;
+      for (auto& sg : mnear[i]) P.n_mut_pairs += (int64_t)npts(b) * sg.w;
+      const int cb = (int)nchunks.size();
+      int n = 0, nchk = 0, ml = -1, mh = -1;
+      auto flush = [&]() {
+        if (n == 0) return;
+        if (ml < 0) ml = mh = n;
+        nchunks.push_back(make_int4((int)(nsrc.size() - n), n | (nchk << 10) | (ml << 20), mh, 0));
+        n = nchk = 0;
+        ml = mh = -1;
+      };
+      auto add = [&](int kind, int a, int len) {  // kind 0 one-sided, 1 own points, 3 mutual
+        for (int off = 0; off < len;) {
+          const int take = std::min(len - off, NR_CH - n);
+          if (kind == 1) nchk = n + take;
+          if (kind == 3) { if (ml < 0) ml = n; mh = n + take; }
+          for (int t = 0; t < take; ++t) nsrc.push_back(a + off + t);
+          n += take;
+          off += take;
+          if (n == NR_CH) flush();
+        }
+      };
+      add(1, T.pbeg[b], npts(b));
+      for (auto& sg : mnear[i]) add(3, sg.y, sg.w);
+      for (size_t k = 1; k < near[i].size(); ++k) add(0, near[i][k].y, near[i][k].w);
+      flush();
+      const int ce = (int)nchunks.size(), cap = near_shape_cap(nr_tab, shp[i]);
+      for (int t0 = 0; t0 < npts(b); t0 += cap)
+        for (int c0 = cb; c0 < ce; c0 += kUnitChunks) {
+          const int c1 = std::min(ce, c0 + kUnitChunks);
+          int64_t srcs = 0;
+          for (int c = c0; c < c1; ++c) srcs += nchunks[c].y & 1023;
+          units[shp[i]].push_back({srcs * cap, make_int4(T.pbeg[b] + t0, std::min(cap, npts(b) - t0), c0, c1)});
+          ++cnt[shp[i]];
+        }
+    }
     int cmax = 0;
     for (int c = 0; c < kNearShapes; ++c)
       if (cnt[c]) cmax = c;
@@ -283,42 +325,17 @@ int build_schedules(Plan& P, cudaStream_t st) {
     }
     for (int c = cmax - 1; c >= 0; --c)
       if (remap[c] < 0) remap[c] = remap[c + 1];
-    std::vector<int4> nitems, nchunks;
-    std::vector<int> nsrc;
+    // a unit of a smaller shape runs as the larger shape's pass (more padding, same result)
+    std::vector<int4> nitems;
     for (int c = 0; c < kNearShapes; ++c) {
+      std::vector<std::pair<int64_t, int4>> g;
+      for (int c2 = 0; c2 < kNearShapes; ++c2)
+        if (remap[c2] == c) g.insert(g.end(), units[c2].begin(), units[c2].end());
+      if (g.empty()) continue;
+      std::stable_sort(g.begin(), g.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
       const int first = (int)nitems.size();
-      for (int i = 0; i < nt; ++i) {
-        if (remap[shp[i]] != c) continue;
-        const int b = titems[i].x;
-        if (!mnear[i].empty()) ++P.n_tleaf_mut;
-        for (auto& sg : mnear[i]) P.n_mut_pairs += (int64_t)npts(b) * sg.w;
-        const int cb = (int)nchunks.size();
-        int n = 0, nchk = 0, ml = -1, mh = -1;
-        auto flush = [&]() {
-          if (n == 0) return;
-          if (ml < 0) ml = mh = n;
-          nchunks.push_back(make_int4((int)(nsrc.size() - n), n | (nchk << 10) | (ml << 20), mh, 0));
-          n = nchk = 0;
-          ml = mh = -1;
-        };
-        auto add = [&](int kind, int a, int len) {  // kind 0 one-sided, 1 own points, 3 mutual
-          for (int off = 0; off < len;) {
-            const int take = std::min(len - off, NR_CH - n);
-            if (kind == 1) nchk = n + take;
-            if (kind == 3) { if (ml < 0) ml = n; mh = n + take; }
-            for (int t = 0; t < take; ++t) nsrc.push_back(a + off + t);
-            n += take;
-            off += take;
-            if (n == NR_CH) flush();
-          }
-        };
-        add(1, T.pbeg[b], npts(b));
-        for (auto& sg : mnear[i]) add(3, sg.y, sg.w);
-        for (size_t k = 1; k < near[i].size(); ++k) add(0, near[i][k].y, near[i][k].w);
-        flush();
-        nitems.push_back(make_int4(T.pbeg[b], npts(b), cb, (int)nchunks.size()));
-      }
-      if ((int)nitems.size() > first) P.nr_groups.push_back(make_int3(c, first, (int)nitems.size() - first));
+      for (auto& u : g) nitems.push_back(u.second);
+      P.nr_groups.push_back(make_int3(c, first, (int)nitems.size() - first));
     }
     P.nr_src_bytes = (int64_t)nsrc.size() * sizeof(int);
     std::vector<int> counters(P.nr_groups.size(), 0);
