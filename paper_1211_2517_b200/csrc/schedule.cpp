@@ -263,7 +263,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   // k_near tables (mutual mode): per target leaf its source list — own points (checked),
   // mutual segments, one-sided point segments — cut into chunks of NR_CH source slots;
   // work units = (pass of <= TB x MQ targets, <= kUnitChunks chunks), grouped by pass
-  // shape (groups under kMinGroup units join the next larger shape), longest first
+  // shape (see below), longest first
   P.nr_on = mutual;
   P.n_tleaf_mut = 0;
   P.n_mut_pairs = 0;
@@ -271,8 +271,24 @@ int build_schedules(Plan& P, cudaStream_t st) {
   if (mutual && nt > 0) {
     static const int kMinGroup = [] { const char* e = std::getenv("KIFMM_NEAR_MINGROUP"); return e ? std::atoi(e) : 2048; }();
     static const int kUnitChunks = [] { const char* e = std::getenv("KIFMM_NEAR_UNIT"); return e ? std::atoi(e) : 4; }();
+    // pass shape per leaf: the least-padding shape, unless its group would have fewer than
+    // kMinGroup leaves — then the next larger kept shape (more padding), or for the
+    // largest leaves the largest kept smaller shape (more passes)
     std::vector<int> shp(nt), cnt(kNearShapes, 0);
-    for (int i = 0; i < nt; ++i) shp[i] = nr_shape(npts(titems[i].x));
+    for (int i = 0; i < nt; ++i) ++cnt[shp[i] = nr_shape(npts(titems[i].x))];
+    {
+      std::vector<int> kept;
+      for (int c = 0; c < kNearShapes; ++c)
+        if (cnt[c] >= kMinGroup) kept.push_back(c);
+      if (kept.empty()) kept.push_back(*std::max_element(shp.begin(), shp.end()));
+      std::vector<int> remap(kNearShapes);
+      for (int c = 0; c < kNearShapes; ++c) {
+        auto it = std::lower_bound(kept.begin(), kept.end(), c);
+        remap[c] = it != kept.end() ? *it : kept.back();
+      }
+      for (int i = 0; i < nt; ++i) shp[i] = remap[shp[i]];
+      std::fill(cnt.begin(), cnt.end(), 0);
+    }
     std::vector<int4> nchunks;
     std::vector<int> nsrc;
     std::vector<std::vector<std::pair<int64_t, int4>>> units(kNearShapes);  // (cost, unit) per shape
@@ -314,23 +330,9 @@ int build_schedules(Plan& P, cudaStream_t st) {
           ++cnt[shp[i]];
         }
     }
-    int cmax = 0;
-    for (int c = 0; c < kNearShapes; ++c)
-      if (cnt[c]) cmax = c;
-    std::vector<int> remap(kNearShapes);
-    for (int c = 0, carry = 0; c < kNearShapes; ++c) {
-      remap[c] = c;
-      if (c < cmax && cnt[c] + carry < kMinGroup) { carry += cnt[c]; remap[c] = -1; }
-      else carry = 0;
-    }
-    for (int c = cmax - 1; c >= 0; --c)
-      if (remap[c] < 0) remap[c] = remap[c + 1];
-    // a unit of a smaller shape runs as the larger shape's pass (more padding, same result)
     std::vector<int4> nitems;
     for (int c = 0; c < kNearShapes; ++c) {
-      std::vector<std::pair<int64_t, int4>> g;
-      for (int c2 = 0; c2 < kNearShapes; ++c2)
-        if (remap[c2] == c) g.insert(g.end(), units[c2].begin(), units[c2].end());
+      std::vector<std::pair<int64_t, int4>>& g = units[c];
       if (g.empty()) continue;
       std::stable_sort(g.begin(), g.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
       const int first = (int)nitems.size();
