@@ -197,6 +197,8 @@ struct Plan {
   std::vector<int3> nr_groups;             // (pass shape, first item, count) per k_near launch
   int* d_near_off = nullptr; int4* d_near_seg = nullptr; int n_near_seg = 0;
   int* d_far_off = nullptr;  int4* d_far_seg = nullptr;  int n_far_seg = 0;
+  int n_fitems = 0; int4* d_fitems = nullptr;      // target leaves with far segments (compact far pass)
+  int* d_fitem_off = nullptr; int4* d_fitem_seg = nullptr;
   int* d_all_off = nullptr;  int4* d_all_seg = nullptr;  // near + far segments (fused pass)
   bool split_phases = false;  // separate near / far passes (phase exports)
   // per-leaf operators (leaf-op mode): S2M  q^'_B = S_B q_B  with S_B = S' G(UC_B, x_B)

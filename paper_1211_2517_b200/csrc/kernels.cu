@@ -1813,12 +1813,16 @@ int kernels_init() {
 // Evaluation work lists live in the plan; see build_schedules (schedule.cpp).
 // k_eval with 128 threads per target leaf (measured best of 128 / 256 threads and
 // a warp-per-leaf variant; KIFMM_EVAL_NT=256 selects the 256-thread kernel)
-static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st, bool dl = false) {
+static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st, bool dl = false, int nitems = -1) {
   static const int nt = [] { const char* e = std::getenv("KIFMM_EVAL_NT"); return e ? std::atoi(e) : 128; }();
-  a.items = P.d_tleaf_items;
-  if (dl) k_eval<128, 256, true><<<P.n_tleaf, 128, 0, st>>>(a, chk_self);
-  else if (nt == 256) k_eval<256, 512><<<P.n_tleaf, 256, 0, st>>>(a, chk_self);
-  else k_eval<128, 256><<<P.n_tleaf, 128, 0, st>>>(a, chk_self);
+  if (nitems < 0) {
+    a.items = P.d_tleaf_items;
+    nitems = P.n_tleaf;
+  }
+  if (nitems == 0) return;
+  if (dl) k_eval<128, 256, true><<<nitems, 128, 0, st>>>(a, chk_self);
+  else if (nt == 256) k_eval<256, 512><<<nitems, 256, 0, st>>>(a, chk_self);
+  else k_eval<128, 256><<<nitems, 128, 0, st>>>(a, chk_self);
 }
 
 static int launch_sym(const Plan& P, cudaStream_t st);
@@ -2066,7 +2070,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         else { a.seg_off = P.d_all_off; a.segs = P.d_all_seg; }
         a.out = far_out;
         a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
-        launch_eval(P, a, sep || nr_fused ? 0 : 1, st);
+        int nitems = -1;  // adding to stored results: only the leaves that have far segments
+        if ((sep || nr_fused) && a.accumulate) {
+          a.items = P.d_fitems; a.seg_off = P.d_fitem_off; a.segs = P.d_fitem_seg;
+          nitems = P.n_fitems;
+        }
+        launch_eval(P, a, sep || nr_fused ? 0 : 1, st, false, nitems);
         ++g_launches;
         KIFMM_CUDA(cudaGetLastError());
       }

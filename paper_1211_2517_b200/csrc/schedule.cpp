@@ -377,6 +377,20 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (int rc = bem_build_near(P, blocks, st)) return rc;
   }
   P.n_far_seg = (int)far_seg.size();
+  {  // the far pass over only the leaves with far segments (when it adds to stored results)
+    std::vector<int4> fi, fs;
+    std::vector<int> fo{0};
+    for (int i = 0; i < nt; ++i) {
+      if (far[i].empty()) continue;
+      fi.push_back(titems[i]);
+      fs.insert(fs.end(), far[i].begin(), far[i].end());
+      fo.push_back((int)fs.size());
+    }
+    P.n_fitems = (int)fi.size();
+    if (P.n_fitems > 0 &&
+        (upload(P, &P.d_fitems, fi, st) || upload(P, &P.d_fitem_off, fo, st) || upload(P, &P.d_fitem_seg, fs, st)))
+      return -3;
+  }
   if (upload(P, &P.d_tleaf_items, titems, st) ||
       (!P.bem && (upload(P, &P.d_near_off, near_off, st) || upload(P, &P.d_near_seg, near_seg, st))) ||
       upload(P, &P.d_far_off, far_off, st) ||
