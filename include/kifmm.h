@@ -139,6 +139,8 @@ typedef struct {
   int64_t near_mutual_leaves; /* target leaves evaluating symmetric (mutual) leaf pairs */
   int64_t near_mutual_pairs;  /* unordered near-field point pairs evaluated once for both sides */
   int64_t near_sym_pairs;     /* leaf pairs of the warp-pair symmetric kernel (KIFMM_SYM=2) */
+  double m2l_exec_flops;      /* M2L flops the kernels execute: 2 k^2 per sibling-class column
+                                 step (absent children included) + the offset-major pairs */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

@@ -509,8 +509,11 @@ int build_schedules(Plan& P, cudaStream_t st) {
         for (int e = e0; e < e1; ++e)
           if (T.parent[vby[e].y] == qs[i]) { src[T.key[vby[e].y] & 7] = vby[e].y; ++cnt; }
         // cost model (per column, FP64 peak 37 TF/s, fp64 L2 RED 5.2e11/s): the sibling
-        // kernel spends nvalid GEMM columns + 1 RED row, offset-major cnt x (GEMM + RED row)
-        const double Gc = 2.0 * kp * kp / 37e12, Rr = kp / 5.2e11;
+        // kernel spends nvalid GEMM columns + 1 RED row, offset-major cnt x (GEMM + RED row);
+        // the RED weight 0.5 is the measured best of 0.25 / 0.5 / 1 / 2 over C3-C5
+        // (tools/m2l_scale.py: C4 M2L 6.49 ms at 0.5 vs 6.51 at 1; C5 29.0 vs 29.2)
+        static const double red_scale = [] { const char* e = std::getenv("KIFMM_M2L_RED_SCALE"); return e ? std::atof(e) : 0.5; }();
+        const double Gc = 2.0 * kp * kp / 37e12, Rr = red_scale * kp / 5.2e11;
         if (cnt * (Gc + Rr) >= nvalid[cls] * Gc + Rr) {
           auto& cc = cls_cols[cls];
           cc.push_back(b);
@@ -531,6 +534,9 @@ int build_schedules(Plan& P, cudaStream_t st) {
       }
     }
     if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
+    P.m2l_exec_flops = 0;
+    for (int cls = 0; cls < kCls; ++cls) P.m2l_exec_flops += (double)nvalid[cls] * (cls_cols[cls].size() / 9) * 2.0 * P.k * P.k;
+    for (auto& g : groups) P.m2l_exec_flops += (double)g.pairs.size() * 2.0 * P.k * P.k;
     // sibling tiles: per class, columns in target order, NT columns per tile
     const int NTs = sib_tile_width(kp, P.lr.on && P.lr.rp <= 32);  // (k_m2l_lr2 takes rp 16 / 32)
     std::vector<int> cols;
