@@ -246,12 +246,20 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
       return fail(FMM_ECUDA);
     }
   }
-  // KIFMM_OVERLAP=1 (diagnostics): near field on a second stream, concurrent with S2M /
-  // M2M / M2L.  Off by default: both fields are bound by the one FP64 datapath and the
-  // near-field CTAs take the SMs first (measured C2 -1%, C3 +3.5%, C4 +5%)
+  // Near field on a second stream (overlap modes; KIFMM_OVERLAP overrides):
+  //  3 (default with the mutual near field): k_near in two halves on the near stream —
+  //    units [0, nr_split) from the fork after the densities, the rest after the M2L —
+  //    beside the S2M / M2M / X / L2T GEMVs and the far pass; results joined before the
+  //    output (C2 -2.5%, C3 -10%, C4 / C5 +-0.2%).  Off in profiled plans: per-phase
+  //    events on one stream need the phases serialised.
+  //  1 / 2 (diagnostics, k_eval era): whole near field forked after the densities /
+  //    beside a high-priority M2L stream.
   {
     const char* e = std::getenv("KIFMM_OVERLAP");
-    P.overlap = (!P.split_phases && !P.bem && e) ? std::atoi(e) : 0;
+    P.overlap = (!P.split_phases && !P.bem) ? (e ? std::atoi(e) : (P.nr_on && !P.profile ? 3 : 0)) : 0;
+    if (P.overlap == 3 && !P.nr_on) P.overlap = 0;  // mode 3 splits k_near
+    if (const char* f = std::getenv("KIFMM_NEAR_SPLIT")) P.nr_split = std::atof(f);
+    if (const char* f = std::getenv("KIFMM_NEAR_SPARE")) P.nr_spare = std::atoi(f);
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if (P.overlap &&

@@ -193,7 +193,9 @@ struct Plan {
   int4* d_nr_items = nullptr;
   int4* d_nr_chunks = nullptr;
   int* d_nr_src = nullptr;
-  int* d_nr_counters = nullptr;            // one work counter per k_near launch
+  int* d_nr_counters = nullptr;            // work counters per k_near launch (2 per group)
+  int nr_spare = 0;                        // overlap mode 3: CTA slots per SM left to the kernels beside k_near
+  double nr_split = 0.4;                   // overlap mode 3: share of each group's units run beside S2M / M2M
   int64_t nr_src_bytes = 0;
   std::vector<int3> nr_groups;             // (pass shape, first item, count) per k_near launch
   int* d_near_off = nullptr; int4* d_near_seg = nullptr; int n_near_seg = 0;
@@ -300,7 +302,7 @@ int near_shape_count(int tab);           // k_near pass shapes of table tab, by 
 int near_shape_cap(int tab, int shape);  // TB x MQ targets per pass
 extern int g_num_sms;
 extern int g_launches;
-int near_launch(const Plan& P, double* out, cudaStream_t st);
+int near_launch(const Plan& P, double* out, cudaStream_t st, int part = 0, int spare = 0);
 int build_schedules(Plan& P, cudaStream_t st);
 int upload_tables(Plan& P);
 int kernels_init();

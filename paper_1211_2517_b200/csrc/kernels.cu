@@ -1953,6 +1953,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (launch_near(P, ea, P.stream_near)) return -3;
         KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
       }
+      if (P.overlap == 3) {  // k_near part 1 beside the HBM-bound S2M / M2M (one CTA slot per SM left free)
+        KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
+        KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, P.stream_near));
+        if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
+      }
       KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       mark(1);
@@ -2008,6 +2014,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (launch_near(P, ea, P.stream_near)) return -3;
         KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
         KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_m2l, 0));
+      }
+      if (P.overlap == 3) {  // k_near part 2 after the M2L, beside X / L2L / L2T / the far pass
+        KIFMM_CUDA(cudaEventRecord(P.ev_m2l, st));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_m2l, 0));
+        if (near_launch(P, P.d_pot_near, P.stream_near, 2, P.nr_spare)) return -3;
+        KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
       }
       mark(5);
       // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)

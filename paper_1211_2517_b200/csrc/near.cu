@@ -289,14 +289,15 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
   }
 }
 
+// spare > 0: leave that many CTA slots per SM to kernels running beside it (overlap mode 3)
 template <int TB, int MQ>
-int near_launch_one(const NearArgs& a, int count, cudaStream_t st) {
+int near_launch_one(const NearArgs& a, int count, int spare, cudaStream_t st) {
   static int per_sm = -1;
   if (per_sm < 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near<TB, MQ>, NR_NT, 0) != cudaSuccess) per_sm = 1;
     per_sm = std::max(1, per_sm);
   }
-  const int grid = std::min(count, per_sm * g_num_sms);
+  const int grid = std::min(count, std::max(1, per_sm - spare) * g_num_sms);
   k_near<TB, MQ><<<grid, NR_NT, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
@@ -335,24 +336,30 @@ int near_shape_cap(int tab, int shape) {
   return t[shape].tb * t[shape].mq;
 }
 
-int near_launch(const Plan& P, double* out, cudaStream_t st) {
+int near_launch(const Plan& P, double* out, cudaStream_t st, int part, int spare) {
   int cnt = 0;
   const NearShapeDef* tab = near_table(P.nr_table, &cnt);
-  if (!P.nr_groups.empty())
-    KIFMM_CUDA(cudaMemsetAsync(P.d_nr_counters, 0, sizeof(int) * P.nr_groups.size(), st));
-  for (size_t gidx = 0; gidx < P.nr_groups.size(); ++gidx) {
+  const int ng = (int)P.nr_groups.size();
+  if (ng == 0) return 0;
+  // part 0: every unit; 1 / 2: the first P.nr_split / the remaining units of each group
+  // (units are sorted longest first); counters: [0, ng) part 0 / 1, [ng, 2 ng) part 2
+  if (part != 2) KIFMM_CUDA(cudaMemsetAsync(P.d_nr_counters, 0, sizeof(int) * 2 * ng, st));
+  for (int gidx = 0; gidx < ng; ++gidx) {
     const int3& g = P.nr_groups[gidx];
+    const int na = part == 0 ? g.z : std::min(g.z, (int)(P.nr_split * g.z + 0.5));
+    const int first = part == 2 ? na : 0, count = part == 1 ? na : g.z - first;
+    if (count <= 0) continue;
     NearArgs a;
-    a.counter = P.d_nr_counters + gidx;
-    a.items = P.d_nr_items + g.y;
-    a.nitems = g.z;
+    a.counter = P.d_nr_counters + (part == 2 ? ng : 0) + gidx;
+    a.items = P.d_nr_items + g.y + first;
+    a.nitems = count;
     a.chunks = P.d_nr_chunks;
     a.src = P.d_nr_src;
     a.pts = P.tree.d_pts;
     a.out = out;
     int rc = -3;
     switch (tab[g.x].tb * 64 + tab[g.x].mq) {
-#define KIFMM_NS(TBv, MQv) case TBv * 64 + MQv: rc = near_launch_one<TBv, MQv>(a, g.z, st); break;
+#define KIFMM_NS(TBv, MQv) case TBv * 64 + MQv: rc = near_launch_one<TBv, MQv>(a, count, spare, st); break;
       KIFMM_NS(2, 4) KIFMM_NS(3, 4) KIFMM_NS(4, 4) KIFMM_NS(5, 4) KIFMM_NS(6, 4) KIFMM_NS(8, 4)
       KIFMM_NS(2, 8) KIFMM_NS(3, 8) KIFMM_NS(4, 8) KIFMM_NS(5, 8) KIFMM_NS(6, 8) KIFMM_NS(7, 8) KIFMM_NS(8, 8)
       KIFMM_NS(2, 16) KIFMM_NS(3, 16) KIFMM_NS(5, 16) KIFMM_NS(6, 16) KIFMM_NS(7, 16) KIFMM_NS(8, 16)

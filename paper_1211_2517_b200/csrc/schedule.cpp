@@ -340,7 +340,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
       P.nr_groups.push_back(make_int3(c, first, (int)nitems.size() - first));
     }
     P.nr_src_bytes = (int64_t)nsrc.size() * sizeof(int);
-    std::vector<int> counters(P.nr_groups.size(), 0);
+    std::vector<int> counters(2 * P.nr_groups.size(), 0);
     if (upload(P, &P.d_nr_items, nitems, st) || upload(P, &P.d_nr_chunks, nchunks, st) ||
         upload(P, &P.d_nr_src, nsrc, st) || upload(P, &P.d_nr_counters, counters, st))
       return -3;

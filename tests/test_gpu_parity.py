@@ -179,16 +179,20 @@ def test_edge_cases():
     assert rel(s2, 0.5 * s1) < 1e-14
 
 
-@pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k"])
-def test_overlapped_near_stream(case, monkeypatch):
-    # diagnostics option: near field on a second stream joined before the output
-    monkeypatch.setenv("KIFMM_OVERLAP", "1")
+@pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k", "torus50k"])
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
+def test_overlapped_near_stream(case, mode, monkeypatch):
+    # near field on a second stream joined before the output (mode 3: k_near split around
+    # the M2L, beside the S2M / L2T GEMVs); repeated matvecs reuse the streams and events
+    monkeypatch.setenv("KIFMM_OVERLAP", mode)
     pts, q, p, k, s = CASES[case]()
     tb = tables(p, k)
     ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q)
     for lo in (0, 1):
-        out = gpu_plan(pts, p, k, s, tb=tb, leaf_ops=lo).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-        assert rel(out, ref) <= TOL
+        gp = gpu_plan(pts, p, k, s, tb=tb, leaf_ops=lo)
+        for _ in range(2):
+            out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+            assert rel(out, ref) <= TOL
 
 
 STAGE2_CASES = ["C1", "sphere6k_s16", "octa_sphere32k", "torus50k"]
