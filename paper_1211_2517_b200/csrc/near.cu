@@ -10,7 +10,7 @@
 // per unordered pair instead of 2 x 12 one-sided.
 //
 // Work unit: a pass of up to TB x MQ targets of one leaf against its source list, in
-// chunks of <= NR_CH sources made of whole segments (host-built chunk table: no
+// chunks of <= near_ch(TB MQ) source slots (host-built point-index table: no
 // per-source search, no segment scan on the device).  Thread (ti, gi) holds targets
 // ti + MQ u (u < TB) and sweeps sources gi, gi + G, ... of each chunk (G = NT / MQ
 // slices).  MQ is a power of two, so a slice's MQ lanes are adjacent lanes of one
@@ -42,7 +42,6 @@ __device__ __forceinline__ void nr_commit() { asm volatile("cp.async.commit_grou
 __device__ __forceinline__ void nr_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 constexpr int NR_NT = 128;
-constexpr int NR_PER = NR_CH / NR_NT;  // sources staged per thread and chunk
 
 struct NearArgs {
   const int4* items;    // work units: (first target point, targets <= TB MQ, chunk begin, chunk end)
@@ -102,6 +101,8 @@ __device__ __forceinline__ void nr_mutual_batch(const double4* sbuf, const int* 
     }
     v[t] = sj;
   }
+  // (a layout keeping step t ^ (l % SB) in slot t avoids the selects below but makes the
+  // slice's lanes read different sources: measured slower)
 #pragma unroll
   for (int off = SB / 2; off >= 1; off >>= 1) {  // lane l keeps the partial of step l % SB
     const bool up = lane & off;
@@ -150,11 +151,11 @@ __global__ void __launch_bounds__(NR_NT, KIFMM_NEAR_MINB) k_near(NearArgs A) {
 #else
 __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
 #endif
-  constexpr int NT = NR_NT, G = NT / MQ, CAP = TB * MQ;
-  __shared__ __align__(16) double4 sbuf[2][NR_CH];
+  constexpr int NT = NR_NT, G = NT / MQ, CAP = TB * MQ, CH = near_ch(CAP), NR_PER = CH / NT;
+  static_assert(TB * NT * sizeof(double) <= CH * sizeof(double4), "slice sums alias a source buffer");
+  __shared__ __align__(16) double4 sbuf[2][CH];
   __shared__ __align__(16) double4 tbuf[2][CAP];
-  __shared__ int sidx[2][NR_CH];
-  __shared__ double red[TB * NT];
+  __shared__ int sidx[2][CH];
   __shared__ int s_ring[4];
   const int tid = threadIdx.x;
   const int ti = tid & (MQ - 1), gi = tid / MQ;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
   int b = 0, mm = 0;
   while (true) {
     nr_wait0();
-    __syncthreads();  // chunk cur in buffer b; buffer b ^ 1 and red[] free
+    __syncthreads();  // chunk cur in buffer b; buffer b ^ 1 free
     if (more) stage(nxt, ck_nxt, idx, b ^ 1);
     nr_commit();
     // records of the chunk after next, read while this chunk is evaluated
@@ -269,6 +270,10 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
       if (n > mh) nr_onesided<TB, false>(sbuf[b], first(mh), n, G, x, acc);
     }
     if (cur.chunk + 1 == cur.rec.w) {  // last chunk of the unit: sum the slices, RED into p
+      // (the slice sums go to the chunk buffer just evaluated: after this barrier nobody
+      // reads it, and the next staging into it follows the next top-of-loop barrier)
+      double* red = reinterpret_cast<double*>(&sbuf[b][0]);
+      __syncthreads();
 #pragma unroll
       for (int u = 0; u < TB; ++u) red[u * NT + tid] = acc[u];
       __syncthreads();

@@ -261,7 +261,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     ++n_l2t;
   }
   // k_near tables (mutual mode): per target leaf its source list — own points (checked),
-  // mutual segments, one-sided point segments — cut into chunks of NR_CH source slots;
+  // mutual segments, one-sided point segments — cut into chunks of near_ch(cap) source slots;
   // work units = (pass of <= TB x MQ targets, <= kUnitChunks chunks), grouped by pass
   // shape (see below), longest first
   P.nr_on = mutual;
@@ -296,6 +296,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
       const int b = titems[i].x;
       if (!mnear[i].empty()) ++P.n_tleaf_mut;
       for (auto& sg : mnear[i]) P.n_mut_pairs += (int64_t)npts(b) * sg.w;
+      const int CH = near_ch(near_shape_cap(nr_tab, shp[i]));
       const int cb = (int)nchunks.size();
       int n = 0, nchk = 0, ml = -1, mh = -1;
       auto flush = [&]() {
@@ -307,13 +308,13 @@ int build_schedules(Plan& P, cudaStream_t st) {
       };
       auto add = [&](int kind, int a, int len) {  // kind 0 one-sided, 1 own points, 3 mutual
         for (int off = 0; off < len;) {
-          const int take = std::min(len - off, NR_CH - n);
+          const int take = std::min(len - off, CH - n);
           if (kind == 1) nchk = n + take;
           if (kind == 3) { if (ml < 0) ml = n; mh = n + take; }
           for (int t = 0; t < take; ++t) nsrc.push_back(a + off + t);
           n += take;
           off += take;
-          if (n == NR_CH) flush();
+          if (n == CH) flush();
         }
       };
       add(1, T.pbeg[b], npts(b));
