@@ -153,7 +153,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
     size_t fr = 0, tot = 0;
     KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
     const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot);
-    if (4.0 * (double)slots > budget) mutual = false;
+    // (slot offsets are int32: past ~2e9 slots the one-sided k_eval path takes over)
+    if (4.0 * (double)slots > budget || slots > 2000000000LL) mutual = false;
   }
   static const double sym_r = [] { const char* e = std::getenv("KIFMM_SYM_R"); return e ? std::atof(e) : 1.4; }();
   auto pass_slots = [](int m) { int full = m / 96, rem = m - 96 * full; return 96 * full + 32 * ((rem + 31) / 32); };
