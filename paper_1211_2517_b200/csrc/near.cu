@@ -312,8 +312,8 @@ struct NearShapeDef {
 };
 // pass shapes by capacity TB x MQ: table 0 favours TB (fewer reductions per pair),
 // table 1 small TB (fewer registers, more resident warps)
-const NearShapeDef kNearTab0[] = {{2, 4}, {3, 4}, {4, 4}, {5, 4}, {6, 4}, {4, 8}, {5, 8}, {6, 8},
-                                  {7, 8}, {8, 8}, {5, 16}, {6, 16}, {7, 16}, {8, 16}, {5, 32}, {6, 32}};
+const NearShapeDef kNearTab0[] = {{2, 4}, {3, 4}, {4, 4}, {5, 4}, {6, 4}, {4, 8}, {5, 8}, {6, 8}, {7, 8},
+                                  {8, 8}, {5, 16}, {6, 16}, {7, 16}, {8, 16}, {5, 32}, {6, 32}, {7, 32}, {8, 32}};
 const NearShapeDef kNearTab1[] = {{2, 4}, {3, 4}, {2, 8}, {3, 8}, {2, 16}, {3, 16}, {2, 32}, {3, 32}, {4, 32},
                                   {5, 32}, {6, 32}};
 
@@ -368,7 +368,7 @@ int near_launch(const Plan& P, double* out, cudaStream_t st, int part, int spare
       KIFMM_NS(2, 4) KIFMM_NS(3, 4) KIFMM_NS(4, 4) KIFMM_NS(5, 4) KIFMM_NS(6, 4) KIFMM_NS(8, 4)
       KIFMM_NS(2, 8) KIFMM_NS(3, 8) KIFMM_NS(4, 8) KIFMM_NS(5, 8) KIFMM_NS(6, 8) KIFMM_NS(7, 8) KIFMM_NS(8, 8)
       KIFMM_NS(2, 16) KIFMM_NS(3, 16) KIFMM_NS(5, 16) KIFMM_NS(6, 16) KIFMM_NS(7, 16) KIFMM_NS(8, 16)
-      KIFMM_NS(2, 32) KIFMM_NS(3, 32) KIFMM_NS(4, 32) KIFMM_NS(5, 32) KIFMM_NS(6, 32)
+      KIFMM_NS(2, 32) KIFMM_NS(3, 32) KIFMM_NS(4, 32) KIFMM_NS(5, 32) KIFMM_NS(6, 32) KIFMM_NS(7, 32) KIFMM_NS(8, 32)
 #undef KIFMM_NS
       default: break;
     }

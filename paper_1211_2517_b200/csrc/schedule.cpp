@@ -275,8 +275,11 @@ int build_schedules(Plan& P, cudaStream_t st) {
     // pass shape per leaf: the least-padding shape, unless its group would have fewer than
     // kMinGroup leaves — then the next larger kept shape (more padding), or for the
     // largest leaves the largest kept smaller shape (more passes)
+    // (a leaf above the largest capacity runs in equal passes: ceil(m / cap_max) of them)
+    const int cap_max = near_shape_cap(nr_tab, kNearShapes - 1);
+    auto pass_size = [&](int m) { const int np = (m + cap_max - 1) / cap_max; return (m + np - 1) / np; };
     std::vector<int> shp(nt), cnt(kNearShapes, 0);
-    for (int i = 0; i < nt; ++i) ++cnt[shp[i] = nr_shape(npts(titems[i].x))];
+    for (int i = 0; i < nt; ++i) ++cnt[shp[i] = nr_shape(pass_size(npts(titems[i].x)))];
     {
       std::vector<int> kept;
       for (int c = 0; c < kNearShapes; ++c)
@@ -322,7 +325,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
       for (auto& sg : mnear[i]) add(3, sg.y, sg.w);
       for (size_t k = 1; k < near[i].size(); ++k) add(0, near[i][k].y, near[i][k].w);
       flush();
-      const int ce = (int)nchunks.size(), cap = near_shape_cap(nr_tab, shp[i]);
+      const int ce = (int)nchunks.size(), cap = std::min(near_shape_cap(nr_tab, shp[i]), pass_size(npts(b)));
       for (int t0 = 0; t0 < npts(b); t0 += cap)
         for (int c0 = cb; c0 < ce; c0 += kUnitChunks) {
           const int c1 = std::min(ce, c0 + kUnitChunks);
