@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) 
 // 2 n kernel values per point on the FP64 pipe.
 // k_leafop_build: out(j, a) = scale * sum_i Op[a * sa + i * si] * G(surface_i, x_j),
 //   MODE 0 (S2M): point-major rows  out[(pbeg + j - own_lo) * kp + a]
-//   MODE 1 (L2T): kp-major per leaf out[(pbeg - own_lo) * kp + a * m + j], scale r_B
+//   MODE 1 (L2T): point-major rows  out[(pbeg + j - own_lo) * kp + a], scale r_B
 // ----------------------------------------------------------------------------
 constexpr int LO_CH = 32;
 
@@ -1008,13 +1008,66 @@ __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ i
       const int j = c0 + jj;
       if (MODE == 0) out[(size_t)(p0 + j - own_lo) * kp + a] = acc;
       else if (MODE == 2) out[xmoff[blockIdx.x] + (size_t)j * kp + a] = acc;
-      else out[(size_t)(p0 - own_lo) * kp + (size_t)a * m + j] = acc;
+      else out[(size_t)(p0 + j - own_lo) * kp + a] = acc;  // L2T: point-major rows like S2M
     }
   }
 }
 
-// S2M with leaf operators: q^'_B[a] = sum_j q_j S_B[j][a]; one warp per leaf, rows of
-// kp doubles read coalesced; stored (a leaf's multipole is written only here)
+// Leaf-operator GEMVs (HBM-bound: each operator entry is read once per matvec).  Operators
+// are point-major rows of kp doubles.  A warp covers a row with R = kp / 4 lanes, each
+// loading 32 bytes (2 x 16-byte streaming loads), and RPW = 32 / R rows at a time (RPW = 1
+// when R is not a power of two); rows are unrolled 2-deep per lane for bytes in flight.
+struct RowMap {
+  int R, RPW, rsub, c4;
+  bool act;
+  __device__ RowMap(int kp, int lane) {
+    R = kp >> 2;
+    RPW = (R & (R - 1)) == 0 ? 32 / R : 1;
+    rsub = lane / R;
+    c4 = lane - rsub * R;
+    act = rsub < RPW;
+  }
+};
+__device__ __forceinline__ void ld_row4(const double* p, double (&v)[4]) {
+  const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+// acc[e] += sum over this lane's rows j < m of q_j M[j][4 c4 + e] (rows rsub, rsub + RPW, ...;
+// the loop is uniform over the warp: the shuffles need every lane)
+template <int U>
+__device__ __forceinline__ void gemv_rows_t(const double* __restrict__ M, const double4* __restrict__ pts, int p0,
+                                            int m, int kp, const RowMap& rm, int lane, double (&acc)[4]) {
+  for (int j0 = 0; j0 < m; j0 += 32) {  // densities 32 at a time, fetched by shuffle
+    const double qv = j0 + lane < m ? pts[p0 + j0 + lane].w : 0.0;
+    const int jn = min(32, m - j0);
+    for (int jb = 0; jb < jn; jb += U * rm.RPW) {  // U rows per lane in flight
+      double qu[U], v[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = jb + rm.rsub + u * rm.RPW;
+        qu[u] = __shfl_sync(0xffffffffu, qv, min(j, 31));
+        if (rm.act && j < jn) ld_row4(M + (size_t)(j0 + j) * kp + 4 * rm.c4, v[u]);
+        else v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = fma(qu[u], v[u][e], acc[e]);
+    }
+  }
+}
+// sum acc over the warp's RPW row groups: the totals land on the lanes with rsub = 0
+__device__ __forceinline__ void gemv_rows_reduce(const RowMap& rm, double (&acc)[4]) {
+  for (int o = rm.R; o < 32 && rm.RPW > 1; o <<= 1)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[e] += __shfl_down_sync(0xffffffffu, acc[e], o);
+}
+
+// S2M with leaf operators: q^'_B[a] = sum_j q_j S_B[j][a]; one warp per leaf; stored (a
+// leaf's multipole is written only here)
+template <int U>
 __global__ void __launch_bounds__(256) k_s2m_leafop(const int4* __restrict__ items, int nitems,
                                                     const double4* __restrict__ pts, const int* __restrict__ pbeg,
                                                     const int* __restrict__ pend, const double* __restrict__ S, int kp,
@@ -1023,73 +1076,50 @@ __global__ void __launch_bounds__(256) k_s2m_leafop(const int4* __restrict__ ite
   if (w >= nitems) return;
   const int b = items[w].x;
   const int p0 = pbeg[b], m = pend[b] - p0;
+  const RowMap rm(kp, lane);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const double* row = S + (size_t)(p0 - own_lo) * kp;
-  for (int j0 = 0; j0 < m; j0 += 32) {  // densities 32 at a time, broadcast by shuffle
-    const double qv = j0 + lane < m ? pts[p0 + j0 + lane].w : 0.0;
-    const int jn = min(32, m - j0);
-#pragma unroll 4
-    for (int jj = 0; jj < jn; ++jj) {
-      const double q = __shfl_sync(0xffffffffu, qv, jj);
-      const double* rj = row + (size_t)(j0 + jj) * kp;
+  gemv_rows_t<U>(S + (size_t)(p0 - own_lo) * kp, pts, p0, m, kp, rm, lane, acc);
+  gemv_rows_reduce(rm, acc);
+  if (rm.rsub == 0) {
+    double* o = qhat + (size_t)b * kp + 4 * rm.c4;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int a = lane + 32 * c;
-        if (a < kp) acc[c] = fma(q, __ldcs(rj + a), acc[c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int a = lane + 32 * c;
-    if (a < kp) qhat[(size_t)b * kp + a] = acc[c];
+    for (int e = 0; e < 4; ++e) o[e] = acc[e];
   }
 }
 
 // X list with its operators: l^_B[a] += sum over B's X rows, sum_j q_j X_row[j][a]; one warp
-// per target box (its rows are contiguous), rows of kp doubles read coalesced; M2L into l^
-// finished earlier on the stream and a target belongs to one warp: plain read-add-write
+// per target box (its rows are contiguous); M2L into l^ finished earlier on the stream and a
+// target belongs to one warp: plain read-add-write
+template <int U>
 __global__ void __launch_bounds__(256) k_x_gemv(const int4* __restrict__ xt, int nxt, const int4* __restrict__ xsegs,
                                                 const int64_t* __restrict__ xmoff, const double4* __restrict__ pts,
                                                 const double* __restrict__ X, int kp, double* __restrict__ lhat) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= nxt) return;
   const int4 t = xt[w];
+  const RowMap rm(kp, lane);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int r = t.y; r < t.z; ++r) {
     const int4 sg = xsegs[r];
-    const double* row = X + xmoff[r];
-    for (int j0 = 0; j0 < sg.w; j0 += 32) {  // densities 32 at a time, broadcast by shuffle
-      const double qv = j0 + lane < sg.w ? pts[sg.y + j0 + lane].w : 0.0;
-      const int jn = min(32, sg.w - j0);
-#pragma unroll 4
-      for (int jj = 0; jj < jn; ++jj) {
-        const double q = __shfl_sync(0xffffffffu, qv, jj);
-        const double* rj = row + (size_t)(j0 + jj) * kp;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int a = lane + 32 * c;
-          if (a < kp) acc[c] = fma(q, __ldcs(rj + a), acc[c]);
-        }
-      }
-    }
+    gemv_rows_t<U>(X + xmoff[r], pts, sg.y, sg.w, kp, rm, lane, acc);
   }
+  gemv_rows_reduce(rm, acc);
+  if (rm.rsub == 0) {
+    double* o = lhat + (size_t)t.x * kp + 4 * rm.c4;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int a = lane + 32 * c;
-    if (a < kp) lhat[(size_t)t.x * kp + a] += acc[c];
+    for (int e = 0; e < 4; ++e) o[e] += acc[e];
   }
 }
 
-// L2T with leaf operators: pot[p0 + j] = sum_a T_B[a][j] l^_B[a] for every owned target
-// leaf (leaves above level 2 have no far field: 0); one warp per leaf
+// L2T with leaf operators: pot[p0 + j] = sum_a T_B[j][a] l^_B[a] for every owned target
+// leaf (leaves above level 2 have no far field: 0); one warp per leaf, the lane's four
+// l^ entries in registers, each row's dot product reduced over its R lanes
 constexpr int L2T_WARPS = 8;
 __global__ void __launch_bounds__(L2T_WARPS * 32) k_l2t_leafop(const int4* __restrict__ items, int nitems,
                                                              const int* __restrict__ level, const int* __restrict__ pbeg,
                                                              const int* __restrict__ pend, const double* __restrict__ Tm,
                                                              const double* __restrict__ lhat, int kp, int own_lo,
                                                              double* __restrict__ pot) {
-  __shared__ double lh[L2T_WARPS][128];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w = blockIdx.x * L2T_WARPS + wl;
   if (w >= nitems) return;
@@ -1099,19 +1129,36 @@ __global__ void __launch_bounds__(L2T_WARPS * 32) k_l2t_leafop(const int4* __res
     for (int j = lane; j < m; j += 32) pot[p0 + j] = 0.0;
     return;
   }
-  for (int a = lane; a < kp; a += 32) lh[wl][a] = lhat[(size_t)b * kp + a];
-  __syncwarp();
-  const double* base = Tm + (size_t)(p0 - own_lo) * kp;
-  for (int j = lane; j < m; j += 32) {
-    double acc0 = 0.0, acc1 = 0.0;
-    int a = 0;
-#pragma unroll 4
-    for (; a + 1 < kp; a += 2) {
-      acc0 = fma(__ldcs(base + (size_t)a * m + j), lh[wl][a], acc0);
-      acc1 = fma(__ldcs(base + (size_t)(a + 1) * m + j), lh[wl][a + 1], acc1);
+  const RowMap rm(kp, lane);
+  double lh[4] = {0.0, 0.0, 0.0, 0.0};
+  if (rm.act) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) lh[e] = lhat[(size_t)b * kp + 4 * rm.c4 + e];
+  }
+  const double* base = Tm + (size_t)(p0 - own_lo) * kp + 4 * rm.c4;
+  const int wid = rm.RPW > 1 ? rm.R : 32;  // reduction span: the row's lanes
+  for (int j0 = 0; j0 < m; j0 += 4 * rm.RPW) {  // 4 rows per lane in flight
+    double d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + rm.rsub + u * rm.RPW;
+      double v[4];
+      d[u] = 0.0;
+      if (rm.act && j < m) {
+        ld_row4(base + (size_t)j * kp, v);
+        d[u] = fma(v[3], lh[3], fma(v[2], lh[2], fma(v[1], lh[1], v[0] * lh[0])));
+      }
     }
-    if (a < kp) acc0 = fma(__ldcs(base + (size_t)a * m + j), lh[wl][a], acc0);
-    pot[p0 + j] = acc0 + acc1;
+    for (int o = wid >> 1; o >= 1; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+    if (rm.act && rm.c4 == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + rm.rsub + u * rm.RPW;
+        if (j < m) pot[p0 + j] = d[u];
+      }
+    }
   }
 }
 
@@ -1965,8 +2012,14 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       if (P.leaf_s2m) {  // S2M as one GEMV per leaf with its precomputed operator
         if (P.n_s2m > 0) {
           ++g_launches;
-          k_s2m_leafop<<<(P.n_s2m + 7) / 8, 256, 0, st>>>(P.d_s2m_items, P.n_s2m, T.d_pts, T.d_pbeg, T.d_pend,
-                                                          P.d_s2m_mat, kp, Dp.own_lo, P.d_qhat);
+          // 4 rows per lane in flight when a row is a power-of-two number of 32-byte lane
+          // loads (kp <= 64, several rows per warp), else 2 (registers: occupancy)
+          if (kp <= 64 && ((kp / 4) & (kp / 4 - 1)) == 0)
+            k_s2m_leafop<4><<<(P.n_s2m + 7) / 8, 256, 0, st>>>(P.d_s2m_items, P.n_s2m, T.d_pts, T.d_pbeg, T.d_pend,
+                                                               P.d_s2m_mat, kp, Dp.own_lo, P.d_qhat);
+          else
+            k_s2m_leafop<2><<<(P.n_s2m + 7) / 8, 256, 0, st>>>(P.d_s2m_items, P.n_s2m, T.d_pts, T.d_pbeg, T.d_pend,
+                                                               P.d_s2m_mat, kp, Dp.own_lo, P.d_qhat);
           KIFMM_CUDA(cudaGetLastError());
         }
       } else if (P.n_s2m > 0) {  // S2M stage 1: check potentials of leaves at level >= 2
@@ -2025,7 +2078,11 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
       if (P.leaf_x && P.n_xt > 0) {
         ++g_launches;
-        k_x_gemv<<<(P.n_xt + 7) / 8, 256, 0, st>>>(P.d_xt_items, P.n_xt, P.d_x_seg, P.d_x_moff, T.d_pts, P.d_x_mat, kp,
+        if (kp <= 64 && ((kp / 4) & (kp / 4 - 1)) == 0)
+          k_x_gemv<4><<<(P.n_xt + 7) / 8, 256, 0, st>>>(P.d_xt_items, P.n_xt, P.d_x_seg, P.d_x_moff, T.d_pts, P.d_x_mat,
+                                                        kp, P.d_lhat);
+        else
+          k_x_gemv<2><<<(P.n_xt + 7) / 8, 256, 0, st>>>(P.d_xt_items, P.n_xt, P.d_x_seg, P.d_x_moff, T.d_pts, P.d_x_mat, kp,
                                                    P.d_lhat);
         KIFMM_CUDA(cudaGetLastError());
       } else if (P.n_xnd > 0) {
