@@ -48,64 +48,85 @@ __global__ void k_enclosure(const int* __restrict__ leaves, int nleaves, const d
 }
 
 // one CTA per near block (target leaf t, source range [a, a + len)): column-major entries
-// A[off + j * m + i] = int_{T_{a+j}} G(x_{tb+i}, y) dy, analytic when tb + i == a + j
+// A[off + j * mp + i] = int_{T_{a+j}} G(x_{tb+i}, y) dy, analytic when tb + i == a + j;
+// columns padded to mp = 4 ceil(m / 4) rows (zeros) so that the SpMV reads 32-byte quads
 __global__ void __launch_bounds__(128) k_bem_near_build(const int4* __restrict__ blocks, const int64_t* __restrict__ off,
                                                         int nblocks, const double4* __restrict__ pts,
                                                         const double4* __restrict__ tri, double* __restrict__ A) {
   const int bi = blockIdx.x;
   if (bi >= nblocks) return;
   const int4 bk = blocks[bi];  // (tb, m, a, len)
+  const int mp = (bk.y + 3) & ~3;
   const int64_t o = off[bi];
-  const int64_t cnt = (int64_t)bk.y * bk.w;
+  const int64_t cnt = (int64_t)mp * bk.w;
   for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
-    const int j = (int)(e / bk.y), i = (int)(e - (int64_t)j * bk.y);
-    const double4 p = pts[bk.x + i];
-    const double x[3] = {p.x, p.y, p.z};
-    A[o + e] = bem_integral(load_tri(tri + 3 * (int64_t)(bk.z + j)), x, bk.x + i == bk.z + j);
+    const int j = (int)(e / mp), i = (int)(e - (int64_t)j * mp);
+    double v = 0.0;
+    if (i < bk.y) {
+      const double4 p = pts[bk.x + i];
+      const double x[3] = {p.x, p.y, p.z};
+      v = bem_integral(load_tri(tri + 3 * (int64_t)(bk.z + j)), x, bk.x + i == bk.z + j);
+    }
+    A[o + e] = v;
   }
 }
 
 // near field: pot[tb + i] = sum over the leaf's blocks of A[:, i] . q[a : a + len]; one CTA
-// per target leaf; thread (ti, gi) owns target t0 + ti and the source slice j = gi (mod G),
-// so a warp reads contiguous runs of a column-major block; slices summed in shared memory
+// per target leaf; thread (c4, gi) owns targets 4 c4 .. 4 c4 + 3 and the source slice j = gi
+// (mod G): each load is one 32-byte quad of a column (2 x 16-byte streaming loads), two
+// sources in flight per thread; slices summed in shared memory (HBM-bound: every matrix
+// entry is read once per matvec)
 constexpr int BN_NT = 128;
 __global__ void __launch_bounds__(BN_NT) k_bem_near(const int4* __restrict__ items, const int* __restrict__ pbeg,
                                                     const int* __restrict__ pend, const int* __restrict__ seg_off,
                                                     const int4* __restrict__ segs, const int64_t* __restrict__ moff,
                                                     const double4* __restrict__ pts, const double* __restrict__ A,
                                                     double* __restrict__ pot) {
-  __shared__ double red[BN_NT];
+  __shared__ double red[4 * BN_NT];
   const int item = blockIdx.x;
   const int b = items[item].x;
-  const int tb = pbeg[b], m = pend[b] - tb;
+  const int tb = pbeg[b], m = pend[b] - tb, mp = (m + 3) & ~3;
   const int s0 = seg_off[item], s1 = seg_off[item + 1];
-  for (int t0 = 0; t0 < m; t0 += BN_NT) {
-    const int mm = min(BN_NT, m - t0);
-    const int G = BN_NT / mm;
-    const int ti = threadIdx.x % mm, gi = threadIdx.x / mm;
-    double acc = 0.0;
+  for (int t0 = 0; t0 < mp; t0 += 4 * BN_NT) {
+    const int nq = min(BN_NT, (mp - t0) >> 2);  // target quads in this pass
+    const int G = BN_NT / nq;
+    const int c4 = threadIdx.x % nq, gi = threadIdx.x / nq;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (gi < G) {
       for (int s = s0; s < s1; ++s) {
         const int4 sg = segs[s];
-        const double* col = A + moff[s] + t0 + ti;
-        double acc2 = 0.0;
+        const double* col = A + moff[s] + t0 + 4 * c4;
         int j = gi;
-#pragma unroll 4
-        for (; j + G < sg.w; j += 2 * G) {  // two independent chains
-          acc = fma(__ldcs(col + (int64_t)j * m), pts[sg.y + j].w, acc);
-          acc2 = fma(__ldcs(col + (int64_t)(j + G) * m), pts[sg.y + j + G].w, acc2);
+        for (; j + G < sg.w; j += 2 * G) {
+          const double qa = pts[sg.y + j].w, qb = pts[sg.y + j + G].w;
+          const double2* pa = reinterpret_cast<const double2*>(col + (int64_t)j * mp);
+          const double2* pb = reinterpret_cast<const double2*>(col + (int64_t)(j + G) * mp);
+          const double2 a0 = __ldcs(pa), a1 = __ldcs(pa + 1), b0 = __ldcs(pb), b1 = __ldcs(pb + 1);
+          acc[0] = fma(b0.x, qb, fma(a0.x, qa, acc[0]));
+          acc[1] = fma(b0.y, qb, fma(a0.y, qa, acc[1]));
+          acc[2] = fma(b1.x, qb, fma(a1.x, qa, acc[2]));
+          acc[3] = fma(b1.y, qb, fma(a1.y, qa, acc[3]));
         }
-        if (j < sg.w) acc = fma(__ldcs(col + (int64_t)j * m), pts[sg.y + j].w, acc);
-        acc += acc2;
+        if (j < sg.w) {
+          const double qa = pts[sg.y + j].w;
+          const double2* pa = reinterpret_cast<const double2*>(col + (int64_t)j * mp);
+          const double2 a0 = __ldcs(pa), a1 = __ldcs(pa + 1);
+          acc[0] = fma(a0.x, qa, acc[0]);
+          acc[1] = fma(a0.y, qa, acc[1]);
+          acc[2] = fma(a1.x, qa, acc[2]);
+          acc[3] = fma(a1.y, qa, acc[3]);
+        }
       }
     }
     __syncthreads();
-    red[threadIdx.x] = gi < G ? acc : 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) red[e * BN_NT + threadIdx.x] = gi < G ? acc[e] : 0.0;
     __syncthreads();
-    if (threadIdx.x < mm) {
+    for (int i = threadIdx.x; i < 4 * nq; i += BN_NT) {  // target t0 + i = quad i / 4, entry i % 4
+      const int q4 = i >> 2, e = i & 3;
       double sum = 0.0;
-      for (int g = 0; g < G; ++g) sum += red[g * mm + threadIdx.x];
-      pot[tb + t0 + threadIdx.x] = sum;
+      for (int g = 0; g < G; ++g) sum += red[e * BN_NT + g * nq + q4];
+      if (t0 + i < m) pot[tb + t0 + i] = sum;
     }
   }
 }
@@ -158,8 +179,8 @@ int bem_check_enclosure(Plan& P, cudaStream_t st) {
 // blocks: (target box first point, m, source first point, len) per near segment, aligned
 // with the near segment CSR; offsets into the matrix (int64)
 int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
-  std::vector<int64_t> off(blocks.size() + 1, 0);
-  for (size_t i = 0; i < blocks.size(); ++i) off[i + 1] = off[i] + (int64_t)blocks[i].y * blocks[i].w;
+  std::vector<int64_t> off(blocks.size() + 1, 0);  // columns of mp = 4 ceil(m / 4) rows: 32-byte aligned
+  for (size_t i = 0; i < blocks.size(); ++i) off[i + 1] = off[i] + (int64_t)((blocks[i].y + 3) & ~3) * blocks[i].w;
   const int64_t entries = off.back();
   size_t fr = 0, tot = 0;
   KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
