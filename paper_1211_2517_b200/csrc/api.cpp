@@ -247,7 +247,7 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     }
   }
   // Near field on a second stream (overlap modes; KIFMM_OVERLAP overrides):
-  //  3 (default with the mutual near field): k_near in two halves on the near stream —
+  //  3 (default with the mutual near field, up to 8M owned points): k_near in two halves on the near stream —
   //    units [0, nr_split) from the fork after the densities, the rest after the M2L —
   //    beside the S2M / M2M / X / L2T GEMVs and the far pass; results joined before the
   //    output (C2 -2.5%, C3 -10%, C4 / C5 +-0.2%).  Off in profiled plans: per-phase
@@ -256,7 +256,11 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
   //    beside a high-priority M2L stream.
   {
     const char* e = std::getenv("KIFMM_OVERLAP");
-    P.overlap = (!P.split_phases && !P.bem) ? (e ? std::atoi(e) : (P.nr_on && !P.profile ? 3 : 0)) : 0;
+    // (default only up to 8M owned points: C2 / C3 gain 2-10%, C4 / C5 lose 1-2% — their long
+    // k_near and M2L launches have little tail to fill, and the split costs k_near balance)
+    const int64_t owned = P.dist.own_hi - P.dist.own_lo;
+    const bool ovl_default = P.nr_on && !P.profile && owned <= (int64_t)8 << 20;
+    P.overlap = (!P.split_phases && !P.bem) ? (e ? std::atoi(e) : (ovl_default ? 3 : 0)) : 0;
     if (P.overlap == 3 && !P.nr_on) P.overlap = 0;  // mode 3 splits k_near
     if (const char* f = std::getenv("KIFMM_NEAR_SPLIT")) P.nr_split = std::atof(f);
     if (const char* f = std::getenv("KIFMM_NEAR_SPARE")) P.nr_spare = std::atoi(f);
