@@ -850,6 +850,9 @@ __global__ void __launch_bounds__(NT) k_eval(EvalArgs A, int chk_self) {
 // at a time in shared memory and every lane accumulates CHK_TB check points.
 // ----------------------------------------------------------------------------
 constexpr int CHK_WARPS = 8;
+#ifndef KIFMM_CHK_MINB
+#define KIFMM_CHK_MINB 3  // 80 registers: 3 CTAs per SM (the default heuristic took 92: 2 CTAs)
+#endif
 
 // BEM X-list check potentials (P:445-456 restated for S2L): one warp per item, each lane
 // CHK_TB check points, the source elements' integrals by bem_integral
@@ -875,7 +878,7 @@ __global__ void __launch_bounds__(CHK_WARPS * 32) k_chk_bem(EvalArgs A, int nite
 }
 
 template <int CHK_TB, bool DL = false>
-__global__ void __launch_bounds__(CHK_WARPS * 32) k_chk(EvalArgs A, int nitems) {
+__global__ void __launch_bounds__(CHK_WARPS * 32, KIFMM_CHK_MINB) k_chk(EvalArgs A, int nitems) {
   __shared__ double4 ssrc[CHK_WARPS][32];
   __shared__ double2 ssrcw[CHK_WARPS][DL ? 32 : 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
