@@ -214,9 +214,10 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     set_error("fmm_setup: normals (double layer) and triangles (BEM) are exclusive");
     return fail(FMM_EINVAL);
   }
-  if (opt->normals) {  // double-layer sources: no symmetric near-field pairs (dG/dn is not symmetric)
+  if (opt->normals) {  // double-layer sources: mutual pairs use the sign rule of k_near's
+    // double-layer path; the warp-pair kernel (mode 2) is single-layer only
     if (kifmm::sort_normals(P, opt->normals, st)) return fail(FMM_ECUDA);
-    P.sym_opt = 0;
+    if (P.sym_opt == 2) P.sym_opt = 0;
   }
   if (opt->triangles) {  // BEM elements: collocation at the points (= centroids), element integrals
     if (opt->nranks > 1) {

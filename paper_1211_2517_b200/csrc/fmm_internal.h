@@ -298,7 +298,7 @@ const char* last_error();
 int build_tree_device(Plan& P, const double* d_points_caller, cudaStream_t st);
 int build_lists_device(Plan& P, cudaStream_t st);
 // k_near sources per chunk for a pass shape of cap = TB x MQ targets (static shared memory <= 48 KB)
-__host__ __device__ constexpr int near_ch(int cap) { return cap <= 128 ? 512 : 256; }
+__host__ __device__ constexpr int near_ch(int cap, bool dl = false) { return dl ? 128 : cap <= 128 ? 512 : 256; }
 int near_shape_count(int tab);           // k_near pass shapes of table tab, by capacity
 int near_shape_cap(int tab, int shape);  // TB x MQ targets per pass
 extern int g_num_sms;

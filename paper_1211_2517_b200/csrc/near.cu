@@ -50,6 +50,7 @@ struct NearArgs {
   const int* src;       // per chunk: the point index of each source slot
   const double4* pts;   // sorted (x, y, z, q)
   double* out;          // potentials (sorted order), added to with RED
+  const double4* nrm;   // double layer: sorted source normals (else null)
   int* counter;         // items handed out beyond the first gridDim.x (zeroed per launch)
 };
 
@@ -137,6 +138,93 @@ __device__ __forceinline__ void nr_mutual(const double4* sbuf, const int* sidx, 
   if (s0 < nsteps) nr_mutual_batch<TB, MQ, 1, true>(sbuf, sidx, j0, j1, G, s0, x, q, acc, out);
 }
 
+// Double layer: the source term is q_j (x - y_j).n_j / r^3 (1/(4 pi) once per
+// sum).  Sources are staged as (y, q) and (n, 0); w_j = q_j n_j is formed per step.  For a
+// mutual pair with d = x_i - x_j and r3 = 1 / |d|^3: p_i += (d . w_j) r3 and
+// p_j += (x_j - x_i) . w_i r3 = -(d . w_i) r3 — ~21 FP64 instructions for both sides
+// against 2 x 18 one-sided.
+template <int TB, bool CHECK>
+__device__ __forceinline__ void nr_onesided_dl(const double4* sbuf, const double4* nbuf, int j0, int j1, int G,
+                                               const double (&x)[TB][3], double (&acc)[TB]) {
+#pragma unroll 2
+  for (int j = j0; j < j1; j += G) {
+    const double4 sv = sbuf[j], sn = nbuf[j];
+    const double wx = sv.w * sn.x, wy = sv.w * sn.y, wz = sv.w * sn.z;
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double ri = CHECK ? rinv_or_zero(r2) : rinv_nonzero(r2);
+      const double dw = fma(dz, wz, fma(dy, wy, dx * wx));
+      acc[u] = fma(dw * ri, ri * ri, acc[u]);
+    }
+  }
+}
+
+template <int TB, int MQ, int SB, bool LAST>
+__device__ __forceinline__ void nr_mutual_batch_dl(const double4* sbuf, const double4* nbuf, const int* sidx, int j0,
+                                                   int j1, int G, int s0, const double (&x)[TB][3],
+                                                   const double (&wt)[TB][3], double (&acc)[TB],
+                                                   double* __restrict__ out) {
+  static_assert(SB <= MQ && (!LAST || SB == 1), "batch shape");
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double v[SB];
+  bool valid = true;
+#pragma unroll
+  for (int t = 0; t < SB; ++t) {
+    int j = j0 + G * (s0 + t);
+    if (LAST) {
+      valid = j < j1;
+      j = valid ? j : j1 - 1;
+    }
+    const double4 sv = sbuf[j], sn = nbuf[j];
+    const double qs = LAST && !valid ? 0.0 : sv.w;
+    const double wx = qs * sn.x, wy = qs * sn.y, wz = qs * sn.z;
+    double sj = 0.0;
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+      const double ri = rinv_nonzero(fma(dz, dz, fma(dy, dy, dx * dx)));  // distinct leaves: r > 0
+      const double r3 = ri * (ri * ri);
+      acc[u] = fma(fma(dz, wz, fma(dy, wy, dx * wx)), r3, acc[u]);
+      sj = fma(fma(dz, wt[u][2], fma(dy, wt[u][1], dx * wt[u][0])), r3, sj);
+    }
+    v[t] = sj;
+  }
+#pragma unroll
+  for (int off = SB / 2; off >= 1; off >>= 1) {  // lane l keeps the partial of step l % SB
+    const bool up = lane & off;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double send = up ? v[i] : v[i + off];
+      const double keep = up ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(FULL, send, off);
+    }
+  }
+#pragma unroll
+  for (int off = SB; off < MQ; off <<= 1) v[0] += __shfl_xor_sync(FULL, v[0], off);
+  if ((lane & (MQ - 1)) < SB && valid) atomicAdd(out + sidx[j0 + G * (s0 + (lane & (SB - 1)))], -v[0] * kInv4Pi);
+}
+
+template <int TB, int MQ>
+__device__ __forceinline__ void nr_mutual_dl(const double4* sbuf, const double4* nbuf, const int* sidx, int lo, int j0,
+                                             int j1, int G, const double (&x)[TB][3], const double (&wt)[TB][3],
+                                             double (&acc)[TB], double* __restrict__ out) {
+  constexpr int SB = MQ < 4 ? MQ : 4;
+  const int nmin = (j1 - lo) / G, nsteps = (j1 - lo + G - 1) / G;  // uniform over the CTA
+  int s0 = 0;
+  for (; s0 + SB <= nmin; s0 += SB)
+    nr_mutual_batch_dl<TB, MQ, SB, false>(sbuf, nbuf, sidx, j0, j1, G, s0, x, wt, acc, out);
+  if (SB >= 4 && s0 + 2 <= nmin) {
+    nr_mutual_batch_dl<TB, MQ, (SB >= 2 ? 2 : 1), false>(sbuf, nbuf, sidx, j0, j1, G, s0, x, wt, acc, out);
+    s0 += SB >= 2 ? 2 : 1;
+  }
+  if (s0 < nmin) nr_mutual_batch_dl<TB, MQ, 1, false>(sbuf, nbuf, sidx, j0, j1, G, s0++, x, wt, acc, out);
+  if (s0 < nmin) nr_mutual_batch_dl<TB, MQ, 1, false>(sbuf, nbuf, sidx, j0, j1, G, s0++, x, wt, acc, out);
+  if (s0 < nsteps) nr_mutual_batch_dl<TB, MQ, 1, true>(sbuf, nbuf, sidx, j0, j1, G, s0, x, wt, acc, out);
+}
+
 // the CTA's work sequence: unit blockIdx.x, then units taken from a global counter
 // (dynamic: units differ in cost; the host orders them longest first), two ahead of use
 // through a 4-slot ring in shared memory; per unit its chunks
@@ -145,16 +233,15 @@ struct Cursor {
   int4 rec;  // this unit's record
 };
 
-template <int TB, int MQ>
-#ifdef KIFMM_NEAR_MINB
-__global__ void __launch_bounds__(NR_NT, KIFMM_NEAR_MINB) k_near(NearArgs A) {
-#else
+template <int TB, int MQ, bool DL = false>
 __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
-#endif
-  constexpr int NT = NR_NT, G = NT / MQ, CAP = TB * MQ, CH = near_ch(CAP), NR_PER = CH / NT;
-  static_assert(TB * NT * sizeof(double) <= CH * sizeof(double4), "slice sums alias a source buffer");
+  constexpr int NT = NR_NT, G = NT / MQ, CAP = TB * MQ, CH = near_ch(CAP, DL), NR_PER = CH / NT;
+  static_assert(DL || TB * NT * sizeof(double) <= CH * sizeof(double4), "slice sums alias a source buffer");
   __shared__ __align__(16) double4 sbuf[2][CH];
   __shared__ __align__(16) double4 tbuf[2][CAP];
+  __shared__ __align__(16) double4 nbuf[2][DL ? CH : 1];   // double layer: source normals
+  __shared__ __align__(16) double4 tnbuf[2][DL ? CAP : 1]; // double layer: target normals
+  __shared__ double red_dl[DL ? TB * NT : 1];
   __shared__ int sidx[2][CH];
   __shared__ int s_ring[4];
   const int tid = threadIdx.x;
@@ -184,6 +271,12 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
         double* dst = reinterpret_cast<double*>(&sbuf[b][f]);
         nr_cp16(dst, src);
         nr_cp16(dst + 2, src + 2);
+        if constexpr (DL) {
+          const double* nsrc = reinterpret_cast<const double*>(A.nrm + idx[r]);
+          double* ndst = reinterpret_cast<double*>(&nbuf[b][f]);
+          nr_cp16(ndst, nsrc);
+          nr_cp16(ndst + 2, nsrc + 2);
+        }
         sidx[b][f] = idx[r];
       }
     }
@@ -193,6 +286,12 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
         double* dst = reinterpret_cast<double*>(&tbuf[b][i]);
         nr_cp16(dst, src);
         nr_cp16(dst + 2, src + 2);
+        if constexpr (DL) {
+          const double* nsrc = reinterpret_cast<const double*>(A.nrm + c.rec.x + i);
+          double* ndst = reinterpret_cast<double*>(&tnbuf[b][i]);
+          nr_cp16(ndst, nsrc);
+          nr_cp16(ndst + 2, nsrc + 2);
+        }
       }
     }
   };
@@ -227,6 +326,7 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
   if (more) load_idx(ck_nxt, idx);
 
   double x[TB][3], q[TB], acc[TB];
+  double wt[DL ? TB : 1][3];  // double layer: the targets' q_i n_i
   int b = 0, mm = 0;
   while (true) {
     nr_wait0();
@@ -257,6 +357,12 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
         } else {  // padding target: far away, zero density (results discarded)
           x[u][0] = 1e100; x[u][1] = 0.0; x[u][2] = 0.0; q[u] = 0.0;
         }
+        if constexpr (DL) {
+          const double4 nv = i < mm ? tnbuf[b][i] : make_double4(0.0, 0.0, 0.0, 0.0);
+          wt[u][0] = q[u] * nv.x;
+          wt[u][1] = q[u] * nv.y;
+          wt[u][2] = q[u] * nv.z;
+        }
       }
     }
     {
@@ -264,15 +370,22 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
       auto first = [&](int lo) { return lo <= gi ? gi : gi + ((lo - gi + G - 1) / G) * G; };
       // [0, nchk) checked one-sided (the leaf's own points), [nchk, ml) one-sided,
       // [ml, mh) mutual, [mh, n) one-sided
-      if (nchk > 0) nr_onesided<TB, true>(sbuf[b], gi, nchk, G, x, acc);
-      if (ml > nchk) nr_onesided<TB, false>(sbuf[b], first(nchk), ml, G, x, acc);
-      if (mh > ml) nr_mutual<TB, MQ>(sbuf[b], sidx[b], ml, first(ml), mh, G, x, q, acc, A.out);
-      if (n > mh) nr_onesided<TB, false>(sbuf[b], first(mh), n, G, x, acc);
+      if constexpr (DL) {
+        if (nchk > 0) nr_onesided_dl<TB, true>(sbuf[b], nbuf[b], gi, nchk, G, x, acc);
+        if (ml > nchk) nr_onesided_dl<TB, false>(sbuf[b], nbuf[b], first(nchk), ml, G, x, acc);
+        if (mh > ml) nr_mutual_dl<TB, MQ>(sbuf[b], nbuf[b], sidx[b], ml, first(ml), mh, G, x, wt, acc, A.out);
+        if (n > mh) nr_onesided_dl<TB, false>(sbuf[b], nbuf[b], first(mh), n, G, x, acc);
+      } else {
+        if (nchk > 0) nr_onesided<TB, true>(sbuf[b], gi, nchk, G, x, acc);
+        if (ml > nchk) nr_onesided<TB, false>(sbuf[b], first(nchk), ml, G, x, acc);
+        if (mh > ml) nr_mutual<TB, MQ>(sbuf[b], sidx[b], ml, first(ml), mh, G, x, q, acc, A.out);
+        if (n > mh) nr_onesided<TB, false>(sbuf[b], first(mh), n, G, x, acc);
+      }
     }
     if (cur.chunk + 1 == cur.rec.w) {  // last chunk of the unit: sum the slices, RED into p
       // (the slice sums go to the chunk buffer just evaluated: after this barrier nobody
       // reads it, and the next staging into it follows the next top-of-loop barrier)
-      double* red = reinterpret_cast<double*>(&sbuf[b][0]);
+      double* red = DL ? red_dl : reinterpret_cast<double*>(&sbuf[b][0]);
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < TB; ++u) red[u * NT + tid] = acc[u];
@@ -295,16 +408,27 @@ __global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
 }
 
 // spare > 0: leave that many CTA slots per SM to kernels running beside it (overlap mode 3)
-template <int TB, int MQ>
+template <int TB, int MQ, bool DL>
 int near_launch_one(const NearArgs& a, int count, int spare, cudaStream_t st) {
   static int per_sm = -1;
   if (per_sm < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near<TB, MQ>, NR_NT, 0) != cudaSuccess) per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near<TB, MQ, DL>, NR_NT, 0) != cudaSuccess) per_sm = 1;
     per_sm = std::max(1, per_sm);
   }
   const int grid = std::min(count, std::max(1, per_sm - spare) * g_num_sms);
-  k_near<TB, MQ><<<grid, NR_NT, 0, st>>>(a);
+  k_near<TB, MQ, DL><<<grid, NR_NT, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// double-layer variants exist for passes of <= 160 targets (table 3)
+template <int TB, int MQ>
+int near_launch_sel(const NearArgs& a, int count, int spare, cudaStream_t st) {
+  if constexpr (TB * MQ <= 160) {
+    if (a.nrm) return near_launch_one<TB, MQ, true>(a, count, spare, st);
+  } else {
+    if (a.nrm) return -3;
+  }
+  return near_launch_one<TB, MQ, false>(a, count, spare, st);
 }
 
 struct NearShapeDef {
@@ -321,6 +445,10 @@ const NearShapeDef kNearTab2[] = {{2, 4}, {4, 4}, {6, 4}, {8, 4}, {5, 8}, {6, 8}
                                   {5, 16}, {6, 16}, {7, 16}, {8, 16}, {5, 32}, {6, 32}};
 
 const NearShapeDef* near_table(int tab, int* count) {
+  if (tab == 3) {  // double layer: table 0 up to 160 targets (static shared memory <= 48 KB)
+    *count = (int)(sizeof(kNearTab0) / sizeof(kNearTab0[0])) - 3;
+    return kNearTab0;
+  }
   if (tab == 1) { *count = (int)(sizeof(kNearTab1) / sizeof(kNearTab1[0])); return kNearTab1; }
   if (tab == 2) { *count = (int)(sizeof(kNearTab2) / sizeof(kNearTab2[0])); return kNearTab2; }
   *count = (int)(sizeof(kNearTab0) / sizeof(kNearTab0[0]));
@@ -361,10 +489,11 @@ int near_launch(const Plan& P, double* out, cudaStream_t st, int part, int spare
     a.chunks = P.d_nr_chunks;
     a.src = P.d_nr_src;
     a.pts = P.tree.d_pts;
+    a.nrm = P.d_nrm;
     a.out = out;
     int rc = -3;
     switch (tab[g.x].tb * 64 + tab[g.x].mq) {
-#define KIFMM_NS(TBv, MQv) case TBv * 64 + MQv: rc = near_launch_one<TBv, MQv>(a, count, spare, st); break;
+#define KIFMM_NS(TBv, MQv) case TBv * 64 + MQv: rc = near_launch_sel<TBv, MQv>(a, count, spare, st); break;
       KIFMM_NS(2, 4) KIFMM_NS(3, 4) KIFMM_NS(4, 4) KIFMM_NS(5, 4) KIFMM_NS(6, 4) KIFMM_NS(8, 4)
       KIFMM_NS(2, 8) KIFMM_NS(3, 8) KIFMM_NS(4, 8) KIFMM_NS(5, 8) KIFMM_NS(6, 8) KIFMM_NS(7, 8) KIFMM_NS(8, 8)
       KIFMM_NS(2, 16) KIFMM_NS(3, 16) KIFMM_NS(5, 16) KIFMM_NS(6, 16) KIFMM_NS(7, 16) KIFMM_NS(8, 16)

@@ -169,7 +169,9 @@ int build_schedules(Plan& P, cudaStream_t st) {
     return r1 <= r2 ? 1 : 2;
   };
   // k_near pass shape of an m-point leaf (the least padding; passes of the largest beyond it)
-  static const int nr_tab = [] { const char* e = std::getenv("KIFMM_NEAR_TAB"); return e ? std::atoi(e) : 0; }();
+  static const int nr_tab_env = [] { const char* e = std::getenv("KIFMM_NEAR_TAB"); return e ? std::atoi(e) : 0; }();
+  const bool dl = P.d_nrm != nullptr;
+  const int nr_tab = dl ? 3 : nr_tab_env;  // double layer: shapes up to 160 targets
   P.nr_table = nr_tab;
   const int kNearShapes = near_shape_count(nr_tab);
   auto nr_shape = [&](int m) {
@@ -300,7 +302,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
       const int b = titems[i].x;
       if (!mnear[i].empty()) ++P.n_tleaf_mut;
       for (auto& sg : mnear[i]) P.n_mut_pairs += (int64_t)npts(b) * sg.w;
-      const int CH = near_ch(near_shape_cap(nr_tab, shp[i]));
+      const int CH = near_ch(near_shape_cap(nr_tab, shp[i]), dl);
       const int cb = (int)nchunks.size();
       int n = 0, nchk = 0, ml = -1, mh = -1;
       auto flush = [&]() {

@@ -314,3 +314,22 @@ def test_near_field_modes(case, mode, monkeypatch):
         assert rel(out, ref) <= TOL, (mode, split)
         if split:
             assert rel(gp.export_phase("near"), ph["near"]) <= TOL
+
+
+@pytest.mark.parametrize("case", ["sphere6k_s16", "torus50k", "sphere20k_s400"])
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_double_layer_near_modes(case, mode, monkeypatch):
+    """Double-layer sources with mutual leaf pairs (k_near, sign rule p_j -= (d . w_i) r^-3)
+    and all one-sided (k_eval): the oracle's double-layer potential, fused and split."""
+    pts, q, p, k, s = {**CASES, **NEAR_CASES}[case]()
+    rng = np.random.default_rng(11)
+    nrm = rng.normal(size=pts.shape)
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    tb = tables(p, k)
+    ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q, normals=nrm)
+    monkeypatch.setenv("KIFMM_SYM", mode)
+    for split in (False, True):
+        gp = gpu_plan(pts, p, k, s, tb=tb, split_phases=split, normals=torch.from_numpy(nrm).cuda())
+        assert (gp.info["near_mutual_leaves"] > 0) == (mode == "1")
+        out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+        assert rel(out, ref) <= TOL, (mode, split)
