@@ -108,6 +108,10 @@ typedef struct {
                          fmm_info.bem_extrusion, setup fails (FMM_EINVAL) if an element reaches
                          its leaf's upward check surface.  The near-field matrix is built at setup
                          (FMM_ENOMEM if it does not fit).  Single GPU. */
+  const char* operator_file; /* host path or NULL (ignored when `tables` is set).  The operator
+                         tables' versioned binary file (tables_io.cpp): loaded if it exists —
+                         FMM_ECONFIG if it was built for another (p, k, d, pinv_rcond), is
+                         corrupt or of another version — else computed and written there. */
 } fmm_options;
 
 typedef struct {
@@ -248,6 +252,10 @@ int fmm_export_phase(const fmm_plan* plan, int which, double* out);
 int fmm_tables_build(int p, int k, double d, double rcond, fmm_tables** out);
 int fmm_tables_view_get(const fmm_tables* t, fmm_tables_view* view, const double** sigma);
 void fmm_tables_free(fmm_tables* t);
+/* The tables' versioned binary file (see fmm_options.operator_file): write (FMM_EINVAL if
+ * the path cannot be written) / read (FMM_ECONFIG: missing, corrupt or another version). */
+int fmm_tables_save(const fmm_tables* t, const char* path);
+int fmm_tables_load(const char* path, fmm_tables** out);
 
 const char* fmm_last_error(void);
 

@@ -35,7 +35,7 @@ class Options(ctypes.Structure):
                 ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("leaf_ops", ctypes.c_int), ("m2l_c2", ctypes.c_double), ("normals", ctypes.c_void_p),
-                ("triangles", ctypes.c_void_p)]
+                ("triangles", ctypes.c_void_p), ("operator_file", ctypes.c_char_p)]
 
 
 class Info(ctypes.Structure):
@@ -71,7 +71,7 @@ EXPORTS = ("fmm_default_options", "fmm_setup", "fmm_setup_ex", "fmm_matvec", "fm
            "fmm_info", "fmm_export_tree", "fmm_export_lists", "fmm_export_phase", "fmm_tables_build",
            "fmm_tables_view_get", "fmm_tables_free", "fmm_last_error", "fmm_matvec_owned", "fmm_matvec_owned_host",
            "fmm_owned_range", "fmm_nccl_unique_id", "fmm_matvec_group", "fmm_partition_host", "fmm_partition_get",
-           "fmm_partition_free", "fmm_plan_partition", "fmm_gmres")
+           "fmm_partition_free", "fmm_plan_partition", "fmm_gmres", "fmm_tables_save", "fmm_tables_load")
 
 _lib = None
 
@@ -100,6 +100,8 @@ def lib():
         L.fmm_tables_view_get.argtypes = [vp, ctypes.POINTER(TablesView), ctypes.POINTER(ctypes.POINTER(ctypes.c_double))]
         L.fmm_tables_free.argtypes = [vp]
         L.fmm_tables_free.restype = None
+        L.fmm_tables_save.argtypes = [vp, ctypes.c_char_p]
+        L.fmm_tables_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
         L.fmm_last_error.argtypes = []
         L.fmm_last_error.restype = ctypes.c_char_p
         L.fmm_matvec_owned.argtypes = [vp, vp, vp, vp]
@@ -132,10 +134,28 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def fmm_tables_build(p: int, k: int, d: float = 0.1, rcond: float = 1e-10) -> dict:
-    """Host precompute of the operator tables (no GPU needed)."""
+def fmm_tables_build(p: int, k: int, d: float = 0.1, rcond: float = 1e-10, save: str | None = None) -> dict:
+    """Host precompute of the operator tables (no GPU needed); save: also write the
+    versioned table file there (fmm_tables_save)."""
     h = ctypes.c_void_p()
     _check(lib().fmm_tables_build(p, k, d, rcond, ctypes.byref(h)), "fmm_tables_build")
+    if save is not None:
+        try:
+            _check(lib().fmm_tables_save(h, os.fsencode(save)), "fmm_tables_save")
+        except Exception:
+            lib().fmm_tables_free(h)
+            raise
+    return _tables_dict(h, rcond)
+
+
+def fmm_tables_load(path: str) -> dict:
+    """Read a versioned table file (fmm_tables_load): the same dict as fmm_tables_build."""
+    h = ctypes.c_void_p()
+    _check(lib().fmm_tables_load(os.fsencode(path), ctypes.byref(h)), "fmm_tables_load")
+    return _tables_dict(h, None)
+
+
+def _tables_dict(h, rcond) -> dict:
     try:
         v = TablesView()
         sig = ctypes.POINTER(ctypes.c_double)()
@@ -200,7 +220,7 @@ class Plan:
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
                  split_phases: bool = False, stream=None, nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, leaf_ops: int = -1, m2l_c2: float = 0.0, normals=None,
-                 triangles=None):
+                 triangles=None, operator_file: str | None = None):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -223,6 +243,10 @@ class Plan:
             self.triangles = triangles.contiguous().to(torch.float64)
             opt.triangles = ctypes.c_void_p(self.triangles.data_ptr())
         self._keep = []
+        if operator_file is not None:  # versioned table file: loaded, or computed and written
+            fname = ctypes.create_string_buffer(os.fsencode(operator_file))
+            self._keep.append(fname)
+            opt.operator_file = ctypes.cast(fname, ctypes.c_char_p)
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             self._keep.append(idbuf)

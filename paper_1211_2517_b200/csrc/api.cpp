@@ -30,6 +30,7 @@ struct fmm_plan {
 
 struct fmm_tables {
   kifmm::HostTables H;
+  int k_req = 0;  // the requested k (H.k is k_eff)
 };
 
 namespace kifmm {
@@ -91,6 +92,7 @@ void fmm_default_options(fmm_options* o) {
   o->m2l_c2 = 0.0;
   o->normals = nullptr;
   o->triangles = nullptr;
+  o->operator_file = nullptr;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -105,6 +107,27 @@ int fmm_tables_build(int p, int k, double d, double rcond, fmm_tables** out) {
   if (!t) { set_error("fmm_tables_build: out of host memory"); return FMM_ENOMEM; }
   int rc = kifmm::build_tables(p, k, d, rcond, &t->H);
   if (rc) { delete t; return rc; }
+  t->k_req = k;
+  *out = t;
+  return FMM_OK;
+}
+
+int fmm_tables_save(const fmm_tables* t, const char* path) {
+  if (!t || !path) { set_error("fmm_tables_save: null argument"); return FMM_EINVAL; }
+  return kifmm::save_tables(t->H, t->k_req, path) ? FMM_EINVAL : FMM_OK;
+}
+
+int fmm_tables_load(const char* path, fmm_tables** out) {
+  if (!path || !out) { set_error("fmm_tables_load: null argument"); return FMM_EINVAL; }
+  *out = nullptr;
+  fmm_tables* t = new (std::nothrow) fmm_tables();
+  if (!t) { set_error("fmm_tables_load: out of host memory"); return FMM_ENOMEM; }
+  const int rc = kifmm::load_tables(path, &t->H, &t->k_req);
+  if (rc) {
+    delete t;
+    if (rc == 1) set_error(std::string("fmm_tables_load: no such file ") + path);
+    return FMM_ECONFIG;
+  }
   *out = t;
   return FMM_OK;
 }
@@ -191,6 +214,21 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
             H.surf.push_back(-1.0 + 2.0 / (pp - 1) * j);
             H.surf.push_back(-1.0 + 2.0 / (pp - 1) * l);
           }
+  } else if (opt->operator_file) {  // the table file: load it, or compute and write it
+    int k_req = 0;
+    const int rc = kifmm::load_tables(opt->operator_file, &P.tables, &k_req);
+    if (rc < 0) return fail(FMM_ECONFIG);
+    if (rc == 0 && (P.tables.p != opt->p || k_req != opt->k || P.tables.n != n_expect ||
+                    std::fabs(P.tables.d - opt->d) > 1e-15 || P.tables.rcond != opt->pinv_rcond)) {
+      set_error(std::string("fmm_setup: operator file ") + opt->operator_file + " was built for (p, k, d, rcond) = (" +
+                std::to_string(P.tables.p) + ", " + std::to_string(k_req) + ", " + std::to_string(P.tables.d) + ", " +
+                std::to_string(P.tables.rcond) + ")");
+      return fail(FMM_ECONFIG);
+    }
+    if (rc == 1) {
+      if (int b = kifmm::build_tables(opt->p, opt->k, opt->d, opt->pinv_rcond, &P.tables)) return fail(b);
+      if (kifmm::save_tables(P.tables, opt->k, opt->operator_file)) return fail(FMM_EINVAL);
+    }
   } else {
     int rc = kifmm::build_tables(opt->p, opt->k, opt->d, opt->pinv_rcond, &P.tables);
     if (rc) return fail(rc);

@@ -29,6 +29,8 @@ struct HostTables {
 };
 
 int build_tables(int p, int k, double d, double rcond, HostTables* out);
+int save_tables(const HostTables& H, int k_req, const std::string& path);
+int load_tables(const std::string& path, HostTables* H, int* k_req);  // 1: no file
 int build_stage2(HostTables& H, double C2);
 
 // One launch of the grouped gather-GEMM-scatter kernel: Y[tgt] (+)= scale * Op * X[src].

@@ -5,6 +5,8 @@
 * accuracy vs the direct sum: GPU error <= oracle error + 1e-12
 * own host precompute: within the intrinsic table-sensitivity bound
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -333,3 +335,22 @@ def test_double_layer_near_modes(case, mode, monkeypatch):
         assert (gp.info["near_mutual_leaves"] > 0) == (mode == "1")
         out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
         assert rel(out, ref) <= TOL, (mode, split)
+
+
+def test_operator_file_cache(tmp_path):
+    """fmm_options.operator_file: the first plan computes and writes the table file, the
+    second loads it (the same tables: potentials equal up to the order of the atomic
+    adds, and equal to a plan on the file's tables passed in memory); another (p, k) is
+    refused with FMM_ECONFIG."""
+    pts, q, p, k, s = CASES["sphere6k_s16"]()
+    path = str(tmp_path / "p6k60.kifmm")
+    a = gpu_plan(pts, p, k, s, operator_file=path)
+    assert os.path.exists(path)
+    b = gpu_plan(pts, p, k, s, operator_file=path)
+    c = gpu_plan(pts, p, k, s, tb=K().fmm_tables_load(path))
+    Q = torch.from_numpy(q).cuda()
+    oa, ob, oc = (x.matvec(Q).cpu().numpy() for x in (a, b, c))
+    assert rel(oa, ob) <= 1e-14 and rel(oa, oc) <= 1e-14
+    with pytest.raises(RuntimeError) as e:
+        gpu_plan(pts, 4, 24, s, operator_file=path)
+    assert "(-2)" in str(e.value) and "operator file" in str(e.value)
