@@ -261,10 +261,12 @@ def run_ours(args):
     peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")))
     peak = float(peaks["dmma_m8n8k4_tflops"])
     achieved = m2l_flops / m2l_s / 1e12
-    traffic = None
+    traffic, pipe_pct = None, None
     tf = os.path.join(ROOT, "profiles", "m2l_dram_bytes.json")
     if os.path.exists(tf) and ws == 1:
-        traffic = json.load(open(tf)).get("bytes_per_launch")
+        mt = json.load(open(tf))
+        traffic = mt.get("bytes_per_launch")
+        pipe_pct = mt.get("tensor_pipe_active_pct")
     # ---- cpu baseline: the oracle on the host cores, one full matvec (rank 0, N = 1 only)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
@@ -286,6 +288,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "roofline": {"bound": "tensor", "kernel": "M2L: k_m2l_sib + k_ggs_sq (DMMA.8x8x4 FP64)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "tensor_pipe_active_pct_ncu": pipe_pct,
                      "peak_source": "measured: tools/microbench/fp64_peaks.cu DMMA m8n8k4 loop on this pool's B200 "
                                     "(profiles/fp64_peaks_r01.json)",
                      "flops_per_launch": m2l_flops, "ms_per_launch": phase["m2l"],
