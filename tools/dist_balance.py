@@ -1,7 +1,8 @@
 """Per-rank work of a Morton partition, measured on ONE GPU with a loopback group
 (diagnostics; the ranks run one after another, so the per-rank phase events measure each
-rank's own kernels).  Weak-scaling workload of bench.py: R tiled unit cubes of C2.
-    python tools/dist_balance.py R"""
+rank's own kernels).  Default: the weak-scaling workload of bench.py (R tiled unit cubes
+of C2); with a config name, that one problem partitioned R ways (strong scaling).
+    python tools/dist_balance.py R [C4]"""
 import json
 import os
 import sys
@@ -14,7 +15,8 @@ import paper_1211_2517_b200 as K  # noqa: E402
 import synth_inputs  # noqa: E402
 
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-pts, q, cfg = synth_inputs.make("C2", scale=R)
+name = sys.argv[2] if len(sys.argv) > 2 else None
+pts, q, cfg = synth_inputs.make(name, seed=0) if name else synth_inputs.make("C2", scale=R)
 dev = torch.device("cuda:0")
 P = torch.from_numpy(pts).to(dev)
 plans = [K.Plan(P, None, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], nranks=R, rank=r, profile=True)
@@ -37,7 +39,17 @@ for _ in range(5):
                      for pl in plans])
 ms = np.median(np.array(per_rank), axis=0)
 infos = [pl.get_info() for pl in plans]
-print(json.dumps(dict(ranks=R, N=cfg["N"], per_rank_compute_ms=[round(float(x), 3) for x in ms],
+single = None
+if name:  # the same problem on one rank (profiled plan), for the strong-scaling comparison
+    del plans
+    torch.cuda.empty_cache()
+    one = K.Plan(P, None, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True)
+    Qd = torch.from_numpy(q).to(dev)
+    for _ in range(3):
+        one.matvec(Qd)
+    torch.cuda.synchronize()
+    single = float(sum(v for k, v in one.get_info()["phase_ms"].items() if k not in ("density", "exchange")))
+print(json.dumps(dict(config=name or f"C2 x {R} tiles", single_rank_ms=single, ranks=R, N=cfg["N"], per_rank_compute_ms=[round(float(x), 3) for x in ms],
                       max_ms=float(ms.max()), mean_ms=float(ms.mean()), imbalance=float(ms.max() / ms.mean()),
                       owned=[i["own_hi"] - i["own_lo"] for i in infos],
                       ghost_q_rows=[i["ghost_q_recv"] for i in infos], ghost_dens=[i["ghost_d_recv"] for i in infos],
