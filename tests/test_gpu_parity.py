@@ -354,3 +354,24 @@ def test_operator_file_cache(tmp_path):
     with pytest.raises(RuntimeError) as e:
         gpu_plan(pts, 4, 24, s, operator_file=path)
     assert "(-2)" in str(e.value) and "operator file" in str(e.value)
+
+
+def test_depth_cap_duplicate_clusters():
+    """Coincident points beyond the leaf size end in depth-cap leaves larger than s (here
+    500 and 300 copies of two points, s = 64): k_near runs them in several passes with the
+    r = 0 test on the leaf's own points; the result is the oracle's (and the direct sum's
+    where the FMM is exact enough)."""
+    rng = np.random.default_rng(21)
+    pts = np.vstack([rng.random((3000, 3)), np.tile([[0.25, 0.5, 0.75]], (500, 1)),
+                     np.tile([[0.25 + 1e-9, 0.5, 0.75]], (300, 1))])
+    q = rng.uniform(-1, 1, pts.shape[0])
+    tb = tables(4, 24)
+    ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
+    for mode in ("1", "0"):
+        os.environ["KIFMM_SYM"] = mode
+        try:
+            gp = gpu_plan(pts, 4, 24, 64, tb=tb)
+        finally:
+            del os.environ["KIFMM_SYM"]
+        out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+        assert rel(out, ref) <= TOL, mode
