@@ -488,9 +488,22 @@ int build_schedules(Plan& P, cudaStream_t st) {
       std::vector<int> fill(vcnt.begin(), vcnt.end() - 1);
       for (auto& v : V) vby[fill[v.x]++] = v;
     }
-    std::vector<std::vector<int>> cls_cols(kCls);  // column records (9 ints) per class
+    // Sibling groups (target B, source parent Q) with only some of Q's V-children present
+    // (surface trees) become columns of a *masked* class — the class's steps restricted to
+    // the present children (same kernel, no absent-child GEMM steps, one RED row per
+    // column) — when that (class, mask) gathers at least mask_min columns; the rest go by
+    // the cost model below (the full class, absent children included, or one-operator
+    // pseudo-classes per pair).
     std::vector<PairGroup> groups(kNumOffsets);
     for (int o = 0; o < kNumOffsets; ++o) groups[o] = PairGroup{o, 1.0, {}};
+    const int NTs = sib_tile_width(kp, P.lr.on && P.lr.rp <= 32);  // (k_m2l_lr2 takes rp 16 / 32)
+    static const int mask_min_env = [] { const char* e = std::getenv("KIFMM_M2L_MASK_MIN"); return e ? std::atoi(e) : -1; }();
+    // 256 measured best of 16-2048 (tools/m2l_scale.py): C4 M2L 6.50 -> 5.61 ms, C5 29.0 ->
+    // 28.0 ms; C3 neutral (below ~512 its sparse masks split into partly filled tiles)
+    const int mask_min = mask_min_env >= 0 ? mask_min_env : 256;
+    struct SibGroup { int b, cls, mask, cnt; int src[8]; };
+    std::vector<SibGroup> sgs;
+    std::vector<int> mcount(kSib * 256, 0);
     int ap[3], aq[3];
     for (int b = 0; b < nb; ++b) {
       const int e0 = vcnt[b], e1 = vcnt[b + 1];
@@ -511,44 +524,81 @@ int build_schedules(Plan& P, cudaStream_t st) {
       for (int i = 0; i < nq; ++i) {
         anchor(qs[i], aq);
         const int lin = (aq[0] - ap[0] + 1) * 9 + (aq[1] - ap[1] + 1) * 3 + (aq[2] - ap[2] + 1);
-        const int cls = (lin < 13 ? lin : lin - 1) * 8 + a;
-        int src[8] = {-1, -1, -1, -1, -1, -1, -1, -1}, cnt = 0;
+        SibGroup g{b, (lin < 13 ? lin : lin - 1) * 8 + a, 0, 0, {-1, -1, -1, -1, -1, -1, -1, -1}};
         for (int e = e0; e < e1; ++e)
-          if (T.parent[vby[e].y] == qs[i]) { src[T.key[vby[e].y] & 7] = vby[e].y; ++cnt; }
-        // cost model (per column, FP64 peak 37 TF/s, fp64 L2 RED 5.2e11/s): the sibling
-        // kernel spends nvalid GEMM columns + 1 RED row, offset-major cnt x (GEMM + RED row);
-        // the RED weight 0.5 is the measured best of 0.25 / 0.5 / 1 / 2 over C3-C5
-        // (tools/m2l_scale.py: C4 M2L 6.49 ms at 0.5 vs 6.51 at 1; C5 29.0 vs 29.2)
-        static const double red_scale = [] { const char* e = std::getenv("KIFMM_M2L_RED_SCALE"); return e ? std::atof(e) : 0.5; }();
-        const double Gc = 2.0 * kp * kp / 37e12, Rr = red_scale * kp / 5.2e11;
-        if (cnt * (Gc + Rr) >= nvalid[cls] * Gc + Rr) {
-          auto& cc = cls_cols[cls];
-          cc.push_back(b);
-          for (int j = 0; j < 8; ++j) cc.push_back(src[j]);
-        } else {
-          for (int e = e0; e < e1; ++e)
-            if (T.parent[vby[e].y] == qs[i]) {
-              if (sparse_in_sib) {
-                auto& cc = cls_cols[kSib + vby[e].z];
-                cc.push_back(b);
-                cc.push_back(vby[e].y);
-                for (int j = 1; j < 8; ++j) cc.push_back(-1);
-              } else {
-                groups[vby[e].z].pairs.push_back(make_int2(vby[e].y, b));
-              }
-            }
+          if (T.parent[vby[e].y] == qs[i]) {
+            const int cb = (int)(T.key[vby[e].y] & 7);
+            g.src[cb] = vby[e].y;
+            g.mask |= 1 << cb;
+            ++g.cnt;
+          }
+        ++mcount[g.cls * 256 + g.mask];
+        sgs.push_back(g);
+      }
+    }
+    std::vector<int> full_mask(kSib, 0);
+    for (int c = 0; c < kSib; ++c)
+      for (int j = 0; j < classes[c * 17]; ++j) full_mask[c] |= 1 << classes[c * 17 + 1 + j];
+    std::vector<int> vclass(kSib * 256, -1);  // (class, mask) -> masked class id
+    std::vector<std::vector<int>> cls_cols(kCls);  // column records (9 ints) per class
+    auto add_col = [&](int c, const SibGroup& g) {
+      auto& cc = cls_cols[c];
+      cc.push_back(g.b);
+      for (int j = 0; j < 8; ++j) cc.push_back(g.src[j]);
+    };
+    for (const SibGroup& g : sgs) {
+      if (g.mask == full_mask[g.cls]) { add_col(g.cls, g); continue; }
+      if (mcount[g.cls * 256 + g.mask] >= mask_min) {
+        int& id = vclass[g.cls * 256 + g.mask];
+        if (id < 0) {  // record: the full class's steps whose child is present
+          id = (int)cls_cols.size();
+          cls_cols.emplace_back();
+          std::vector<int> rec(17, -1);
+          const int* fr = &classes[g.cls * 17];
+          int nv = 0;
+          for (int j = 0; j < fr[0]; ++j)
+            if (g.mask >> fr[1 + j] & 1) { rec[1 + nv] = fr[1 + j]; rec[9 + nv] = fr[9 + j]; ++nv; }
+          rec[0] = nv;
+          classes.insert(classes.end(), rec.begin(), rec.end());
+          nvalid.push_back(nv);
+        }
+        add_col(id, g);
+        continue;
+      }
+      // cost model (per column, FP64 peak 37 TF/s, fp64 L2 RED 5.2e11/s): the sibling
+      // kernel spends nvalid GEMM columns + 1 RED row, offset-major cnt x (GEMM + RED row);
+      // the RED weight 0.5 is the measured best of 0.25 / 0.5 / 1 / 2 over C3-C5
+      // (tools/m2l_scale.py: C4 M2L 6.49 ms at 0.5 vs 6.51 at 1; C5 29.0 vs 29.2)
+      static const double red_scale = [] { const char* e = std::getenv("KIFMM_M2L_RED_SCALE"); return e ? std::atof(e) : 0.5; }();
+      const double Gc = 2.0 * kp * kp / 37e12, Rr = red_scale * kp / 5.2e11;
+      if (g.cnt * (Gc + Rr) >= nvalid[g.cls] * Gc + Rr) {
+        add_col(g.cls, g);
+      } else {
+        for (int j = 0; j < 8; ++j) {
+          if (g.src[j] < 0) continue;
+          int o = -1;  // the pair's offset id: the class step of child j
+          for (int t = 0; t < classes[g.cls * 17]; ++t)
+            if (classes[g.cls * 17 + 1 + t] == j) o = classes[g.cls * 17 + 9 + t];
+          if (sparse_in_sib) {
+            auto& cc = cls_cols[kSib + o];
+            cc.push_back(g.b);
+            cc.push_back(g.src[j]);
+            for (int t = 1; t < 8; ++t) cc.push_back(-1);
+          } else {
+            groups[o].pairs.push_back(make_int2(g.src[j], g.b));
+          }
         }
       }
     }
     if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
     P.m2l_exec_flops = 0;
-    for (int cls = 0; cls < kCls; ++cls) P.m2l_exec_flops += (double)nvalid[cls] * (cls_cols[cls].size() / 9) * 2.0 * P.k * P.k;
+    const int ncls = (int)cls_cols.size();
+    for (int cls = 0; cls < ncls; ++cls) P.m2l_exec_flops += (double)nvalid[cls] * (cls_cols[cls].size() / 9) * 2.0 * P.k * P.k;
     for (auto& g : groups) P.m2l_exec_flops += (double)g.pairs.size() * 2.0 * P.k * P.k;
     // sibling tiles: per class, columns in target order, NT columns per tile
-    const int NTs = sib_tile_width(kp, P.lr.on && P.lr.rp <= 32);  // (k_m2l_lr2 takes rp 16 / 32)
     std::vector<int> cols;
     std::vector<int4> tiles;
-    for (int cls = 0; cls < kCls; ++cls) {
+    for (int cls = 0; cls < ncls; ++cls) {
       const auto& cc = cls_cols[cls];
       const int ncol = (int)cc.size() / 9;
       const int base = (int)cols.size() / 9;
