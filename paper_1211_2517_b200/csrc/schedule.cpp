@@ -591,6 +591,15 @@ int build_schedules(Plan& P, cudaStream_t st) {
       }
     }
     if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
+    if (std::getenv("KIFMM_DEBUG_M2L")) {  // diagnostics: columns per class kind
+      int64_t full = 0, masked = 0, pseudo = 0;
+      for (size_t c = 0; c < cls_cols.size(); ++c) {
+        const int64_t n = cls_cols[c].size() / 9;
+        if ((int)c < kSib) full += n; else if ((int)c < kCls) pseudo += n; else masked += n;
+      }
+      std::fprintf(stderr, "m2l columns: full-class %lld masked %lld (classes %zu) pseudo %lld; groups %zu\n",
+                   (long long)full, (long long)masked, cls_cols.size() - kCls, (long long)pseudo, sgs.size());
+    }
     P.m2l_exec_flops = 0;
     const int ncls = (int)cls_cols.size();
     for (int cls = 0; cls < ncls; ++cls) P.m2l_exec_flops += (double)nvalid[cls] * (cls_cols[cls].size() / 9) * 2.0 * P.k * P.k;
