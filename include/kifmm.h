@@ -88,7 +88,7 @@ typedef struct {
   int leaf_ops;       /* per-leaf S2M and L2T operators built at setup (owned points x kp
                          doubles each): a matvec then streams them from HBM instead of
                          evaluating n kernel values per point and operator.  -1 (default): each
-                         while max(16 GB, 25% of the device) stays free; 0 off; 1 on. */
+                         while max(16 GB, 10% of the device) stays free; 0 off; 1 on. */
   double m2l_c2;      /* stage 2 of the M2L compression: each core C_o is replaced
                          by its SVD truncated at eps2 ||K_fat||_2 with eps2 = C2 eps1 / k
                          (eq-vareps2; eps1 = sigma_{k+1} / sigma_1, the stage-1 truncation) and

@@ -13,6 +13,11 @@
 
 namespace kifmm {
 
+// device memory the automatic leaf / X operators leave free: max(16 GB, 10% of the device)
+// (measured headroom need: the plan's own work buffers are allocated before this check)
+static double leaf_op_reserve(size_t total) { return std::max(16.0 * (1 << 30), 0.10 * (double)total); }
+
+
 namespace {
 
 template <typename T>
@@ -107,12 +112,12 @@ int build_schedules(Plan& P, cudaStream_t st) {
   const DistPlan& Dp = P.dist;
   auto inD = [&](int b) { return Dp.inD[b] != 0; };
   // per-leaf S2M / L2T operators (owned points x kp doubles each): on request, or
-  // automatically while they leave max(16 GB, 25% of the device) free (S2M first)
+  // automatically while they leave kLeafOpReserve free (S2M first)
   {
     const double one = (double)(Dp.own_hi - Dp.own_lo) * kp * sizeof(double);
     size_t fr = 0, tot = 0;
     KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
-    const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot);
+    const double budget = (double)fr - leaf_op_reserve(tot);
     const bool on = P.leaf_ops_opt > 0, au = P.leaf_ops_opt < 0;
     P.leaf_s2m = on || P.bem || (au && one <= budget);  // BEM: S2M by element integration, always an operator
     P.leaf_l2t = on || (au && one * (P.leaf_s2m ? 2 : 1) <= budget);
@@ -152,7 +157,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
       if (inD(x.x) && x.z) slots += npts(x.y);
     size_t fr = 0, tot = 0;
     KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
-    const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot);
+    const double budget = (double)fr - leaf_op_reserve(tot);
     // (slot offsets are int32: past ~2e9 slots the one-sided k_eval path takes over)
     if (4.0 * (double)slots > budget || slots > 2000000000LL) mutual = false;
   }
@@ -688,8 +693,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     size_t fr = 0, tot = 0;
     KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
     const double used = (P.leaf_s2m ? 1.0 : 0.0) + (P.leaf_l2t ? 1.0 : 0.0);
-    const double budget = (double)fr - std::max(16.0 * (1 << 30), 0.25 * (double)tot) -
-                          used * (double)(Dp.own_hi - Dp.own_lo) * kp * sizeof(double);
+    const double budget = (double)fr - leaf_op_reserve(tot) - used * (double)(Dp.own_hi - Dp.own_lo) * kp * sizeof(double);
     P.leaf_x = !xitems.empty() && (P.leaf_ops_opt > 0 || P.bem ||
                                    (P.leaf_ops_opt < 0 && (double)xcnt * sizeof(double) <= budget));
     if (P.leaf_x) {
