@@ -9,21 +9,23 @@
 // with a leaf of another rank) complete its source list.  About 13 FP64 instructions
 // per unordered pair instead of 2 x 12 one-sided.
 //
-// Work unit: a pass of up to TB x MQ targets of one leaf against its source list, in
-// chunks of <= near_ch(TB MQ) source slots (host-built point-index table: no
-// per-source search, no segment scan on the device).  Thread (ti, gi) holds targets
-// ti + MQ u (u < TB) and sweeps sources gi, gi + G, ... of each chunk (G = NT / MQ
-// slices).  MQ is a power of two, so a slice's MQ lanes are adjacent lanes of one
-// warp: for mutual sources each lane forms s_j = sum_u q_u G(x_u, y_j) and every SB
-// steps a butterfly reduce-scatter over the slice leaves sum_i q_i G(x_i, y_j) on one
-// lane, which adds it to p_j with one RED.  Target sums are reduced over the G slices
-// in shared memory at the end of the pass and added with RED (other CTAs deposit
-// mutual contributions into the same potentials).
+// Work unit: a pass of up to TB x MQ targets of one leaf against at most 4 chunks of its
+// source list; a chunk is <= near_ch(TB MQ) source slots of a host-built point-index
+// table (no per-source search, no segment scan on the device).  Thread (ti, gi) holds
+// targets ti + MQ u (u < TB) and sweeps sources gi, gi + G, ... of each chunk (G = NT / MQ
+// slices).  MQ is a power of two, so a slice's MQ lanes are adjacent lanes of one warp:
+// for mutual sources each lane forms s_j = sum_u q_u G(x_u, y_j) and every SB steps a
+// butterfly reduce-scatter over the slice leaves sum_i q_i G(x_i, y_j) on one lane, which
+// adds it to p_j with one RED.  Target sums are reduced over the G slices in shared memory
+// at the end of the unit and added with RED (other CTAs deposit mutual contributions into
+// the same potentials).  Double-layer sources take the same path with their normals
+// (k_near<TB, MQ, true>).
 //
-// Persistent CTAs, software-pipelined across work units: while chunk c is evaluated,
-// chunk c + 1 — possibly the first chunk of the CTA's next item, together with that
-// pass's targets — is already in flight into the other buffer (cp.async), and the
-// item records are plain int4 (no dependent metadata loads).
+// Persistent CTAs, one launch per pass shape; units are taken from a global counter
+// (longest first), two ahead of use.  Software-pipelined: while chunk c is evaluated,
+// chunk c + 1 — possibly the first chunk of the CTA's next unit, with that unit's targets —
+// is already in flight into the other buffer (cp.async from slot indices loaded one chunk
+// earlier), so no load of the critical path waits on metadata.
 #include <algorithm>
 #include <vector>
 
