@@ -197,7 +197,7 @@ struct Plan {
   int* d_nr_src = nullptr;
   int* d_nr_counters = nullptr;            // work counters per k_near launch (2 per group)
   int nr_spare = 0;                        // overlap mode 3: CTA slots per SM left to the kernels beside k_near
-  double nr_split = 0.4;                   // overlap mode 3: share of each group's units run beside S2M / M2M
+  double nr_split = 1.0;                   // overlap mode 3: share of each group's units launched at the fork (rest after M2L)
   int64_t nr_src_bytes = 0;
   std::vector<int3> nr_groups;             // (pass shape, first item, count) per k_near launch
   int* d_near_off = nullptr; int4* d_near_seg = nullptr; int n_near_seg = 0;
