@@ -298,9 +298,10 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     // (default only up to 8M owned points: C2 / C3 gain 2-10%, C4 / C5 lose 1-2% — their long
     // k_near and M2L launches have little tail to fill, and the split costs k_near balance)
     const int64_t owned = P.dist.own_hi - P.dist.own_lo;
-    const bool ovl_default = P.nr_on && !P.profile && owned <= (int64_t)8 << 20;
-    P.overlap = (!P.split_phases && !P.bem) ? (e ? std::atoi(e) : (ovl_default ? 3 : 0)) : 0;
-    if (P.overlap == 3 && !P.nr_on) P.overlap = 0;  // mode 3 splits k_near
+    const bool ovl_default = (P.nr_on || P.bem) && !P.profile && owned <= (int64_t)8 << 20;
+    P.overlap = !P.split_phases ? (e ? std::atoi(e) : (ovl_default ? 3 : 0)) : 0;
+    if (P.bem && P.overlap != 3) P.overlap = 0;         // BEM: only the SpMV fork (mode 3)
+    if (P.overlap == 3 && !P.nr_on && !P.bem) P.overlap = 0;  // mode 3 runs k_near or the BEM SpMV
     if (const char* f = std::getenv("KIFMM_NEAR_SPLIT")) P.nr_split = std::atof(f);
     if (const char* f = std::getenv("KIFMM_NEAR_SPARE")) P.nr_spare = std::atoi(f);
     int lo_prio = 0, hi_prio = 0;

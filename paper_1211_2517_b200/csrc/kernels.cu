@@ -2003,11 +2003,17 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (launch_near(P, ea, P.stream_near)) return -3;
         KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
       }
-      if (P.overlap == 3) {  // k_near part 1 beside the HBM-bound S2M / M2M (one CTA slot per SM left free)
+      if (P.overlap == 3) {  // near field on the near stream from here, beside the far field
         KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
         KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
-        KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, P.stream_near));
-        if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
+        if (P.bem) {  // BEM: the element-integral block SpMV (HBM-bound) beside the M2L (tensor)
+          ++g_launches;
+          if (bem_near_matvec(P, P.stream_near)) return -3;
+          KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
+        } else {
+          KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, P.stream_near));
+          if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
+        }
       }
       KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
@@ -2071,7 +2077,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
         KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_m2l, 0));
       }
-      if (P.overlap == 3) {  // k_near part 2 after the M2L, beside X / L2L / L2T / the far pass
+      if (P.overlap == 3 && !P.bem) {  // k_near part 2 after the M2L, beside X / L2L / L2T / the far pass
         KIFMM_CUDA(cudaEventRecord(P.ev_m2l, st));
         KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_m2l, 0));
         if (near_launch(P, P.d_pot_near, P.stream_near, 2, P.nr_spare)) return -3;
@@ -2106,8 +2112,10 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       // kernel) unless it runs on the overlapped near stream
       const bool sep = P.split_phases || P.overlap || P.d_nrm || P.bem;
       if (P.bem) {  // BEM near field: the precomputed element-integral blocks
-        ++g_launches;
-        if (bem_near_matvec(P, st)) return -3;
+        if (P.overlap != 3) {  // (overlapped: launched on the near stream at the fork)
+          ++g_launches;
+          if (bem_near_matvec(P, st)) return -3;
+        }
       } else if (sep && !P.overlap && launch_near(P, ea, st)) {
         return -3;
       }
