@@ -58,11 +58,15 @@ print(json.dumps(dict(workload=f"BEM sphere octa-{lv}", N=N, leaf=s, p=p, k=inf[
 f = Q.clone()
 pl.gmres(f, restart=50, maxit=20, tol=1e-6)  # warm-up (workspace allocation)
 torch.cuda.synchronize()
-t0 = time.perf_counter()
-x, gi = pl.gmres(f, restart=50, maxit=500, tol=1e-6)
-wall = time.perf_counter() - t0
+walls = []
+for _ in range(3):  # host-driven solve: wall clock; the best of three (host jitter)
+    t0 = time.perf_counter()
+    x, gi = pl.gmres(f, restart=50, maxit=500, tol=1e-6)
+    walls.append(time.perf_counter() - t0)
+wall = min(walls)
 r = f - pl.matvec(x)
 print(json.dumps(dict(workload=f"BEM GMRES sphere octa-{lv}", N=N, p=p, k=inf["k"], tol=1e-6, restart=50,
                       iters=gi["iters"], relres=gi["relres"],
                       true_relres=float(torch.linalg.norm(r) / torch.linalg.norm(f)), solve_s=wall,
-                      T_it_ms=wall / max(1, gi["iters"]) * 1e3, matvec_ms=gi["t_matvec_ms"])))
+                      T_it_ms=wall / max(1, gi["iters"]) * 1e3, matvec_ms=gi["t_matvec_ms"],
+                      solve_s_all=walls)))
