@@ -375,3 +375,20 @@ def test_depth_cap_duplicate_clusters():
             del os.environ["KIFMM_SYM"]
         out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
         assert rel(out, ref) <= TOL, mode
+
+
+def test_degenerate_clouds():
+    """All points coincident (one depth-cap leaf of 1000 points: every pair has r = 0,
+    the potential is exactly zero) and points on a line (a flat bounding box): the
+    oracle's results."""
+    tb = tables(4, 24)
+    pts = np.tile([[0.3, -0.2, 0.7]], (1000, 1))
+    q = np.random.default_rng(5).uniform(-1, 1, 1000)
+    out = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert np.all(out == 0.0)
+    t = np.random.default_rng(6).random(5000)
+    pts = np.stack([t, 2 * t + 1, np.full_like(t, 0.5)], axis=1)
+    q = np.random.default_rng(7).uniform(-1, 1, t.size)
+    ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
+    out = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel(out, ref) <= TOL
