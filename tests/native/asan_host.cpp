@@ -1,11 +1,12 @@
 // Host-code sanitizer driver (host code under -fsanitize=address,undefined).
-// Builds the library's HOST-ONLY parts (partition.cpp, precompute.cpp) from source with
+// Builds the library's HOST-ONLY parts (partition.cpp, precompute.cpp, tables_io.cpp) from source with
 // AddressSanitizer + UBSan and exercises them:
 //   * build_partition for nranks 1, 2, 3, 5, 8 and every rank on a tree + lists read
 //     from a binary dump (written by tests/test_native_asan.py from the oracle),
 //     checking that what rank s sends to r is what r expects from s;
-//   * build_tables (p = 4, k = 24) and build_stage2 (C2 = 1).
-// Usage: asan_host dump.bin   (exit 0 = clean)
+//   * build_tables (p = 4, k = 24), the operator-table file round trip (tables_io.cpp) and
+//     build_stage2 (C2 = 1).
+// Usage: asan_host dump.bin [table_file]   (exit 0 = clean)
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -63,6 +64,23 @@ int main(int argc, char** argv) {
   }
   HostTables H;
   if (build_tables(4, 24, 0.1, 1e-10, &H) || H.k != 25) { std::fprintf(stderr, "tables failed\n"); return 1; }
+  // the operator-table file: write, read back bit for bit, refuse a corrupted copy
+  if (argc > 2) {
+    const std::string path = argv[2];
+    if (save_tables(H, 24, path)) { std::fprintf(stderr, "save failed\n"); return 1; }
+    HostTables L;
+    int kr = 0;
+    if (load_tables(path, &L, &kr) || kr != 24 || L.C != H.C || L.U != H.U || L.S != H.S || L.T != H.T ||
+        L.M != H.M || L.L != H.L || L.sigma != H.sigma || L.surf != H.surf) {
+      std::fprintf(stderr, "table file round trip failed\n");
+      return 1;
+    }
+    FILE* f = std::fopen(path.c_str(), "r+b");
+    std::fseek(f, 200, SEEK_SET);
+    std::fputc(0x5a, f);
+    std::fclose(f);
+    if (load_tables(path, &L, &kr) != -1) { std::fprintf(stderr, "corrupt table file accepted\n"); return 1; }
+  }
   if (build_stage2(H, 1.0) || (int)H.ranks.size() != 316) { std::fprintf(stderr, "stage2 failed\n"); return 1; }
   std::printf("asan host driver ok\n");
   return 0;

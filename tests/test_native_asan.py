@@ -1,5 +1,5 @@
-"""Host code under AddressSanitizer + UBSan: the library's host-only partition
-and precompute sources compiled with -fsanitize=address,undefined into a driver run on an
+"""Host code under AddressSanitizer + UBSan: the library's host-only partition,
+precompute and table-file sources compiled with -fsanitize=address,undefined into a driver run on an
 oracle-built adaptive tree (tests/native/asan_host.cpp)."""
 import os
 import subprocess
@@ -18,7 +18,7 @@ def test_host_code_clean_under_asan_ubsan(tmp_path):
     cmd = ["g++", "-std=c++17", "-O1", "-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined",
            "-fno-sanitize-recover=all", "-fopenmp", "-I/usr/local/cuda/include",
            os.path.join(ROOT, "tests", "native", "asan_host.cpp"), os.path.join(CSRC, "partition.cpp"),
-           os.path.join(CSRC, "precompute.cpp"), "-o", str(exe)]
+           os.path.join(CSRC, "precompute.cpp"), os.path.join(CSRC, "tables_io.cpp"), "-o", str(exe)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         pytest.fail("build failed:\n" + r.stderr[-3000:])
@@ -36,6 +36,7 @@ def test_host_code_clean_under_asan_ubsan(tmp_path):
         for a in "UVWX":
             L[a].astype(np.int32).tofile(f)
     env = dict(os.environ, ASAN_OPTIONS="detect_leaks=1:abort_on_error=1", OMP_NUM_THREADS="2")
-    r = subprocess.run([str(exe), str(dump)], capture_output=True, text=True, env=env, timeout=600)
+    r = subprocess.run([str(exe), str(dump), str(tmp_path / "t.kifmm")], capture_output=True, text=True, env=env,
+                       timeout=600)
     assert r.returncode == 0, r.stderr[-4000:]
     assert "asan host driver ok" in r.stdout
