@@ -127,10 +127,17 @@ template <int TB, int MQ>
 __device__ __forceinline__ void nr_mutual(const double4* sbuf, const int* sidx, int lo, int j0, int j1, int G,
                                           const double (&x)[TB][3], const double (&q)[TB], double (&acc)[TB],
                                           double* __restrict__ out) {
-  constexpr int SB = MQ < 4 ? MQ : 4;
+#ifndef KIFMM_NEAR_SB
+#define KIFMM_NEAR_SB 4
+#endif
+  constexpr int SB = MQ < KIFMM_NEAR_SB ? MQ : KIFMM_NEAR_SB;
   const int nmin = (j1 - lo) / G, nsteps = (j1 - lo + G - 1) / G;  // uniform over the CTA
   int s0 = 0;
   for (; s0 + SB <= nmin; s0 += SB) nr_mutual_batch<TB, MQ, SB, false>(sbuf, sidx, j0, j1, G, s0, x, q, acc, out);
+  if (SB >= 8 && s0 + 4 <= nmin) {
+    nr_mutual_batch<TB, MQ, (SB >= 4 ? 4 : 1), false>(sbuf, sidx, j0, j1, G, s0, x, q, acc, out);
+    s0 += SB >= 4 ? 4 : 1;
+  }
   if (SB >= 4 && s0 + 2 <= nmin) {
     nr_mutual_batch<TB, MQ, (SB >= 2 ? 2 : 1), false>(sbuf, sidx, j0, j1, G, s0, x, q, acc, out);
     s0 += SB >= 2 ? 2 : 1;
