@@ -1,4 +1,5 @@
-"""Single- vs double-layer matvec timing on a config (diagnostics).
+"""Single- vs double-layer matvec timing on a config (diagnostics): production plans
+(default overlap), and the phases of a profiled twin.
     python tools/dl_timing.py C3"""
 import os
 import sys
@@ -17,7 +18,7 @@ nrm = p / np.linalg.norm(p, axis=1, keepdims=True) if c["kind"] == "sphere_octa"
 nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
 P, Q, Nt = (torch.from_numpy(x).cuda() for x in (p, q, nrm))
 for layer, normals in (("single", None), ("double", Nt)):
-    pl = K.Plan(P, Q, p=c["p"], k=c["k"], leaf_size=c["leaf"], normals=normals, profile=True)
+    pl = K.Plan(P, Q, p=c["p"], k=c["k"], leaf_size=c["leaf"], normals=normals)
     for _ in range(3):
         pl.matvec(Q)
     torch.cuda.synchronize()
@@ -29,7 +30,12 @@ for layer, normals in (("single", None), ("double", Nt)):
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    ph = pl.get_info()["phase_ms"]
-    print(f"{name} {layer}: {sorted(ts)[3]:.3f} ms  ({c['N'] / sorted(ts)[3] / 1e-3:.3e} pts/s)  "
-          + " ".join(f"{k}={v:.3f}" for k, v in ph.items()), flush=True)
     pl.free()
+    pp = K.Plan(P, Q, p=c["p"], k=c["k"], leaf_size=c["leaf"], normals=normals, profile=True)
+    for _ in range(3):
+        pp.matvec(Q)
+    torch.cuda.synchronize()
+    ph = pp.get_info()["phase_ms"]
+    pp.free()
+    print(f"{name} {layer}: {sorted(ts)[3]:.3f} ms  ({c['N'] / sorted(ts)[3] / 1e-3:.3e} pts/s)  phases (serialised): "
+          + " ".join(f"{k}={v:.3f}" for k, v in ph.items()), flush=True)
