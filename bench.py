@@ -267,6 +267,23 @@ def run_ours(args):
         mt = json.load(open(tf))
         traffic = mt.get("bytes_per_launch")
         pipe_pct = mt.get("tensor_pipe_active_pct")
+    # ---- near field (P2P, FP64 ALU): directed point pairs over the profiled "eval" phase, against
+    # the FP64 pipe at the minimal per-pair instruction counts of k_near (13 FP64 per unordered
+    # mutual pair, 12 per one-sided pair: 3 DADD, r^2 3, rsqrt refinement 5, accumulation 1-2)
+    p2p = None
+    if info["near_pairs"] > 0:
+        npair, pm = int(info["near_pairs"]), int(info["near_mutual_pairs"])
+        instr = 13.0 * pm + 12.0 * (npair - 2 * pm)
+        lane_peak = float(peaks["dfma_tflops"]) * 1e12 / 2  # FP64 instruction-lanes / s (a DFMA = 2 flops)
+        eval_s = phase["eval"] * 1e-3
+        p2p = {"bound": "fp64_alu", "kernel": "k_near (mutual leaf pairs)", "directed_pairs": npair,
+               "mutual_pairs": pm, "ms": phase["eval"], "pairs_per_s": npair / eval_s,
+               "fp64_instr_lanes": instr, "peak_instr_lanes_per_s": lane_peak, "frac": instr / lane_peak / eval_s,
+               "note": "ms = the profiled 'eval' phase, which also holds the L2T leaf GEMV and the W far pass; "
+                       "peak = measured DFMA loop (profiles/fp64_peaks_r01.json) / 2"}
+        pf = os.path.join(ROOT, "profiles", "p2p_fp64_pipe.json")
+        if os.path.exists(pf) and ws == 1:
+            p2p["fp64_pipe_active_pct_ncu"] = json.load(open(pf)).get("fp64_pipe_active_pct")
     # ---- cpu baseline: the oracle on the host cores, one full matvec (rank 0, N = 1 only)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
@@ -295,6 +312,7 @@ def run_ours(args):
                      "timed_in": "profiled twin plan of the same workload: phases serialised on one stream, "
                                  "CUDA events around the M2L launches, L2 flushed, same step count"},
         "phase_ms": phase,
+        "p2p": p2p,
         "clocks": clk.summary(),
         "e2e": {"value": N / e2e_s, "unit": "points/s", "h2d_bytes_per_step": e2e_bytes,
                 "d2h_bytes_per_step": e2e_bytes, "ms_per_step": e2e_s * 1e3, "api": e2e_api},

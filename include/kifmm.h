@@ -145,6 +145,9 @@ typedef struct {
   int64_t near_sym_pairs;     /* leaf pairs of the warp-pair symmetric kernel (KIFMM_SYM=2) */
   double m2l_exec_flops;      /* M2L flops the kernels execute: 2 k^2 per sibling-class column
                                  step (absent children included) + the offset-major pairs */
+  int64_t near_pairs;         /* directed near-field point pairs (U + direct W/X, r = 0 pairs
+                                 included) delivered by k_near per matvec: own points m^2, 2 per
+                                 mutual pair, 1 per one-sided pair (mutual mode; 0 otherwise) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

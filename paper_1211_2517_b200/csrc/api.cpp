@@ -598,6 +598,7 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
   info->near_mutual_pairs = P.n_mut_pairs;
   info->near_sym_pairs = P.n_sym;
   info->m2l_exec_flops = P.m2l_exec_flops;
+  info->near_pairs = P.n_near_pairs;
   info->m2l_flops = P.m2l_flops;
   info->m2l_eps2 = P.tables.eps2;
   {

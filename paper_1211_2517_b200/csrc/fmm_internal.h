@@ -191,6 +191,7 @@ struct Plan {
   int nr_table = 0;                        // k_near shape table (KIFMM_NEAR_TAB)
   int n_tleaf_mut = 0;                     // target leaves with mutual segments
   int64_t n_mut_pairs = 0;                 // unordered point pairs of the mutual segments
+  int64_t n_near_pairs = 0;               // directed near-field point pairs (k_near mode)
   double m2l_exec_flops = 0;               // M2L flops executed incl. absent sibling children
   int4* d_nr_items = nullptr;
   int4* d_nr_chunks = nullptr;

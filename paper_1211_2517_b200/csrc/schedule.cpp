@@ -275,6 +275,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   P.nr_on = mutual;
   P.n_tleaf_mut = 0;
   P.n_mut_pairs = 0;
+  P.n_near_pairs = 0;
   P.nr_groups.clear();
   if (mutual && nt > 0) {
     static const int kMinGroup = [] { const char* e = std::getenv("KIFMM_NEAR_MINGROUP"); return e ? std::atoi(e) : 2048; }();
@@ -307,6 +308,9 @@ int build_schedules(Plan& P, cudaStream_t st) {
       const int b = titems[i].x;
       if (!mnear[i].empty()) ++P.n_tleaf_mut;
       for (auto& sg : mnear[i]) P.n_mut_pairs += (int64_t)npts(b) * sg.w;
+      P.n_near_pairs += (int64_t)npts(b) * npts(b);
+      for (auto& sg : mnear[i]) P.n_near_pairs += 2 * (int64_t)npts(b) * sg.w;
+      for (size_t k = 1; k < near[i].size(); ++k) P.n_near_pairs += (int64_t)npts(b) * near[i][k].w;
       const int CH = near_ch(near_shape_cap(nr_tab, shp[i]), dl);
       const int cb = (int)nchunks.size();
       int n = 0, nchk = 0, ml = -1, mh = -1;

@@ -114,6 +114,22 @@ def test_matvec_parity_shared_tables(case, wx, leaf_ops):
         assert rel(gp.export_phase("far"), ph["far"]) <= TOL
 
 
+@pytest.mark.parametrize("case", list(CASES))
+def test_near_pair_count(case):
+    # fmm_info.near_pairs (the P2P work the bench's near-field roofline divides by) equals
+    # the oracle's count: sum over U pairs and direct W / X pairs of m_target * m_source (O9)
+    pts, q, p, k, s = CASES[case]()
+    tb = tables(p, k)
+    op = oracle.Plan(pts, s, tb["n"])
+    t, li = op.tree(), op.lists()
+    m = (t["pend"] - t["pbeg"]).astype(np.int64)
+    want = int(np.sum(m[li["U"][:, 0]] * m[li["U"][:, 1]]))
+    for f in "WX":
+        d = li[f][li[f][:, 2] != 0]
+        want += int(np.sum(m[d[:, 0]] * m[d[:, 1]]))
+    assert gpu_plan(pts, p, k, s, tb=tb).info["near_pairs"] == want
+
+
 @pytest.mark.parametrize("leaf_ops", [0, 1])
 def test_c2_full_size_parity(leaf_ops):
     # BASELINE configs[1] at full size, in the launch configuration bench.py times
