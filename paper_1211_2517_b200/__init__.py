@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkifmm_b200.so")
+LIB_PATH = os.environ.get("KIFMM_LIB") or os.path.join(_HERE, "libkifmm_b200.so")  # KIFMM_LIB: diagnostic builds
 
 FMM_OK, FMM_EINVAL, FMM_ECONFIG, FMM_ECUDA, FMM_ENOMEM, FMM_ENCCL = 0, -1, -2, -3, -4, -5
 
