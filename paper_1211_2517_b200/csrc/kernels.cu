@@ -1001,17 +1001,38 @@ __global__ void __launch_bounds__(256) k_leafop_build(const int4* __restrict__ i
       Gs[i * (LO_CH + 1) + jj] = v;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < kp * LO_CH; e += blockDim.x) {
-      const int a = e / LO_CH, jj = e - a * LO_CH;
-      if (jj >= cm) continue;
-      const double* op = Op + (size_t)a * sa;
-      double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc = fma(op[(size_t)i * si], Gs[i * (LO_CH + 1) + jj], acc);
-      acc *= scale;
-      const int j = c0 + jj;
-      if (MODE == 0) out[(size_t)(p0 + j - own_lo) * kp + a] = acc;
-      else if (MODE == 2) out[xmoff[blockIdx.x] + (size_t)j * kp + a] = acc;
-      else out[(size_t)(p0 + j - own_lo) * kp + a] = acc;  // L2T: point-major rows like S2M
+    // 4 x 4 register blocks (rows a0.., points j0..): 8 loads per 16 FMAs; each entry keeps
+    // the sequential sum over i
+    constexpr int JB = LO_CH / 4;
+    for (int e = threadIdx.x; e < (kp / 4) * JB; e += blockDim.x) {
+      const int a0 = (e / JB) * 4, j0 = (e - (e / JB) * JB) * 4;
+      if (j0 >= cm) continue;
+      double acc[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+      const double* op = Op + (size_t)a0 * sa;
+      for (int i = 0; i < n; ++i) {
+        double o[4], g[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[u] = op[(size_t)u * sa + (size_t)i * si];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) g[v] = Gs[i * (LO_CH + 1) + j0 + v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(o[u], g[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        if (j0 + v >= cm) break;
+        const int j = c0 + j0 + v;
+        double* row = MODE == 2 ? out + xmoff[blockIdx.x] + (size_t)j * kp
+                                : out + (size_t)(p0 + j - own_lo) * kp;  // point-major rows (S2M, L2T)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) row[a0 + u] = acc[u][v] * scale;
+      }
     }
   }
 }

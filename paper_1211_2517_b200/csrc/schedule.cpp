@@ -2,6 +2,7 @@
 // lists: pair lists + tiles for the grouped GEMM kernel, and segment CSRs for the
 // evaluation kernel.  Applies the W/X "direct" shortcut of reading O5.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -53,6 +54,16 @@ int make_launch(Plan& P, GemmLaunch& L, const std::vector<PairGroup>& groups, in
 }  // namespace
 
 int build_schedules(Plan& P, cudaStream_t st) {
+  // KIFMM_DEBUG_SETUP=1: host time per section (device work synchronised) on stderr
+  static const bool dbg = std::getenv("KIFMM_DEBUG_SETUP") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "schedule %-14s %9.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   Tree& T = P.tree;
   Lists& Ls = P.lists;
   const int nb = T.nboxes, n = P.n, np = P.np, kp = P.kp;
@@ -94,6 +105,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (bad(x.x) || bad(x.y) || !T.leaf[x.y] || (x.z && !T.leaf[x.x])) { set_error("build_schedules: corrupt X list"); return -3; }
   auto npts = [&](int b) { return T.pend[b] - T.pbeg[b]; };
   auto rl = [&](int b) { return std::ldexp(T.r0, -T.level[b]); };
+  mark("lists+validate");
 
   // ---- partition; one rank owns everything
   {
@@ -109,6 +121,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     const int nr = P.dist.nranks, rk = P.dist.rank;
     if (build_partition(in, nr, rk, &P.dist)) return -1;
   }
+  mark("partition");
   const DistPlan& Dp = P.dist;
   auto inD = [&](int b) { return Dp.inD[b] != 0; };
   // per-leaf S2M / L2T operators (owned points x kp doubles each): on request, or
@@ -190,12 +203,16 @@ int build_schedules(Plan& P, cudaStream_t st) {
   };
   // target side of a mutual pair {a, b}, or -1 (not both owned)
   static const bool mut_off = std::getenv("KIFMM_MUT_OFF") != nullptr;  // diagnostics: k_near one-sided only
+  std::vector<int> leaf_slots(nb, 0);  // nr_slots of every owned leaf, once
+  if (mutual)
+    for (int i = 0; i < nt; ++i) leaf_slots[titems[i].x] = nr_slots(npts(titems[i].x));
   auto mut_target = [&](int a, int b) {
     if (!mutual || mut_off || !inD(a) || !inD(b)) return -1;
-    const int64_t ca = (int64_t)nr_slots(npts(a)) * npts(b), cb = (int64_t)nr_slots(npts(b)) * npts(a);
+    const int64_t ca = (int64_t)leaf_slots[a] * npts(b), cb = (int64_t)leaf_slots[b] * npts(a);
     if (ca != cb) return ca < cb ? a : b;
     return ((a ^ b) & 1) ? std::min(a, b) : std::max(a, b);
   };
+  mark("segments setup");
   std::vector<std::vector<int4>> mnear(nt);
   std::vector<int2> sympairs;
   auto add_sym = [&](int a, int b, int c) { sympairs.push_back(c == 1 ? make_int2(a, b) : make_int2(b, a)); };
@@ -211,6 +228,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     }
     near[leaf_row[u.x]].push_back(make_int4(0, T.pbeg[u.y], 0, npts(u.y)));
   }
+  mark("segments U");
   // W pairs: direct -> P2P over the source subtree; else M2T through the source's equivalent density
   std::vector<PairGroup> wgroups;  // grouped by source level (scale r_A)
   std::map<int, int> wlevel;
@@ -268,6 +286,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     far[i].insert(far[i].begin(), make_int4(1, n_l2t, b, n));
     ++n_l2t;
   }
+  mark("segments");
   // k_near tables (mutual mode): per target leaf its source list — own points (checked),
   // mutual segments, one-sided point segments — cut into chunks of near_ch(cap) source slots;
   // work units = (pass of <= TB x MQ targets, <= kUnitChunks chunks), grouped by pass
@@ -301,23 +320,48 @@ int build_schedules(Plan& P, cudaStream_t st) {
       for (int i = 0; i < nt; ++i) shp[i] = remap[shp[i]];
       std::fill(cnt.begin(), cnt.end(), 0);
     }
-    std::vector<int4> nchunks;
-    std::vector<int> nsrc;
-    std::vector<std::vector<std::pair<int64_t, int4>>> units(kNearShapes);  // (cost, unit) per shape
+    // sizes per leaf (slots, chunks = ceil(slots / CH), units = passes x ceil(chunks / kUnitChunks)),
+    // prefix offsets, then every leaf's slots / chunks / units filled in parallel at its offsets
+    std::vector<int64_t> slot_off(nt + 1, 0), chunk_off(nt + 1, 0), unit_off(nt + 1, 0);
+    for (int i = 0; i < nt; ++i) {
+      const int b = titems[i].x, m = npts(b);
+      if (!mnear[i].empty()) ++P.n_tleaf_mut;
+      int64_t slots = m;
+      P.n_near_pairs += (int64_t)m * m;
+      for (auto& sg : mnear[i]) {
+        slots += sg.w;
+        P.n_mut_pairs += (int64_t)m * sg.w;
+        P.n_near_pairs += 2 * (int64_t)m * sg.w;
+      }
+      for (size_t k = 1; k < near[i].size(); ++k) {
+        slots += near[i][k].w;
+        P.n_near_pairs += (int64_t)m * near[i][k].w;
+      }
+      const int CH = near_ch(near_shape_cap(nr_tab, shp[i]), dl);
+      const int cap = std::min(near_shape_cap(nr_tab, shp[i]), pass_size(m));
+      const int64_t nch = (slots + CH - 1) / CH;
+      slot_off[i + 1] = slot_off[i] + slots;
+      chunk_off[i + 1] = chunk_off[i] + nch;
+      unit_off[i + 1] = unit_off[i] + (int64_t)((m + cap - 1) / cap) * ((nch + kUnitChunks - 1) / kUnitChunks);
+    }
+    if (slot_off[nt] > INT32_MAX || chunk_off[nt] > INT32_MAX) {
+      set_error("build_schedules: near-field slot table exceeds 2^31 entries");
+      return -3;
+    }
+    std::vector<int4> nchunks(chunk_off[nt]);
+    std::vector<int> nsrc(slot_off[nt]);
+    std::vector<std::pair<int64_t, int4>> uall(unit_off[nt]);  // (cost, unit), leaf order
+#pragma omp parallel for schedule(dynamic, 256)
     for (int i = 0; i < nt; ++i) {
       const int b = titems[i].x;
-      if (!mnear[i].empty()) ++P.n_tleaf_mut;
-      for (auto& sg : mnear[i]) P.n_mut_pairs += (int64_t)npts(b) * sg.w;
-      P.n_near_pairs += (int64_t)npts(b) * npts(b);
-      for (auto& sg : mnear[i]) P.n_near_pairs += 2 * (int64_t)npts(b) * sg.w;
-      for (size_t k = 1; k < near[i].size(); ++k) P.n_near_pairs += (int64_t)npts(b) * near[i][k].w;
       const int CH = near_ch(near_shape_cap(nr_tab, shp[i]), dl);
-      const int cb = (int)nchunks.size();
+      int64_t spos = slot_off[i];
+      int cpos = (int)chunk_off[i];
       int n = 0, nchk = 0, ml = -1, mh = -1;
       auto flush = [&]() {
         if (n == 0) return;
         if (ml < 0) ml = mh = n;
-        nchunks.push_back(make_int4((int)(nsrc.size() - n), n | (nchk << 10) | (ml << 20), mh, 0));
+        nchunks[cpos++] = make_int4((int)(spos - n), n | (nchk << 10) | (ml << 20), mh, 0);
         n = nchk = 0;
         ml = mh = -1;
       };
@@ -326,7 +370,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
           const int take = std::min(len - off, CH - n);
           if (kind == 1) nchk = n + take;
           if (kind == 3) { if (ml < 0) ml = n; mh = n + take; }
-          for (int t = 0; t < take; ++t) nsrc.push_back(a + off + t);
+          for (int t = 0; t < take; ++t) nsrc[spos++] = a + off + t;
           n += take;
           off += take;
           if (n == CH) flush();
@@ -336,15 +380,21 @@ int build_schedules(Plan& P, cudaStream_t st) {
       for (auto& sg : mnear[i]) add(3, sg.y, sg.w);
       for (size_t k = 1; k < near[i].size(); ++k) add(0, near[i][k].y, near[i][k].w);
       flush();
-      const int ce = (int)nchunks.size(), cap = std::min(near_shape_cap(nr_tab, shp[i]), pass_size(npts(b)));
+      const int cb = (int)chunk_off[i], ce = (int)chunk_off[i + 1];
+      const int cap = std::min(near_shape_cap(nr_tab, shp[i]), pass_size(npts(b)));
+      int64_t upos = unit_off[i];
       for (int t0 = 0; t0 < npts(b); t0 += cap)
         for (int c0 = cb; c0 < ce; c0 += kUnitChunks) {
           const int c1 = std::min(ce, c0 + kUnitChunks);
           int64_t srcs = 0;
           for (int c = c0; c < c1; ++c) srcs += nchunks[c].y & 1023;
-          units[shp[i]].push_back({srcs * cap, make_int4(T.pbeg[b] + t0, std::min(cap, npts(b) - t0), c0, c1)});
-          ++cnt[shp[i]];
+          uall[upos++] = {srcs * cap, make_int4(T.pbeg[b] + t0, std::min(cap, npts(b) - t0), c0, c1)};
         }
+    }
+    std::vector<std::vector<std::pair<int64_t, int4>>> units(kNearShapes);  // (cost, unit) per shape
+    for (int i = 0; i < nt; ++i) {
+      cnt[shp[i]] += (int)(unit_off[i + 1] - unit_off[i]);
+      units[shp[i]].insert(units[shp[i]].end(), uall.begin() + unit_off[i], uall.begin() + unit_off[i + 1]);
     }
     std::vector<int4> nitems;
     for (int c = 0; c < kNearShapes; ++c) {
@@ -361,6 +411,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
         upload(P, &P.d_nr_src, nsrc, st) || upload(P, &P.d_nr_counters, counters, st))
       return -3;
   }
+  mark("k_near tables");
   std::vector<int> near_off{0}, far_off{0}, all_off{0};
   std::vector<int4> near_seg, far_seg, all_seg;
   for (int i = 0; i < nt; ++i) {
@@ -413,6 +464,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
       upload(P, &P.d_far_seg, far_seg, st) || upload(P, &P.d_all_off, all_off, st) ||
       upload(P, &P.d_all_seg, all_seg, st))
     return -3;
+  mark("csr uploads");
   // ---- S2M: leaves at level >= 2
   std::vector<int4> sitems, ssegs;
   std::vector<int> soff{0};
@@ -432,6 +484,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
   if (upload(P, &P.d_s2m_items, sitems, st) || upload(P, &P.d_s2m_off, soff, st) || upload(P, &P.d_s2m_seg, ssegs, st) ||
       upload(P, &P.d_x_items, xitems, st) || upload(P, &P.d_x_off, xoff, st) || upload(P, &P.d_x_seg, xsegs, st))
     return -3;
+  mark("s2m items");
   // ---- dense-algebra launches
   const int w_sq = ggs_tile_width(kp, kp), w_kn = ggs_tile_width(kp, np), w_nk = ggs_tile_width(np, kp);
   if (make_launch(P, P.g_s2m, sgroup, w_kn, st) || make_launch(P, P.g_x, xgroup, w_kn, st) ||
@@ -512,39 +565,46 @@ int build_schedules(Plan& P, cudaStream_t st) {
     const int mask_min = mask_min_env >= 0 ? mask_min_env : 256;
     struct SibGroup { int b, cls, mask, cnt; int src[8]; };
     std::vector<SibGroup> sgs;
+    sgs.reserve(V.size() / 4 + 16);
     std::vector<int> mcount(kSib * 256, 0);
-    int ap[3], aq[3];
+    // integer anchors of every box (its coordinates at its own level), once
+    std::vector<int> anc(3 * (size_t)nb);
+#pragma omp parallel for schedule(static)
+    for (int b = 0; b < nb; ++b) anchor(b, &anc[3 * (size_t)b]);
     for (int b = 0; b < nb; ++b) {
       const int e0 = vcnt[b], e1 = vcnt[b + 1];
       if (e0 == e1 || !inD(b)) continue;
       P.nV_local += e1 - e0;
       for (int e = e0; e < e1; ++e)  // algorithmic flops: 2 k^2 (dense core) or 4 k r_o (stage 2)
         P.m2l_flops += P.lr.on ? 4.0 * P.k * P.tables.ranks[vby[e].z] : 2.0 * P.k * P.k;
-      anchor(T.parent[b], ap);
+      const int* ap = &anc[3 * (size_t)T.parent[b]];
       const int a = (int)(T.key[b] & 7);
-      // distinct source parents (<= 26)
-      int qs[27], nq = 0;
+      // one group per distinct source parent Q (<= 26; Q's offset from parent(b) identifies
+      // it), in order of first appearance
+      SibGroup gq[27];
+      int order[27], nq = 0;
+      bool used[27] = {};
       for (int e = e0; e < e1; ++e) {
-        int q = T.parent[vby[e].y];
-        bool seen = false;
-        for (int i = 0; i < nq; ++i) seen |= qs[i] == q;
-        if (!seen) qs[nq++] = q;
+        const int src = vby[e].y;
+        const int* aq = &anc[3 * (size_t)T.parent[src]];
+        const int lin = (aq[0] - ap[0] + 1) * 9 + (aq[1] - ap[1] + 1) * 3 + (aq[2] - ap[2] + 1);
+        if (!used[lin]) {
+          used[lin] = true;
+          order[nq++] = lin;
+          gq[lin] = SibGroup{b, (lin < 13 ? lin : lin - 1) * 8 + a, 0, 0, {-1, -1, -1, -1, -1, -1, -1, -1}};
+        }
+        SibGroup& g = gq[lin];
+        const int cb = (int)(T.key[src] & 7);
+        g.src[cb] = src;
+        g.mask |= 1 << cb;
+        ++g.cnt;
       }
       for (int i = 0; i < nq; ++i) {
-        anchor(qs[i], aq);
-        const int lin = (aq[0] - ap[0] + 1) * 9 + (aq[1] - ap[1] + 1) * 3 + (aq[2] - ap[2] + 1);
-        SibGroup g{b, (lin < 13 ? lin : lin - 1) * 8 + a, 0, 0, {-1, -1, -1, -1, -1, -1, -1, -1}};
-        for (int e = e0; e < e1; ++e)
-          if (T.parent[vby[e].y] == qs[i]) {
-            const int cb = (int)(T.key[vby[e].y] & 7);
-            g.src[cb] = vby[e].y;
-            g.mask |= 1 << cb;
-            ++g.cnt;
-          }
-        ++mcount[g.cls * 256 + g.mask];
-        sgs.push_back(g);
+        ++mcount[gq[order[i]].cls * 256 + gq[order[i]].mask];
+        sgs.push_back(gq[order[i]]);
       }
     }
+    mark("m2l groups");
     std::vector<int> full_mask(kSib, 0);
     for (int c = 0; c < kSib; ++c)
       for (int j = 0; j < classes[c * 17]; ++j) full_mask[c] |= 1 << classes[c * 17 + 1 + j];
@@ -599,6 +659,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
         }
       }
     }
+    mark("m2l classes");
     if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
     if (std::getenv("KIFMM_DEBUG_M2L")) {  // diagnostics: columns per class kind
       int64_t full = 0, masked = 0, pseudo = 0;
@@ -631,12 +692,14 @@ int build_schedules(Plan& P, cudaStream_t st) {
       std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
         return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
       });
+    mark("m2l tiles");
     P.g_m2l_sib.ntiles = (int)tiles.size();
     P.g_m2l_sib.ncols = (int)cols.size() / 9;
     if (upload(P, &P.g_m2l_sib.d_tiles, tiles, st) || upload(P, &P.g_m2l_sib.d_cols, cols, st) ||
         upload(P, &P.g_m2l_sib.d_classes, classes, st) || upload(P, &P.g_m2l_sib.d_counter, std::vector<int>(1, 0), st))
       return -3;
   }
+  mark("m2l schedule");
   // M2M per child level (finest first) and L2L per parent level (coarsest first), by octant
   P.g_m2m.clear();
   P.g_l2l.clear();
@@ -688,6 +751,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     std::vector<int> sl = Dp.nranks > 1 ? Dp.straddle : std::vector<int>();
     if (upload(P, &P.d_straddle, sl, st) || zalloc(&P.d_straddle_buf, (size_t)P.n_straddle * kp)) return -3;
   }
+  mark("m2m/l2l+buffers");
   // X-list operators (after S2M / L2T, same reserve; BEM: always, its runtime integrals are slow)
   {
     int64_t xcnt = 0;
@@ -715,6 +779,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     }
   }
   if (P.leaf_x && build_x_ops(P, st)) return -3;
+  mark("x operators");
   if (P.leaf_s2m || P.leaf_l2t) {
     const size_t cnt = (size_t)(Dp.own_hi - Dp.own_lo) * kp;
     if (P.leaf_s2m && zalloc(&P.d_s2m_mat, cnt)) return -3;
@@ -722,6 +787,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     P.leaf_op_bytes += (int64_t)((P.leaf_s2m ? 1 : 0) + (P.leaf_l2t ? 1 : 0)) * cnt * sizeof(double);
     if (build_leaf_ops(P, st)) return -3;
   }
+  mark("leaf operators");
   KIFMM_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
