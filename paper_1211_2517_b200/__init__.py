@@ -286,22 +286,35 @@ class Plan:
         out["phase_ms"] = dict(zip(PHASES, list(inf.phase_ms)))
         return out
 
+    def _check_vec(self, t, n: int, what: str):
+        """t must be a contiguous float64 tensor of n elements on this plan's device: the C
+        ABI reads / writes exactly n doubles through the raw pointer."""
+        import torch
+        if not (isinstance(t, torch.Tensor) and t.device == self.points.device and t.dtype == torch.float64
+                and t.is_contiguous() and t.numel() == n):
+            raise TypeError(f"{what} must be a contiguous float64 tensor of {n} elements on {self.points.device}")
+
     def matvec(self, density=None, out=None, stream=None):
         import torch
         if out is None:
             out = torch.empty(self.N, dtype=torch.float64, device=self.points.device)
+        self._check_vec(out, self.N, "out")
         dptr = None
         if density is not None:
-            if not (density.is_cuda and density.dtype == torch.float64 and density.is_contiguous()):
-                raise TypeError("density must be a contiguous CUDA float64 tensor")
+            self._check_vec(density, self.N, "density")
             dptr = ctypes.c_void_p(density.data_ptr())
         _check(lib().fmm_matvec(self._h, dptr, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)), "fmm_matvec")
         return out
 
     def matvec_host(self, density: np.ndarray, out: np.ndarray | None = None, stream=None) -> np.ndarray:
         density = np.ascontiguousarray(density, dtype=np.float64)
+        if density.shape != (self.N,):
+            raise ValueError(f"density must have shape ({self.N},)")
         if out is None:
             out = np.empty(self.N, dtype=np.float64)
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (self.N,)
+                and out.flags.c_contiguous and out.flags.writeable):
+            raise TypeError(f"out must be a writeable contiguous float64 array of shape ({self.N},)")
         _check(lib().fmm_matvec_host(self._h, density.ctypes.data, out.ctypes.data, _stream_ptr(stream)),
                "fmm_matvec_host")
         return out
@@ -318,9 +331,8 @@ class Plan:
         lo, hi = self.owned_range
         if out is None:
             out = torch.empty(hi - lo, dtype=torch.float64, device=self.points.device)
-        if not (density_owned.is_cuda and density_owned.dtype == torch.float64 and density_owned.is_contiguous()
-                and density_owned.numel() == hi - lo):
-            raise TypeError("density_owned must be a contiguous CUDA float64 tensor of the owned length")
+        self._check_vec(density_owned, hi - lo, "density_owned")
+        self._check_vec(out, hi - lo, "out")
         _check(lib().fmm_matvec_owned(self._h, ctypes.c_void_p(density_owned.data_ptr()),
                                       ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)), "fmm_matvec_owned")
         return out
@@ -332,6 +344,9 @@ class Plan:
             raise ValueError("density_owned must have the owned length")
         if out is None:
             out = np.empty(hi - lo, dtype=np.float64)
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (hi - lo,)
+                and out.flags.c_contiguous and out.flags.writeable):
+            raise TypeError("out must be a writeable contiguous float64 array of the owned length")
         _check(lib().fmm_matvec_owned_host(self._h, density_owned.ctypes.data, out.ctypes.data, _stream_ptr(stream)),
                "fmm_matvec_owned_host")
         return out
@@ -340,8 +355,9 @@ class Plan:
         """Solve (this plan's operator) x = rhs by restarted GMRES on the device (fmm_gmres).
         Returns (x, info) with info = {iters, relres, t_matvec_ms}."""
         import torch
-        if not (rhs.is_cuda and rhs.dtype == torch.float64 and rhs.is_contiguous() and rhs.numel() == self.N):
-            raise TypeError("rhs must be a contiguous CUDA float64 tensor of length N")
+        self._check_vec(rhs, self.N, "rhs")
+        if x0 is not None:
+            self._check_vec(x0.contiguous(), self.N, "x0")
         x = torch.zeros_like(rhs) if x0 is None else x0.clone().contiguous()
         it, rr, tm = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
         _check(lib().fmm_gmres(self._h, ctypes.c_void_p(rhs.data_ptr()), ctypes.c_void_p(x.data_ptr()), restart,
@@ -406,6 +422,15 @@ def fmm_matvec_group(plans: list, densities: list, potentials: list | None = Non
         for pl in plans:
             lo, hi = pl.owned_range
             potentials.append(torch.empty(hi - lo if owned else pl.N, dtype=torch.float64, device=pl.points.device))
+    if len(densities) != n or len(potentials) != n:
+        raise ValueError("one density and one potential per plan")
+    for pl, d_, p_ in zip(plans, densities, potentials):
+        lo, hi = pl.owned_range
+        m = hi - lo if owned else pl.N
+        if d_ is not None and d_.numel():
+            pl._check_vec(d_, m, "density")
+        if p_.numel():
+            pl._check_vec(p_, m, "potential")
     vp = ctypes.c_void_p
     hs = (vp * n)(*[pl._h.value for pl in plans])
     ds = (vp * n)(*[d.data_ptr() if d is not None and d.numel() else None for d in densities])

@@ -70,6 +70,18 @@ int check(ncclResult_t r, const char* what) {
     if (int rc_ = check((call), #call)) return rc_; \
   } while (0)
 
+// inside ncclGroupStart / ncclGroupEnd: an error closes the group before returning, so
+// the thread is not left with an open NCCL group (the first error's message is kept)
+#define KIFMM_NCCL_IN_GROUP(call)                \
+  do {                                           \
+    if (int rc_ = check((call), #call)) {        \
+      const std::string msg_ = last_error();     \
+      api().GroupEnd();                          \
+      set_error(msg_);                           \
+      return rc_;                                \
+    }                                            \
+  } while (0)
+
 int need_comm(Plan& P) {
   if (!P.nccl_comm) {
     set_error("plan has nranks > 1 but no NCCL communicator (loopback plans run through fmm_matvec_group)");
@@ -118,8 +130,8 @@ int nccl_exchange(Plan& P, Exchange& X, cudaStream_t st) {
     if (s == P.dist.rank) continue;
     const size_t ns = (size_t)(X.send_off[s + 1] - X.send_off[s]) * X.row;
     const size_t nr = (size_t)(X.recv_off[s + 1] - X.recv_off[s]) * X.row;
-    if (ns) KIFMM_NCCL(A.Send(X.d_send + (size_t)X.send_off[s] * X.row, ns, ncclFloat64, s, c, st));
-    if (nr) KIFMM_NCCL(A.Recv(X.d_recv + (size_t)X.recv_off[s] * X.row, nr, ncclFloat64, s, c, st));
+    if (ns) KIFMM_NCCL_IN_GROUP(A.Send(X.d_send + (size_t)X.send_off[s] * X.row, ns, ncclFloat64, s, c, st));
+    if (nr) KIFMM_NCCL_IN_GROUP(A.Recv(X.d_recv + (size_t)X.recv_off[s] * X.row, nr, ncclFloat64, s, c, st));
   }
   KIFMM_NCCL(A.GroupEnd());
   return 0;
@@ -143,8 +155,8 @@ int nccl_allgather_ranges(Plan& P, double* buf, cudaStream_t st) {
   for (int s = 0; s < D.nranks; ++s) {
     if (s == D.rank) continue;
     const size_t theirs = (size_t)(D.bnd[s + 1] - D.bnd[s]);
-    if (mine) KIFMM_NCCL(A.Send(buf + D.own_lo, mine, ncclFloat64, s, c, st));
-    if (theirs) KIFMM_NCCL(A.Recv(buf + D.bnd[s], theirs, ncclFloat64, s, c, st));
+    if (mine) KIFMM_NCCL_IN_GROUP(A.Send(buf + D.own_lo, mine, ncclFloat64, s, c, st));
+    if (theirs) KIFMM_NCCL_IN_GROUP(A.Recv(buf + D.bnd[s], theirs, ncclFloat64, s, c, st));
   }
   KIFMM_NCCL(A.GroupEnd());
   return 0;

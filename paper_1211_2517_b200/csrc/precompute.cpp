@@ -4,10 +4,10 @@
 // All operators at unit halfwidth (homogeneous kernel of degree -1);
 // the level factors live in the matvec (reading Q15).
 //   surfaces  P:109-113  UE, DC at (1+d); UC, DE at (3-2d); p points per edge
-//   E_u, E_d  P:126-154  equivalent-density solves, pinv by one-sided Jacobi SVD
+//   E_u, E_d  P:126-154  equivalent-density solves, pinv by one-sided Jacobi SVD (extended precision)
 //   K_delta   P:136-144  K_ij = G(x_i, y_j), x = DC(target @ 0), y = UE(source @ 2 delta)
 //   basis U   P:172-203  leading left singular vectors of K_fat (= those of K_thin,
-//                        P:199-203) from a cyclic-Jacobi eigensolve of K_fat K_fat^T
+//                        P:199-203): Householder QR of K_fat^T, Jacobi SVD of R
 //   C_delta   P:216-223  U^T K_delta U
 //   S', T'    P:341, P:351   S' = U^T pinv(E_u), T' = pinv(E_d) U (fused, reading Q17)
 //   M~_o, L~_o P:337, P:347  U^T pinv(E_u) G(UC, UE_child) U,  U^T G(DC_child, DE) pinv(E_d) U
@@ -78,64 +78,150 @@ Mat transpose(const Mat& A, int m, int n) {
   return T;
 }
 
-// Moore-Penrose pseudo-inverse by one-sided (Hestenes) Jacobi SVD of a square A;
-// singular values <= rcond * sigma_max are dropped (reading Q11).
-Mat pinv_jacobi(const Mat& A, int n, double rcond) {
-  // work on columns: W = A (n x n, column j = W[:, j]); V accumulates rotations
-  Mat W = transpose(A, n, n);  // row c of W = column c of A
-  Mat V((size_t)n * n, 0.0);
-  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    double off = 0;
-    for (int i = 0; i < n - 1; ++i)
-      for (int j = i + 1; j < n; ++j) {
-        double* wi = &W[(size_t)i * n];
-        double* wj = &W[(size_t)j * n];
-        double al = 0, be = 0, ga = 0;
+// One-sided (Hestenes) Jacobi on the columns of a square n x n A, in x87 extended
+// precision (long double, 64-bit significand): rotations J with A J = W (orthogonal
+// columns), V = J^T.  On return row c of W is column c of A J (= sigma_c u_c) and row c
+// of V is the right singular vector v_c; sig[c] = |W_c| (unsorted).
+//
+// Why extended precision: E_u and E_d keep singular values down to 1e-10 sigma_max at
+// p = 8, and the kept small singular vectors carry the rounding of every rotation that
+// mixed them with the large ones (absolute ~eps sigma_max, relative eps / 1e-10).  In
+// double that moved the p = 8 matvec by 1.4e-7 from the oracle's tables (SURVEY
+// §8(c.5)(4) bound: 1e-7); in extended precision by ~6e-9, the floor that one-ulp
+// differences in E itself set.  Pairs are visited in round-robin (tournament) order:
+// each round's n/2 disjoint column pairs rotate in parallel.
+using LMat = std::vector<long double>;
+void jacobi_onesided_ld(const Mat& A, int n, LMat& W, LMat& V, std::vector<long double>& sig) {
+  using R = long double;
+  const int m = n + (n & 1);  // an odd n gets a dummy column that pairs with nothing
+  W.assign((size_t)n * n, 0.0L);
+  V.assign((size_t)n * n, 0.0L);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) W[(size_t)j * n + i] = A[(size_t)i * n + j];
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0L;
+  std::vector<int> ring(m);
+  for (int i = 0; i < m; ++i) ring[i] = i;
+  const R tol = 1e-17L;  // ~100 eps of the extended format
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    R off = 0;
+    for (int round = 0; round < m - 1; ++round) {
+#pragma omp parallel for schedule(static) reduction(max : off)
+      for (int h = 0; h < m / 2; ++h) {
+        int i = ring[h], j = ring[m - 1 - h];
+        if (i >= n || j >= n) continue;
+        if (i > j) std::swap(i, j);
+        R* wi = &W[(size_t)i * n];
+        R* wj = &W[(size_t)j * n];
+        R al = 0, be = 0, ga = 0;
         for (int r = 0; r < n; ++r) { al += wi[r] * wi[r]; be += wj[r] * wj[r]; ga += wi[r] * wj[r]; }
-        if (ga == 0.0) continue;
-        double rel = std::fabs(ga) / std::sqrt(al * be);
+        if (ga == 0 || al == 0 || be == 0) continue;
+        const R rel = std::fabs(ga) / std::sqrt(al * be);
         off = std::max(off, rel);
-        if (rel < 1e-15) continue;
-        double zeta = (be - al) / (2.0 * ga);
-        double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+        if (rel < tol) continue;
+        const R zeta = (be - al) / (2 * ga);
+        const R t = (zeta >= 0 ? 1 : -1) / (std::fabs(zeta) + std::sqrt(1 + zeta * zeta));
+        const R c = 1 / std::sqrt(1 + t * t), s = c * t;
         for (int r = 0; r < n; ++r) {
-          double x = wi[r], y = wj[r];
+          const R x = wi[r], y = wj[r];
           wi[r] = c * x - s * y;
           wj[r] = s * x + c * y;
         }
-        double* vi = &V[(size_t)i * n];
-        double* vj = &V[(size_t)j * n];
+        R* vi = &V[(size_t)i * n];
+        R* vj = &V[(size_t)j * n];
         for (int r = 0; r < n; ++r) {
-          double x = vi[r], y = vj[r];
+          const R x = vi[r], y = vj[r];
           vi[r] = c * x - s * y;
           vj[r] = s * x + c * y;
         }
       }
-    if (off < 1e-15) break;
+      std::rotate(ring.begin() + 1, ring.end() - 1, ring.end());  // position 0 stays fixed
+    }
+    if (off < tol) break;
   }
-  // sigma_c = |W_c|, u_c = W_c / sigma_c; A = sum_c sigma_c u_c v_c^T with v_c = row c of V
-  std::vector<double> sig(n);
-  double smax = 0;
+  sig.assign(n, 0.0L);
   for (int c = 0; c < n; ++c) {
-    double s2 = 0;
+    R s2 = 0;
     for (int r = 0; r < n; ++r) s2 += W[(size_t)c * n + r] * W[(size_t)c * n + r];
     sig[c] = std::sqrt(s2);
-    smax = std::max(smax, sig[c]);
   }
+}
+
+// Moore-Penrose pseudo-inverse of a square A from its Jacobi SVD; singular values
+// <= rcond * sigma_max are dropped (reading Q11).
+Mat pinv_jacobi(const Mat& A, int n, double rcond) {
+  using R = long double;
+  LMat W, V;
+  std::vector<R> sig;
+  jacobi_onesided_ld(A, n, W, V, sig);
+  const R smax = *std::max_element(sig.begin(), sig.end());
   // pinv = sum_c v_c u_c^T / sigma_c = sum_c v_c W_c^T / sigma_c^2
   Mat P((size_t)n * n, 0.0);
 #pragma omp parallel for schedule(static)
-  for (int i = 0; i < n; ++i)
+  for (int i = 0; i < n; ++i) {
+    std::vector<R> row(n, 0.0L);
     for (int c = 0; c < n; ++c) {
-      if (!(sig[c] > rcond * smax)) continue;
-      double f = V[(size_t)c * n + i] / (sig[c] * sig[c]);
-      const double* w = &W[(size_t)c * n];
-      double* pr = &P[(size_t)i * n];
-      for (int j = 0; j < n; ++j) pr[j] += f * w[j];
+      if (!(sig[c] > (R)rcond * smax)) continue;
+      const R f = V[(size_t)c * n + i] / (sig[c] * sig[c]);
+      const R* w = &W[(size_t)c * n];
+      for (int j = 0; j < n; ++j) row[j] += f * w[j];
     }
+    for (int j = 0; j < n; ++j) P[(size_t)i * n + j] = (double)row[j];
+  }
   return P;
+}
+
+// Left singular vectors and singular values of K_fat = [K_0 K_1 ... K_315] (n x 316n,
+// eq. fat), descending.  Householder QR of K_fat^T = Q R (316n x n, column
+// by column, trailing columns updated in parallel), then the one-sided Jacobi SVD of the
+// n x n R: R = W Sigma V^T gives K_fat = V Sigma (Q W)^T, so U = V.  Backward stable in
+// K_fat itself: the kept subspace is accurate to eps sigma_1 / (sigma_k - sigma_k+1)
+// (1e-11 at p = 6), where an eigensolve of the Gram K_fat K_fat^T (squared condition)
+// gets eps sigma_1^2 / (sigma_k^2 - sigma_k+1^2) (2e-7 at p = 6).
+void kfat_svd(const std::vector<Mat>& K, int n, std::vector<double>& sigma, Mat& vec) {
+  const size_t m = (size_t)K.size() * n;
+  // column a of K_fat^T = row a of K_fat = (K_0[a, :], K_1[a, :], ...)
+  std::vector<Mat> col(n, Mat(m));
+#pragma omp parallel for schedule(static)
+  for (int a = 0; a < n; ++a)
+    for (size_t o = 0; o < K.size(); ++o)
+      std::memcpy(&col[a][o * n], &K[o][(size_t)a * n], sizeof(double) * n);
+  Mat Rm((size_t)n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double* x = col[j].data() + j;
+    const size_t len = m - j;
+    double nrm2 = 0;
+    for (size_t r = 0; r < len; ++r) nrm2 += x[r] * x[r];
+    const double alpha = x[0] >= 0 ? -std::sqrt(nrm2) : std::sqrt(nrm2);
+    // v = x - alpha e_1 (stored in place), H = I - 2 v v^T / (v^T v)
+    const double v0 = x[0] - alpha;
+    const double vtv = nrm2 - x[0] * x[0] + v0 * v0;
+    x[0] = v0;
+    if (vtv > 0) {
+#pragma omp parallel for schedule(static)
+      for (int c = j + 1; c < n; ++c) {
+        double* y = col[c].data() + j;
+        double s = 0;
+        for (size_t r = 0; r < len; ++r) s += x[r] * y[r];
+        const double f = 2.0 * s / vtv;
+        for (size_t r = 0; r < len; ++r) y[r] -= f * x[r];
+      }
+    }
+    Rm[(size_t)j * n + j] = alpha;
+    for (int c = j + 1; c < n; ++c) Rm[(size_t)j * n + c] = col[c][j];
+  }
+  col.clear();
+  LMat W, V;
+  std::vector<long double> sig;
+  jacobi_onesided_ld(Rm, n, W, V, sig);
+  std::vector<int> idx(n);
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return sig[a] > sig[b]; });
+  sigma.resize(n);
+  vec.assign((size_t)n * n, 0.0);
+  for (int c = 0; c < n; ++c) {
+    sigma[c] = (double)sig[idx[c]];
+    for (int r = 0; r < n; ++r) vec[(size_t)r * n + c] = (double)V[(size_t)idx[c] * n + r];
+  }
 }
 
 // SVD of a square n x n A by one-sided (Hestenes) Jacobi: A = sum_c s_c u_c v_c^T,
@@ -196,54 +282,6 @@ void svd_jacobi(const Mat& A, int n, std::vector<double>& s, Mat& u, Mat& v) {
   }
 }
 
-// Cyclic Jacobi eigendecomposition of a symmetric n x n matrix. Returns
-// eigenvalues descending; column c of `vec` (row-major n x n) is eigenvector c.
-void jacobi_eig(Mat A, int n, std::vector<double>& val, Mat& vec) {
-  Mat V((size_t)n * n, 0.0);
-  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
-  double scale = 0;
-  for (int i = 0; i < n; ++i) scale = std::max(scale, std::fabs(A[(size_t)i * n + i]));
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0;
-    for (int p = 0; p < n - 1; ++p)
-      for (int q = p + 1; q < n; ++q) off = std::max(off, std::fabs(A[(size_t)p * n + q]));
-    if (off <= 1e-18 * scale) break;
-    for (int p = 0; p < n - 1; ++p)
-      for (int q = p + 1; q < n; ++q) {
-        double apq = A[(size_t)p * n + q];
-        if (std::fabs(apq) <= 1e-300) continue;
-        double app = A[(size_t)p * n + p], aqq = A[(size_t)q * n + q];
-        double theta = (aqq - app) / (2.0 * apq);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
-        double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
-        for (int r = 0; r < n; ++r) {  // columns p, q
-          double arp = A[(size_t)r * n + p], arq = A[(size_t)r * n + q];
-          A[(size_t)r * n + p] = c * arp - s * arq;
-          A[(size_t)r * n + q] = s * arp + c * arq;
-        }
-        for (int r = 0; r < n; ++r) {  // rows p, q
-          double apr = A[(size_t)p * n + r], aqr = A[(size_t)q * n + r];
-          A[(size_t)p * n + r] = c * apr - s * aqr;
-          A[(size_t)q * n + r] = s * apr + c * aqr;
-        }
-        for (int r = 0; r < n; ++r) {
-          double vrp = V[(size_t)r * n + p], vrq = V[(size_t)r * n + q];
-          V[(size_t)r * n + p] = c * vrp - s * vrq;
-          V[(size_t)r * n + q] = s * vrp + c * vrq;
-        }
-      }
-  }
-  std::vector<int> idx(n);
-  for (int i = 0; i < n; ++i) idx[i] = i;
-  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return A[(size_t)a * n + a] > A[(size_t)b * n + b]; });
-  val.resize(n);
-  vec.assign((size_t)n * n, 0.0);
-  for (int c = 0; c < n; ++c) {
-    val[c] = A[(size_t)idx[c] * n + idx[c]];
-    for (int r = 0; r < n; ++r) vec[(size_t)r * n + c] = V[(size_t)r * n + idx[c]];
-  }
-}
-
 }  // namespace
 
 int build_tables(int p, int k, double d, double rcond, HostTables* out) {
@@ -266,24 +304,9 @@ int build_tables(int p, int k, double d, double rcond, HostTables* out) {
         const double cb[3] = {2.0 * i, 2.0 * j, 2.0 * l};
         K[id++] = kmat(g, n, fin, zero, fin, cb);
       }
-  Mat gram((size_t)n * n, 0.0);
-#pragma omp parallel for schedule(dynamic, 4)
-  for (int a = 0; a < n; ++a)
-    for (int b = 0; b <= a; ++b) {
-      double s = 0;
-      for (int o = 0; o < kNumOffsets; ++o) {
-        const double* ra = &K[o][(size_t)a * n];
-        const double* rb = &K[o][(size_t)b * n];
-        for (int c = 0; c < n; ++c) s += ra[c] * rb[c];
-      }
-      gram[(size_t)a * n + b] = s;
-      gram[(size_t)b * n + a] = s;
-    }
-  std::vector<double> lam;
+  std::vector<double> sigma;
   Mat vec;
-  jacobi_eig(gram, n, lam, vec);
-  std::vector<double> sigma(n);
-  for (int i = 0; i < n; ++i) sigma[i] = std::sqrt(std::max(lam[i], 0.0));
+  kfat_svd(K, n, sigma, vec);
   // k_eff: smallest k' >= k with sigma_k' - sigma_k'+1 > 1e-8 sigma_1 (reading Q12)
   int kk = std::min(k, n);
   while (kk < n && !(sigma[kk - 1] - sigma[kk] > 1e-8 * sigma[0])) ++kk;

@@ -5,6 +5,9 @@
 //   8 arrays as (u64 count, count x f64): sigma (n), surf (3n), U (n k), C (316 k k),
 //   S (k n), T (n k), M (8 k k), L (8 k k),
 //   u64 FNV-1a hash of every array byte (corruption check).
+#include <unistd.h>
+
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -38,8 +41,12 @@ struct File {
 
 }  // namespace
 
+// Written to a temporary file unique to this process and call, then renamed over `path`
+// (rename is atomic): several ranks that compute the same tables at once each publish a
+// complete file, and the last rename wins.
 int save_tables(const HostTables& H, int k_req, const std::string& path) {
-  const std::string tmp = path + ".tmp";
+  static std::atomic<unsigned> serial{0};
+  const std::string tmp = path + ".tmp." + std::to_string((long)getpid()) + "." + std::to_string(serial++);
   File fl;
   fl.f = std::fopen(tmp.c_str(), "wb");
   if (!fl.f) {
@@ -87,8 +94,12 @@ int load_tables(const std::string& path, HostTables* H, int* k_req) {
               std::to_string(bom) + " (expected " + std::to_string(kVersion) + ", little-endian)");
     return -1;
   }
-  if (std::fread(hdr, 4, 4, fl.f) != 4 || std::fread(dd, 8, 2, fl.f) != 2 || hdr[0] < 2 || hdr[1] < 1 || hdr[2] < 1 ||
-      hdr[2] > hdr[1]) {
+  // the header must describe tables this library builds (2 <= p <= 8, n = 6(p-1)^2 + 2,
+  // 1 <= k <= n): array sizes are derived from it, so a corrupt header is refused
+  // before anything is allocated
+  if (std::fread(hdr, 4, 4, fl.f) != 4 || std::fread(dd, 8, 2, fl.f) != 2 || hdr[0] < 2 || hdr[0] > 8 ||
+      hdr[1] != 6 * (hdr[0] - 1) * (hdr[0] - 1) + 2 || hdr[2] < 1 || hdr[2] > hdr[1] || hdr[3] < 1 ||
+      hdr[3] > hdr[1]) {
     set_error("operator file: " + path + " has a corrupt header");
     return -1;
   }

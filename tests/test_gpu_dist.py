@@ -26,6 +26,14 @@ TOL = 1e-11
 def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
+def par(a, b):
+    """Parity measure: the larger of the relative L2 error and the per-element max error
+    relative to max|b| (a single wrong element cannot hide in the L2 norm)."""
+    a, b = np.asarray(a), np.asarray(b)
+    l2 = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    return max(l2, float(np.abs(a - b).max() / np.abs(b).max()))
+
+
 
 def K():
     import paper_1211_2517_b200 as K
@@ -97,16 +105,16 @@ def test_loopback_group_parity(case, R, wx, leaf_ops):
     assert rng[0][0] == 0 and rng[-1][1] == q.size
     assert all(rng[i][1] == rng[i + 1][0] for i in range(R - 1))
     out = run_owned(plans, q)
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL
     # replicated mode: full caller-order density in, full potential out on every rank
     Q = torch.from_numpy(q).cuda()
     pots = K().fmm_matvec_group(plans, [Q] * R, owned=False)
     for pt in pots:
-        assert rel(pt.cpu().numpy(), ref) <= TOL
+        assert par(pt.cpu().numpy(), ref) <= TOL
     # and the partitioned result is the single-GPU result up to summation order
     one = K().Plan(torch.from_numpy(pts).cuda(), None, p=p, k=k, leaf_size=s, wx_direct_max=wx, tables=tb,
                    leaf_ops=leaf_ops)
-    assert rel(out, one.matvec(Q).cpu().numpy()) <= 1e-13
+    assert par(out, one.matvec(Q).cpu().numpy()) <= 1e-13
 
 
 def test_loopback_ghost_traffic_and_info():
@@ -133,13 +141,13 @@ def test_loopback_more_ranks_than_leaves_and_c2():
     ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
     plans = group(pts, 4, 24, 64, 12, tb)
     assert any(pl.owned_range[0] == pl.owned_range[1] for pl in plans)
-    assert rel(run_owned(plans, q), ref) <= TOL
+    assert par(run_owned(plans, q), ref) <= TOL
     # BASELINE configs[1] at full size over two loopback ranks
     pts, q, cfg = synth_inputs.make("C2")
     tb = tables(cfg["p"], cfg["k"])
     ref = oracle.Plan(pts, cfg["leaf"], tb["n"]).matvec(tb, q)
     plans = group(pts, cfg["p"], cfg["k"], cfg["leaf"], 2, tb)
-    assert rel(run_owned(plans, q), ref) <= TOL
+    assert par(run_owned(plans, q), ref) <= TOL
 
 
 def test_loopback_plan_rejects_single_matvec():
@@ -159,15 +167,15 @@ def test_nccl_transport_one_rank():
     assert len(uid) == 128
     pl = K().Plan(torch.from_numpy(pts).cuda(), None, p=p, k=k, leaf_size=s, tables=tb, nranks=1, rank=0, nccl_id=uid)
     Q = torch.from_numpy(q).cuda()
-    assert rel(pl.matvec(Q).cpu().numpy(), ref) <= TOL
+    assert par(pl.matvec(Q).cpu().numpy(), ref) <= TOL
     lo, hi = pl.owned_range
     assert (lo, hi) == (0, q.size)
     perm = pl.export_tree()["perm"]
     po = pl.matvec_owned(torch.from_numpy(q[perm].copy()).cuda()).cpu().numpy()
     out = np.empty_like(po)
     out[perm] = po
-    assert rel(out, ref) <= TOL
-    assert rel(pl.matvec_owned_host(q[perm])[np.argsort(perm)], ref) <= TOL
+    assert par(out, ref) <= TOL
+    assert par(pl.matvec_owned_host(q[perm])[np.argsort(perm)], ref) <= TOL
 
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k"])
@@ -179,4 +187,4 @@ def test_loopback_stage2(case):
     dev = torch.device("cuda:0")
     P = torch.from_numpy(pts).to(dev)
     plans = [K().Plan(P, None, p=p, k=k, leaf_size=s, tables=tb, m2l_c2=1.0, nranks=3, rank=r) for r in range(3)]
-    assert rel(run_owned(plans, q), ref) <= TOL
+    assert par(run_owned(plans, q), ref) <= TOL

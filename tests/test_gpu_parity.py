@@ -23,6 +23,14 @@ TOL = 1e-11
 def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
+def par(a, b):
+    """Parity measure: the larger of the relative L2 error and the per-element max error
+    relative to max|b| (a single wrong element cannot hide in the L2 norm)."""
+    a, b = np.asarray(a), np.asarray(b)
+    l2 = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    return max(l2, float(np.abs(a - b).max() / np.abs(b).max()))
+
+
 
 def K():
     import paper_1211_2517_b200 as K
@@ -95,11 +103,11 @@ def test_matvec_parity_shared_tables(case, wx, leaf_ops):
     gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb, leaf_ops=leaf_ops)
     assert (gp.info["leaf_op_bytes"] > 0) == bool(leaf_ops)
     out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL
     # split near / far passes (phase exports)
     gp = gpu_plan(pts, p, k, s, wx=wx, tb=tb, split_phases=True, leaf_ops=leaf_ops)
     out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL
     # per-phase parity localises failures.  q^' and l^ are intermediate: S' = U^T pinv(E_u)
     # has entries ~1e3-1e8 x those of q^ at p = 8 (cond E_u 4e11), so summation-order
     # rounding in them is amplified in directions the later steps annihilate; the
@@ -108,10 +116,10 @@ def test_matvec_parity_shared_tables(case, wx, leaf_ops):
     for name in ("qhat", "lhat"):
         a, b = gp.export_phase(name), ph[name]
         if np.linalg.norm(b) > 0:
-            assert rel(a, b) <= amp * TOL, name
-    assert rel(gp.export_phase("near"), ph["near"]) <= TOL
+            assert par(a, b) <= amp * TOL, name
+    assert par(gp.export_phase("near"), ph["near"]) <= TOL
     if np.linalg.norm(ph["far"]) > 0:
-        assert rel(gp.export_phase("far"), ph["far"]) <= TOL
+        assert par(gp.export_phase("far"), ph["far"]) <= TOL
 
 
 @pytest.mark.parametrize("case", list(CASES))
@@ -140,7 +148,7 @@ def test_c2_full_size_parity(leaf_ops):
     gp = gpu_plan(pts, cfg["p"], cfg["k"], cfg["leaf"], tb=tb, leaf_ops=leaf_ops)
     out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
     assert gp.info["nlevels"] == 6 and gp.info["nleaves"] == 32768
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL
     # accuracy vs the direct sum on a seeded sample of targets
     idx = np.random.default_rng(0).choice(pts.shape[0], 2048, replace=False)
     d = oracle.direct(pts, q, idx)
@@ -157,16 +165,18 @@ def test_accuracy_vs_direct_within_oracle_error():
         assert rel(out, d) <= rel(ref, d) + 1e-12
 
 
-@pytest.mark.parametrize("p,k,bound", [(4, 24, 1e-10), (6, 60, 1e-7), (8, 100, 1e-5)])
+@pytest.mark.parametrize("p,k,bound", [(4, 24, 1e-12), (6, 60, 1e-9), (8, 100, 1e-7)])
 def test_own_precompute_within_intrinsic_bound(p, k, bound):
-    # independent precomputes differ by the basis sensitivity
+    # the library's own tables (no `tables=`) against the oracle on its tables: the
+    # intrinsic table-sensitivity bound of SURVEY §8(c.5)(4) (C1, measured on the host
+    # through the oracle: 1.1e-13 / 4.4e-10 / 5.6e-9; tests/test_own_precompute.py)
     pts, q, _ = synth_inputs.make("C1")
     tb = tables(p, k)
     ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
     out = gpu_plan(pts, p, k, 64).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-    assert rel(out, ref) <= bound
+    assert par(out, ref) <= bound
     d = oracle.direct(pts, q)
-    assert rel(out, d) <= 2 * rel(ref, d) + 1e-12
+    assert rel(out, d) <= 1.02 * rel(ref, d)
 
 
 def test_edge_cases():
@@ -178,7 +188,12 @@ def test_edge_cases():
                    (np.array([[0.0, 0, 0], [0.0, 0, 0], [0.0, 3.0, 4.0]]), np.array([1.0, 2.0, 5.0]))]:
         out = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
         ref = oracle.direct(pts, q)
-        np.testing.assert_allclose(out, ref, rtol=1e-13, atol=1e-15 * np.abs(ref).max())
+        # one leaf: the FMM is the direct sum, so the two differ only by the rounding of
+        # an N-term sum in another order: |error_i| <= 2 N eps sum_j |q_j| G_ij (the
+        # forward error bound of recursive summation, doubled for the rsqrt and the
+        # products; the magnitudes come from the oracle's direct sum with |q|)
+        mag = oracle.direct(pts, np.abs(q))
+        assert np.all(np.abs(out - ref) <= 2 * pts.shape[0] * np.finfo(float).eps * mag)
     # zero density, linearity, default density, host-buffer path
     pts, q, _ = synth_inputs.make("C1")
     gp = gpu_plan(pts, 4, 24, 64, tb=tb, q=q)
@@ -186,15 +201,15 @@ def test_edge_cases():
     q2 = np.random.default_rng(3).uniform(-1, 1, q.size)
     a = gp.matvec(torch.from_numpy(0.5 * q - 2 * q2).to(dev)).cpu().numpy()
     b = 0.5 * gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy() - 2 * gp.matvec(torch.from_numpy(q2).to(dev)).cpu().numpy()
-    assert rel(a, b) < 1e-13
+    assert par(a, b) < 1e-13
     # default density == explicit density (atomic scatter-adds reorder sums: not bitwise)
-    assert rel(gp.matvec().cpu().numpy(), gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
+    assert par(gp.matvec().cpu().numpy(), gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
     host = gp.matvec_host(q)
-    assert rel(host, gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
+    assert par(host, gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
     # exact 2x scaling (up to atomic reduction order)
     s1 = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
     s2 = gpu_plan(2 * pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
-    assert rel(s2, 0.5 * s1) < 1e-14
+    assert par(s2, 0.5 * s1) < 1e-14
 
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k", "torus50k"])
@@ -210,7 +225,7 @@ def test_overlapped_near_stream(case, mode, monkeypatch):
         gp = gpu_plan(pts, p, k, s, tb=tb, leaf_ops=lo)
         for _ in range(2):
             out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-            assert rel(out, ref) <= TOL
+            assert par(out, ref) <= TOL
 
 
 STAGE2_CASES = ["C1", "sphere6k_s16", "octa_sphere32k", "torus50k"]
@@ -228,7 +243,7 @@ def test_stage2_lowrank_m2l_parity(case, C2):
     assert gp.info["m2l_eps2"] == pytest.approx(tb["eps2"], rel=1e-12)
     assert gp.info["m2l_rank_mean"] == pytest.approx(tb["ranks"].mean())
     out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL
     # the algorithmic M2L work is 4 k r_o per V pair
     V = gp.export_lists()["V"]
     assert gp.info["m2l_flops"] == pytest.approx(float((4.0 * tb["k"] * tb["ranks"][V[:, 2]]).sum()))
@@ -244,7 +259,7 @@ def test_stage2_c2_full_size_and_accuracy():
     ref2 = op.matvec(t2, q)
     ref1 = op.matvec(tb, q)
     out = gpu_plan(pts, cfg["p"], cfg["k"], cfg["leaf"], tb=t2, m2l_c2=1.0).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-    assert rel(out, ref2) <= TOL
+    assert par(out, ref2) <= TOL
     idx = np.random.default_rng(0).choice(pts.shape[0], 2048, replace=False)
     d = oracle.direct(pts, q, idx)
     assert rel(out[idx], d) <= 1.02 * rel(ref1[idx], d)
@@ -272,13 +287,13 @@ def test_double_layer_parity(case, leaf_ops):
     gp = K().Plan(torch.from_numpy(pts).to(dev), None, p=p, k=k, leaf_size=s, tables=tb, leaf_ops=leaf_ops,
                   normals=torch.from_numpy(nrm).to(dev))
     out = gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL
     gs = K().Plan(torch.from_numpy(pts).to(dev), None, p=p, k=k, leaf_size=s, tables=tb, leaf_ops=leaf_ops,
                   normals=torch.from_numpy(nrm).to(dev), split_phases=True)
     gs.matvec(torch.from_numpy(q).to(dev))
-    assert rel(gs.export_phase("near"), ph["near"]) <= TOL
+    assert par(gs.export_phase("near"), ph["near"]) <= TOL
     amp = {4: 1.0, 6: 1.0, 8: 30.0}[p]
-    assert rel(gs.export_phase("qhat"), ph["qhat"]) <= amp * TOL
+    assert par(gs.export_phase("qhat"), ph["qhat"]) <= amp * TOL
 
 
 def test_double_layer_gauss_and_loopback():
@@ -296,10 +311,10 @@ def test_double_layer_gauss_and_loopback():
     out = K().Plan(Pt, None, p=8, k=100, leaf_size=64, tables=tb, normals=Nt).matvec(Qt).cpu().numpy()
     assert out[0] == pytest.approx(-1.0, abs=5e-5)
     ref = oracle.Plan(P, 64, tb["n"]).matvec(tb, q, normals=Nn)
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL
     plans = [K().Plan(Pt, None, p=8, k=100, leaf_size=64, tables=tb, normals=Nt, nranks=3, rank=r) for r in range(3)]
     for pt in K().fmm_matvec_group(plans, [Qt] * 3, owned=False):
-        assert rel(pt.cpu().numpy(), ref) <= TOL
+        assert par(pt.cpu().numpy(), ref) <= TOL
 
 
 NEAR_CASES = {
@@ -329,9 +344,9 @@ def test_near_field_modes(case, mode, monkeypatch):
         else:
             assert inf["near_mutual_leaves"] == 0
         out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-        assert rel(out, ref) <= TOL, (mode, split)
+        assert par(out, ref) <= TOL, (mode, split)
         if split:
-            assert rel(gp.export_phase("near"), ph["near"]) <= TOL
+            assert par(gp.export_phase("near"), ph["near"]) <= TOL
 
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "torus50k", "sphere20k_s400"])
@@ -350,7 +365,7 @@ def test_double_layer_near_modes(case, mode, monkeypatch):
         gp = gpu_plan(pts, p, k, s, tb=tb, split_phases=split, normals=torch.from_numpy(nrm).cuda())
         assert (gp.info["near_mutual_leaves"] > 0) == (mode == "1")
         out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-        assert rel(out, ref) <= TOL, (mode, split)
+        assert par(out, ref) <= TOL, (mode, split)
 
 
 def test_operator_file_cache(tmp_path):
@@ -366,7 +381,7 @@ def test_operator_file_cache(tmp_path):
     c = gpu_plan(pts, p, k, s, tb=K().fmm_tables_load(path))
     Q = torch.from_numpy(q).cuda()
     oa, ob, oc = (x.matvec(Q).cpu().numpy() for x in (a, b, c))
-    assert rel(oa, ob) <= 1e-14 and rel(oa, oc) <= 1e-14
+    assert par(oa, ob) <= 1e-14 and par(oa, oc) <= 1e-14
     with pytest.raises(RuntimeError) as e:
         gpu_plan(pts, 4, 24, s, operator_file=path)
     assert "(-2)" in str(e.value) and "operator file" in str(e.value)
@@ -390,7 +405,7 @@ def test_depth_cap_duplicate_clusters():
         finally:
             del os.environ["KIFMM_SYM"]
         out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-        assert rel(out, ref) <= TOL, mode
+        assert par(out, ref) <= TOL, mode
 
 
 def test_degenerate_clouds():
@@ -407,4 +422,4 @@ def test_degenerate_clouds():
     q = np.random.default_rng(7).uniform(-1, 1, t.size)
     ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
     out = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).cuda()).cpu().numpy()
-    assert rel(out, ref) <= TOL
+    assert par(out, ref) <= TOL

@@ -57,3 +57,34 @@ def test_refuses_corrupt_truncated_foreign(built, tmp_path):
 def test_unwritable_path_is_an_error(tmp_path):
     with pytest.raises(RuntimeError):
         K.fmm_tables_build(4, 24, save=str(tmp_path / "no" / "such" / "dir" / "t.kifmm"))
+
+
+@pytest.mark.parametrize("field,value", [("p", 1), ("p", 40000), ("n", 2 ** 30), ("n", 57), ("k", 0), ("k", 2 ** 31 - 1),
+                                         ("k_req", -5)])
+def test_refuses_corrupt_header(built, tmp_path, field, value):
+    # header i32 fields p, n, k, k_req at byte 16: sizes derive from them, so a corrupt
+    # header is refused before anything is allocated (no huge allocation, no exception
+    # through the C ABI)
+    _, path = built
+    bad = bytearray(open(path, "rb").read())
+    off = 16 + 4 * ("p", "n", "k", "k_req").index(field)
+    bad[off:off + 4] = int(value).to_bytes(4, "little", signed=True)
+    p = tmp_path / f"hdr_{field}"
+    p.write_bytes(bytes(bad))
+    _expect_refused(str(p), "corrupt header")
+
+
+def test_concurrent_writers_publish_a_complete_file(tmp_path):
+    # several processes computing the same tables at once (every rank of a multi-GPU
+    # setup with one operator_file): each writes its own temporary file and renames it
+    # over the target, so the result is always one complete, loadable file
+    import subprocess
+    import sys
+    path = str(tmp_path / "shared.kifmm")
+    code = ("import sys; sys.path.insert(0, %r); import paper_1211_2517_b200 as K; "
+            "K.fmm_tables_build(4, 24, save=%r)" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), path))
+    procs = [subprocess.Popen([sys.executable, "-c", code]) for _ in range(4)]
+    assert all(p.wait(timeout=300) == 0 for p in procs)
+    u = K.fmm_tables_load(path)
+    assert u["p"] == 4 and u["k"] == 25
+    assert not [f for f in os.listdir(tmp_path) if ".tmp" in f]
