@@ -1,19 +1,20 @@
 """Benchmark: one FP64 KIFMM matvec per step (BASELINE.json metric: FMM matvec
-points/sec and M2L FP64 tensor-pipe fraction of peak).
+points/sec (FP64) and the roofline fraction of the dominant kernel).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference] [--weak]
 
-Workload (N=1): BASELINE.json configs[1] = "C2": 1,048,576 points uniform in the
-unit cube (seed 0), densities U[-1,1], p = 6 (n = 152), k = 60 (k_eff 61), leaf
-128.  A step is one whole fmm_matvec (permute, S2M, M2M, M2L, X, L2L, L2T, W,
-P2P, unpermute) with the inputs resident in HBM; L2 is flushed (a 256 MiB write)
-between timed steps, outside the timed events.  Multi-GPU (torchrun, N ranks):
-weak scaling, ONE problem of N unit cubes tiled (2, 2x2, 2x2x2) with 2^20 points each
-(C2's density, so every rank's Morton share has C2's leaf occupancy) partitioned over the
-ranks by Morton ranges (OWNED mode: each rank's owned densities in, owned
-potentials out), ghost multipoles / densities exchanged over NCCL inside every
-step; `value` = all points / max-over-ranks step time.  `--impl reference` times
-the CPU oracle (oracle/) on the host.
+Workload (default C4 = BASELINE.json configs[3], the config BASELINE runs at 1/2/4/8 GPUs):
+N = 2^24 points on the torus R = 1, r = 0.3 (area-weighted, seed 0), densities U[-1,1],
+p = 6 (n = 152), k = 60 (k_eff 61), leaf 128, adaptive octree.  C2 (configs[1]), C3 and
+C5 (configs[4]: 2^26 points, the 8-GPU scale-out case, `--gpus 8 --config C5`) run with
+--config.  A step is one whole fmm_matvec (permute, S2M, M2M, M2L, X, L2L, L2T, W, P2P,
+unpermute) with the inputs resident in HBM; L2 is flushed (a 256 MiB write) between timed
+steps, outside the timed events.  Multi-GPU (torchrun, N ranks): strong scaling, the SAME
+problem partitioned over the ranks by Morton ranges (OWNED mode: each rank's owned
+densities in, owned potentials out), ghost multipoles / densities exchanged over NCCL
+inside every step; `value` = N / max-over-ranks step time.  `--weak` instead tiles N unit
+cubes of the config (cube configs only).  `--impl reference` times the CPU oracle
+(oracle/) on the host on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -37,7 +38,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--weak", action="store_true", help="N > 1: tile N copies (cube configs) instead of strong scaling")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -95,8 +97,27 @@ def dist_env():
     return ws, rank, local
 
 
+def oracle_sample(name: str, pts, q):
+    """A bounded sample of the workload for the CPU oracle (the oracle runs at ~1e6
+    points/s on a host, so the full C4 / C5 would take minutes per matvec): a contiguous
+    piece of the same surface or volume with the workload's point density, so leaves,
+    lists and the near/far work mix per point are those of the full problem.
+      C1, C2, C3   the whole workload (seconds)
+      C4           the torus sector 0 <= atan2(y, x) < 2 pi / 16 (1/16 of the points)
+      C5           the points of the first of the 64 spheres (2^20 points)
+    Returns (points, densities, description)."""
+    if name == "C4":
+        sel = np.arctan2(pts[:, 1], pts[:, 0])
+        sel = (sel >= 0) & (sel < 2 * np.pi / 16)
+        return np.ascontiguousarray(pts[sel]), np.ascontiguousarray(q[sel]), "torus sector 0 <= u < 2pi/16 of C4"
+    if name == "C5":
+        per = pts.shape[0] // 64
+        return np.ascontiguousarray(pts[:per]), np.ascontiguousarray(q[:per]), "sphere 0 of C5's 64 spheres"
+    return pts, q, f"the whole {name} workload"
+
+
 def oracle_matvec_timer(pts, q, cfg, reps: int = 1):
-    """Time the oracle (as it stands) on the host cores: one full matvec per rep."""
+    """Time the oracle (as it stands) on the host cores: one full matvec of (pts, q) per rep."""
     import oracle
     tb = oracle.precompute.build_tables(cfg["p"], cfg["k"])
     plan = oracle.Plan(pts, cfg["leaf"], tb["n"])
@@ -120,22 +141,30 @@ def run_reference(args):
     if rank != 0:
         return
     pts, q, cfg = synth_inputs.make(args.config)
-    N = cfg["N"]
-    # warm-up and timed steps: each step one full oracle matvec of the same workload
-    ts = oracle_matvec_timer(pts, q, cfg, reps=args.warmup + args.steps)[args.warmup:]
+    sp, sq, what = oracle_sample(args.config, pts, q)
+    ns = sp.shape[0]
+    # warm-up and timed steps: each step one oracle matvec of the sample
+    ts = oracle_matvec_timer(sp, sq, cfg, reps=args.warmup + args.steps)[args.warmup:]
     sec = float(np.mean(ts))
-    value = N / sec
+    value = ns / sec
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "N": N, "p": cfg["p"], "k": cfg["k"], "leaf_size": cfg["leaf"],
+        "scaling": "strong" if not args.weak else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "N": cfg["N"], "p": cfg["p"], "k": cfg["k"], "leaf_size": cfg["leaf"],
                    "kind": cfg["kind"]},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
-                         "sample": f"full {args.config} matvec (N={N}) per step, oracle/ C++ -O2 OpenMP"},
+                         "sample": f"{what}: {ns} points, one oracle matvec per step (oracle/ C++ -O2 OpenMP)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def ncu_evidence(config: str):
+    """Per-config ncu numbers of the timed kernels (profiles/ncu_<config>.json: written from
+    an `ncu --set full` capture of this config's bench command), or None."""
+    f = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
+    return json.load(open(f)) if os.path.exists(f) else None
 
 
 def run_ours(args):
@@ -148,9 +177,10 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # N = 1: the BASELINE workload itself.  N > 1: weak scaling, one partitioned problem of
-    # N x (points of the workload), same recipe (every rank draws the same seeded cloud)
-    pts, q, cfg = synth_inputs.make(args.config, scale=ws)
+    # N = 1: the BASELINE workload itself.  N > 1: strong scaling, the same problem
+    # partitioned over the ranks (every rank draws the same seeded cloud); --weak: N x the
+    # points of the workload (tiled unit cubes for the cube configs)
+    pts, q, cfg = synth_inputs.make(args.config, scale=ws if args.weak else 1)
     N = cfg["N"]
     stream = torch.cuda.current_stream()
     P = torch.from_numpy(pts).to(dev)
@@ -254,65 +284,77 @@ def run_ours(args):
     if rank != 0:
         dist.destroy_process_group()
         return
-    # ---- roofline of the dominant kernel (M2L, DMMA) from the live per-phase events
-    k = info["k"]
-    m2l_flops = 2.0 * k * k * info["nV_local"]
-    m2l_s = phase["m2l"] * 1e-3
+    # ---- rooflines of the two candidate dominant kernels, from the profiled twin's live CUDA
+    # events on the launching stream (phases serialised, L2 flushed, same steps)
     peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")))
-    peak = float(peaks["dmma_m8n8k4_tflops"])
-    achieved = m2l_flops / m2l_s / 1e12
-    traffic, pipe_pct = None, None
-    tf = os.path.join(ROOT, "profiles", "m2l_dram_bytes.json")
-    if os.path.exists(tf) and ws == 1:
-        mt = json.load(open(tf))
-        traffic = mt.get("bytes_per_launch")
-        pipe_pct = mt.get("tensor_pipe_active_pct")
-    # ---- near field (P2P, FP64 ALU): directed point pairs over the profiled "eval" phase, against
-    # the FP64 pipe at the minimal per-pair instruction counts of k_near (13 FP64 per unordered
-    # mutual pair, 12 per one-sided pair: 3 DADD, r^2 3, rsqrt refinement 5, accumulation 1-2)
-    p2p = None
-    if info["near_pairs"] > 0:
+    ncu = ncu_evidence(args.config) if ws == 1 else None
+    k = info["k"]
+    m2l_flops = float(info["m2l_flops"])  # sum over this rank's V pairs of 2 k^2
+    m2l_ms = phase["m2l"]
+    m2l_peak = float(peaks["dmma_m8n8k4_tflops"])
+    m2l_tf = m2l_flops / (m2l_ms * 1e-3) / 1e12
+    m2l = {"bound": "tensor", "kernel": "M2L: k_m2l_sib16 (DMMA.8x8x4 FP64 via mma.sync m16n8k8)",
+           "achieved": m2l_tf, "peak": m2l_peak, "unit": "TFLOP/s", "frac": m2l_tf / m2l_peak,
+           "traffic": (ncu or {}).get("m2l", {}).get("dram_bytes_per_launch"),
+           "tensor_pipe_active_pct_ncu": (ncu or {}).get("m2l", {}).get("tensor_pipe_active_pct"),
+           "peak_source": "measured: tools/microbench/fp64_peaks.cu DMMA loop on this pool's B200 "
+                          "(profiles/fp64_peaks_r01.json; MEASURED_PEAKS.json has no FP64 figure)",
+           "per_unit": "2 k_eff^2 flops per V pair", "units_per_launch": info["nV_local"],
+           "flops_per_launch": m2l_flops, "ms_per_launch": m2l_ms}
+    # near field (P2P, FP64 ALU, issue-bound): the FP64 instructions of the minimal pair
+    # formulation (13 per unordered mutual pair: 3 DADD, DMUL + 2 DFMA for r^2, 5 for the rsqrt
+    # correction, 2 DFMA accumulations; 12 per one-sided pair) over the k_near launches alone
+    # (fmm_info.near_ms), against the FP64 pipe's instruction rate (measured DFMA loop / 2)
+    near = None
+    if info["near_pairs"] > 0 and info["near_ms"] > 0:
         npair, pm = int(info["near_pairs"]), int(info["near_mutual_pairs"])
         instr = 13.0 * pm + 12.0 * (npair - 2 * pm)
-        lane_peak = float(peaks["dfma_tflops"]) * 1e12 / 2  # FP64 instruction-lanes / s (a DFMA = 2 flops)
-        eval_s = phase["eval"] * 1e-3
-        p2p = {"bound": "fp64_alu", "kernel": "k_near (mutual leaf pairs)", "directed_pairs": npair,
-               "mutual_pairs": pm, "ms": phase["eval"], "pairs_per_s": npair / eval_s,
-               "fp64_instr_lanes": instr, "peak_instr_lanes_per_s": lane_peak, "frac": instr / lane_peak / eval_s,
-               "note": "ms = the profiled 'eval' phase, which also holds the L2T leaf GEMV and the W far pass; "
-                       "peak = measured DFMA loop (profiles/fp64_peaks_r01.json) / 2"}
-        pf = os.path.join(ROOT, "profiles", "p2p_fp64_pipe.json")
-        if os.path.exists(pf) and ws == 1:
-            p2p["fp64_pipe_active_pct_ncu"] = json.load(open(pf)).get("fp64_pipe_active_pct")
+        lane_peak = float(peaks["dfma_tflops"]) / 2  # T FP64 instruction-lanes / s (a DFMA = 2 flops)
+        near_s = info["near_ms"] * 1e-3
+        near = {"bound": "alu", "kernel": "k_near (P2P, mutual leaf pairs; every pass-shape launch of one matvec)",
+                "achieved": instr / near_s / 1e12, "peak": lane_peak, "unit": "T FP64 instr-lanes/s",
+                "frac": instr / near_s / 1e12 / lane_peak,
+                "traffic": (ncu or {}).get("near", {}).get("dram_bytes_per_launch"),
+                "fp64_pipe_active_pct_ncu": (ncu or {}).get("near", {}).get("fp64_pipe_active_pct"),
+                "peak_source": "measured DFMA loop (profiles/fp64_peaks_r01.json) / 2 = 148 SMs x 64 FP64 lanes x clock",
+                "per_unit": "13 FP64 instr per unordered mutual pair, 12 per one-sided pair",
+                "directed_pairs": npair, "mutual_pairs": pm, "units_per_launch": npair,
+                "pairs_per_s": npair / near_s, "ms_per_launch": info["near_ms"]}
+    # the dominant kernel of this config is the one with the larger share of the step
+    cand = [x for x in (m2l, near) if x is not None]
+    roof = max(cand, key=lambda x: x["ms_per_launch"])
+    roof = dict(roof, timed_in="profiled twin plan of the same workload: phases serialised on one stream, "
+                                "CUDA events around the kernel's launches, L2 flushed, same step count",
+                share_of_serial_step=roof["ms_per_launch"] / sum(phase.values()))
+    if ncu:
+        roof["ncu_source"] = ncu.get("source")
     # ---- cpu baseline: the oracle on the host cores, one full matvec (rank 0, N = 1 only)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
-        ts = oracle_matvec_timer(pts, q, cfg, reps=1)
-        cpu = {"value": N / ts[0], "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"one full {args.config} matvec (N={N}), oracle/ C++ -O2 OpenMP, {ts[0]:.2f} s"}
+        sp, sq, what = oracle_sample(args.config, pts, q)
+        ts = oracle_matvec_timer(sp, sq, cfg, reps=1)
+        cpu = {"value": sp.shape[0] / ts[0], "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"{what}: one oracle matvec of {sp.shape[0]} points, oracle/ C++ -O2 OpenMP, {ts[0]:.2f} s"}
     value = N / (ms * 1e-3)
-    config = {"workload": args.config if ws == 1 else f"{args.config} x{ws} (weak: {ws} tiled unit cubes)", "N": N,
+    wl = args.config if ws == 1 or not args.weak else f"{args.config} x{ws} (weak: {ws} tiled copies)"
+    config = {"workload": wl, "N": N,
               "N_per_gpu": N // ws, "p": cfg["p"], "k": cfg["k"], "k_eff": k, "leaf_size": cfg["leaf"],
               "kind": cfg["kind"], "parallelism": "single" if ws == 1 else f"morton-partition{ws} (NCCL ghosts)",
               "l2": "flushed (256 MiB write) between timed steps",
-              "near_field": "mutual leaf pairs (k_near) on a second stream beside the far field (overlap mode 3)"}
+              "near_field": ("mutual leaf pairs (k_near) on a second stream beside the far field (overlap mode 3)"
+                             if (info["N"] if ws == 1 else N // ws) <= (8 << 20) else
+                             "mutual leaf pairs (k_near), serialised with the far field (> 8M owned points)")}
     if ws > 1:
         config.update(mode="owned", ghost_q_rows_rank0=info["ghost_q_recv"], ghost_dens_rank0=info["ghost_d_recv"],
                       straddling_boxes=info["n_straddle"])
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if args.weak else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-        "roofline": {"bound": "tensor", "kernel": "M2L: k_m2l_sib + k_ggs_sq (DMMA.8x8x4 FP64)", "achieved": achieved,
-                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                     "tensor_pipe_active_pct_ncu": pipe_pct,
-                     "peak_source": "measured: tools/microbench/fp64_peaks.cu DMMA m8n8k4 loop on this pool's B200 "
-                                    "(profiles/fp64_peaks_r01.json)",
-                     "flops_per_launch": m2l_flops, "ms_per_launch": phase["m2l"],
-                     "timed_in": "profiled twin plan of the same workload: phases serialised on one stream, "
-                                 "CUDA events around the M2L launches, L2 flushed, same step count"},
+        "roofline": roof,
+        "kernels": {"m2l": m2l, "p2p": near},
         "phase_ms": phase,
-        "p2p": p2p,
         "clocks": clk.summary(),
         "e2e": {"value": N / e2e_s, "unit": "points/s", "h2d_bytes_per_step": e2e_bytes,
                 "d2h_bytes_per_step": e2e_bytes, "ms_per_step": e2e_s * 1e3, "api": e2e_api},

@@ -148,6 +148,8 @@ typedef struct {
   int64_t near_pairs;         /* directed near-field point pairs (U + direct W/X, r = 0 pairs
                                  included) delivered by k_near per matvec: own points m^2, 2 per
                                  mutual pair, 1 per one-sided pair (mutual mode; 0 otherwise) */
+  double near_ms;             /* last profiled matvec: the near-field (P2P) launches alone, ms
+                                 (CUDA events on the launching stream; -1 when not profiled) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

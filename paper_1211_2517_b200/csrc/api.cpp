@@ -65,6 +65,10 @@ void free_plan_memory(fmm_plan* h) {
   if (P.stream_near) cudaStreamDestroy(P.stream_near);
   if (P.stream_m2l) cudaStreamDestroy(P.stream_m2l);
   if (P.ev_m2l) cudaEventDestroy(P.ev_m2l);
+  for (auto& e : P.ev_near) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
   P.ev_fork = P.ev_join = P.ev_m2l = nullptr;
   P.stream_near = P.stream_m2l = nullptr;
   kifmm::nccl_comm_destroy(P);
@@ -355,6 +359,8 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     }
     P.ev_phase.resize(kPhases + 1);
     for (auto& e : P.ev_phase) cudaEventCreate(&e);
+    if (P.profile)
+      for (auto& e : P.ev_near) cudaEventCreate(&e);
     if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
       set_error("fmm_setup: CUDA error during setup");
       return fail(FMM_ECUDA);
@@ -646,6 +652,11 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
     info->schedule_ms = h->schedule_ms;
     if (P.profile && P.profiled && P.ev_phase.size() == kPhases + 1 && cudaEventSynchronize(P.ev_phase[kPhases]) == cudaSuccess)
       for (int i = 0; i < kPhases; ++i) cudaEventElapsedTime(&info->phase_ms[i], P.ev_phase[i], P.ev_phase[i + 1]);
+    info->near_ms = -1;
+    if (P.profile && P.profiled && P.near_timed && cudaEventSynchronize(P.ev_near[1]) == cudaSuccess) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, P.ev_near[0], P.ev_near[1]) == cudaSuccess) info->near_ms = ms;
+    }
     info->nranks = P.dist.nranks;
     info->rank = P.dist.rank;
     info->own_lo = P.dist.own_lo;

@@ -239,6 +239,8 @@ struct Plan {
   cudaStream_t stream_near = nullptr;
   cudaStream_t stream_m2l = nullptr;  // overlap 2: high-priority stream of the M2L kernel
   cudaEvent_t ev_m2l = nullptr;
+  cudaEvent_t ev_near[2] = {nullptr, nullptr};  // profiled plans: around the near-field launches
+  bool near_timed = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_phase;
   bool profile = false;

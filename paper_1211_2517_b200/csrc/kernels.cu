@@ -1983,6 +1983,13 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
   const int kp = P.kp, np = P.np, k = P.k, n = P.n;
   const DistPlan& Dp = P.dist;
   auto mark = [&](int i) { if (P.profile) cudaEventRecord(P.ev_phase[i], st); };
+  // profiled plans also time the near-field launches alone (fmm_info.near_ms)
+  auto mark_near = [&](int i) {
+    if (P.profile && P.ev_near[i]) {
+      cudaEventRecord(P.ev_near[i], st);
+      P.near_timed = true;
+    }
+  };
   double* pts_w = reinterpret_cast<double*>(T.d_pts) + 3;  // the q column of the (x, y, z, q) points
   EvalArgs ea{};
   ea.pts = T.d_pts; ea.geom = T.d_geom; ea.pbeg = T.d_pbeg; ea.pend = T.d_pend;
@@ -2024,7 +2031,11 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (launch_near(P, ea, P.stream_near)) return -3;
         KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
       }
-      if (P.overlap == 3) {  // near field on the near stream from here, beside the far field
+      // near field on the near stream from here, beside the far field.  NCCL-connected
+      // plans fork after the ghost exchange instead (stage 3): k_near's persistent CTAs
+      // hold every SM slot, and the NCCL kernels enqueued behind the M2M would wait for
+      // them, serialising the far field behind the whole near field
+      if (P.overlap == 3 && !(P.nccl_comm && !P.bem)) {
         KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
         KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
         if (P.bem) {  // BEM: the element-integral block SpMV (HBM-bound) beside the M2L (tensor)
@@ -2074,6 +2085,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       return pack(P.d_qhat, kp, P.xq.d_send_idx, P.xq.nsend, kp, P.xq.d_send, st);
     case 3: {  // interactions and downward pass for the owned targets
       if (unpack(P.d_qhat, kp, P.xq.d_recv_idx, P.xq.nrecv, kp, P.xq.d_recv, st)) return -3;
+      if (P.overlap == 3 && P.nccl_comm && !P.bem) {  // the near stream's fork, after the exchanges (see stage 1)
+        KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
+        KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, P.stream_near));
+        if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
+      }
       mark(4);
       // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
       //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
@@ -2137,8 +2154,10 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
           ++g_launches;
           if (bem_near_matvec(P, st)) return -3;
         }
-      } else if (sep && !P.overlap && launch_near(P, ea, st)) {
-        return -3;
+      } else if (sep && !P.overlap) {
+        mark_near(0);
+        if (launch_near(P, ea, st)) return -3;
+        mark_near(1);
       }
       // L2T stage 1: q_d = r_l T' l^_B ; W stage 1: q_u = r_A U q^'_A  (store)
       if (launch_ggs(P.g_l2t, P.d_T, 0, np, kp, n, P.d_lhat, kp, P.d_eqd_l2t, np, false, st)) return -3;
@@ -2158,7 +2177,9 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       const bool nr_fused = P.nr_on && !sep;
       if (nr_fused) {
         if (!P.leaf_l2t) KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, st));
+        mark_near(0);
         if (near_launch(P, P.d_pot_near, st)) return -3;
+        mark_near(1);
       }
       // L2T + W stage 2 (and, fused, the near field): potentials at the targets of each leaf
       if (P.n_tleaf > 0 && !(sep && P.leaf_l2t && P.n_far_seg == 0) && !(nr_fused && P.n_far_seg == 0)) {

@@ -65,14 +65,14 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "kifmm.h"\n'
-                   'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(fmm_options), sizeof(fmm_info_t),'
-                   ' sizeof(fmm_tables_view), offsetof(fmm_options, operator_file), offsetof(fmm_info_t, m2l_exec_flops), offsetof(fmm_info_t, near_pairs));'
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(fmm_options), sizeof(fmm_info_t),'
+                   ' sizeof(fmm_tables_view), offsetof(fmm_options, operator_file), offsetof(fmm_info_t, m2l_exec_flops), offsetof(fmm_info_t, near_pairs), offsetof(fmm_info_t, near_ms));'
                    'return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
     got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
     assert got == [ctypes.sizeof(K.Options), ctypes.sizeof(K.Info), ctypes.sizeof(K.TablesView),
-                   K.Options.operator_file.offset, K.Info.m2l_exec_flops.offset, K.Info.near_pairs.offset]
+                   K.Options.operator_file.offset, K.Info.m2l_exec_flops.offset, K.Info.near_pairs.offset, K.Info.near_ms.offset]
 
 
 def test_distributed_entry_points_validate_without_gpu():

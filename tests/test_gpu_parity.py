@@ -112,11 +112,17 @@ def test_matvec_parity_shared_tables(case, wx, leaf_ops):
     # has entries ~1e3-1e8 x those of q^ at p = 8 (cond E_u 4e11), so summation-order
     # rounding in them is amplified in directions the later steps annihilate; the
     # phase tolerance scales with that amplification.
+    # The per-element check (max |a - b| / max |b|) on these intermediates gets 10x the L2
+    # amplification at p = 8: boxes at fine levels have small q^' but the same absolute
+    # rounding from S' (measured 6.4e-10 on octa_sphere32k, p = 8); the final potentials
+    # below and above are held to 1e-11 per element.
     amp = {4: 1.0, 6: 1.0, 8: 30.0}[p]
+    amp_max = {4: 1.0, 6: 1.0, 8: 300.0}[p]
     for name in ("qhat", "lhat"):
         a, b = gp.export_phase(name), ph[name]
         if np.linalg.norm(b) > 0:
-            assert par(a, b) <= amp * TOL, name
+            assert rel(a, b) <= amp * TOL, name
+            assert np.abs(a - b).max() / np.abs(b).max() <= amp_max * TOL, name
     assert par(gp.export_phase("near"), ph["near"]) <= TOL
     if np.linalg.norm(ph["far"]) > 0:
         assert par(gp.export_phase("far"), ph["far"]) <= TOL
@@ -293,7 +299,10 @@ def test_double_layer_parity(case, leaf_ops):
     gs.matvec(torch.from_numpy(q).to(dev))
     assert par(gs.export_phase("near"), ph["near"]) <= TOL
     amp = {4: 1.0, 6: 1.0, 8: 30.0}[p]
-    assert par(gs.export_phase("qhat"), ph["qhat"]) <= amp * TOL
+    amp_max = {4: 1.0, 6: 1.0, 8: 300.0}[p]  # (see test_matvec_parity_shared_tables)
+    a, b = gs.export_phase("qhat"), ph["qhat"]
+    assert rel(a, b) <= amp * TOL
+    assert np.abs(a - b).max() / np.abs(b).max() <= amp_max * TOL
 
 
 def test_double_layer_gauss_and_loopback():
