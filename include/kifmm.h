@@ -112,6 +112,15 @@ typedef struct {
                          tables' versioned binary file (tables_io.cpp): loaded if it exists —
                          FMM_ECONFIG if it was built for another (p, k, d, pinv_rcond), is
                          corrupt or of another version — else computed and written there. */
+  int near_mode;      /* near-field (P2P) kernel: -1 (default) = 1; 1 = mutual leaf pairs (k_near:
+                         each pair of owned leaves once for both sides, G symmetric);
+                         0 = one-sided per target leaf (k_eval); 2 = warp-pair symmetric
+                         (k_p2p_sym; single layer only, else 0).  Same result to rounding. */
+  int overlap;        /* near field beside the far field on a second plan stream: -1 (default) =
+                         3 up to 8M owned points, else 0; 0 = serialised; 3 = k_near (or the BEM
+                         near-field SpMV) forked at the densities (NCCL plans: after the ghost
+                         exchange); 1 / 2 = the one-sided near field forked at the densities /
+                         beside a high-priority M2L stream.  Profiled and split-phase plans: 0. */
 } fmm_options;
 
 typedef struct {
@@ -120,7 +129,7 @@ typedef struct {
   int nboxes, nleaves, nlevels;
   int64_t nU, nV, nW, nX;     /* list sizes (pairs of boxes) */
   int64_t n_s2m, n_xnd, n_l2t, n_wnd;  /* evaluation work items */
-  int64_t m2l_tiles, m2l_pairs;
+  int64_t m2l_tiles, m2l_pairs;  /* M2L tiles of the sibling-class kernel; V pairs it applies */
   int64_t launches;           /* kernels of this library launched by the last fmm_matvec */
   double r0, lo_root[3];
   double precompute_ms, tree_ms, lists_ms, schedule_ms;

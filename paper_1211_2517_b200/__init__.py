@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("KIFMM_LIB") or os.path.join(_HERE, "libkifmm_b200.so")  # KIFMM_LIB: diagnostic builds
+LIB_PATH = os.path.join(_HERE, "libkifmm_b200.so")
 
 FMM_OK, FMM_EINVAL, FMM_ECONFIG, FMM_ECUDA, FMM_ENOMEM, FMM_ENCCL = 0, -1, -2, -3, -4, -5
 
@@ -35,7 +35,8 @@ class Options(ctypes.Structure):
                 ("tables", ctypes.POINTER(TablesView)), ("profile", ctypes.c_int), ("split_phases", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
                 ("leaf_ops", ctypes.c_int), ("m2l_c2", ctypes.c_double), ("normals", ctypes.c_void_p),
-                ("triangles", ctypes.c_void_p), ("operator_file", ctypes.c_char_p)]
+                ("triangles", ctypes.c_void_p), ("operator_file", ctypes.c_char_p), ("near_mode", ctypes.c_int),
+                ("overlap", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -220,7 +221,7 @@ class Plan:
                  rcond: float = 1e-10, wx_direct_max: int = -1, tables: dict | None = None, profile: bool = False,
                  split_phases: bool = False, stream=None, nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, leaf_ops: int = -1, m2l_c2: float = 0.0, normals=None,
-                 triangles=None, operator_file: str | None = None):
+                 triangles=None, operator_file: str | None = None, near_mode: int = -1, overlap: int = -1):
         import torch
         if not (isinstance(points, torch.Tensor) and points.is_cuda):
             raise TypeError("points must be a CUDA tensor [N, 3] float64")
@@ -231,6 +232,7 @@ class Plan:
         opt.p, opt.k, opt.leaf_size, opt.d, opt.pinv_rcond = p, k, leaf_size, d, rcond
         opt.wx_direct_max, opt.profile, opt.split_phases = wx_direct_max, int(profile), int(split_phases)
         opt.nranks, opt.rank, opt.leaf_ops, opt.m2l_c2 = nranks, rank, int(leaf_ops), float(m2l_c2)
+        opt.near_mode, opt.overlap = int(near_mode), int(overlap)
         if normals is not None:  # double-layer sources
             if not (isinstance(normals, torch.Tensor) and normals.is_cuda and tuple(normals.shape) == (self.N, 3)):
                 raise TypeError("normals must be a CUDA tensor [N, 3]")

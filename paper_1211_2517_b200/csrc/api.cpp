@@ -118,6 +118,8 @@ void fmm_default_options(fmm_options* o) {
   o->normals = nullptr;
   o->triangles = nullptr;
   o->operator_file = nullptr;
+  o->near_mode = -1;
+  o->overlap = -1;
 }
 
 const char* fmm_last_error(void) { return kifmm::last_error(); }
@@ -216,7 +218,11 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     P.profile = opt->profile != 0;
     P.split_phases = opt->split_phases != 0;
     P.leaf_ops_opt = opt->leaf_ops;
-    if (const char* e = std::getenv("KIFMM_SYM")) P.sym_opt = std::atoi(e);  // diagnostics: 0 = one-sided near field
+    if (opt->near_mode < -1 || opt->near_mode > 2 || opt->overlap < -1 || opt->overlap > 3) {
+      set_error("fmm_setup: near_mode must be in [-1, 2] and overlap in [-1, 3]");
+      return FMM_EINVAL;
+    }
+    P.sym_opt = opt->near_mode;
     P.dist.nranks = opt->nranks;
     P.dist.rank = opt->rank;
     auto fail = [&](int rc) { free_plan_memory(h); delete h; pending = nullptr; return rc; };
@@ -335,16 +341,13 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     //  1 / 2 (diagnostics, k_eval era): whole near field forked after the densities /
     //    beside a high-priority M2L stream.
     {
-      const char* e = std::getenv("KIFMM_OVERLAP");
       // (default only up to 8M owned points: C2 / C3 gain 2-10%, C4 / C5 lose 1-2% — their long
       // k_near and M2L launches have little tail to fill, and the split costs k_near balance)
       const int64_t owned = P.dist.own_hi - P.dist.own_lo;
       const bool ovl_default = (P.nr_on || P.bem) && !P.profile && owned <= (int64_t)8 << 20;
-      P.overlap = !P.split_phases ? (e ? std::atoi(e) : (ovl_default ? 3 : 0)) : 0;
+      P.overlap = !P.split_phases ? (opt->overlap >= 0 ? opt->overlap : (ovl_default ? 3 : 0)) : 0;
       if (P.bem && P.overlap != 3) P.overlap = 0;         // BEM: only the SpMV fork (mode 3)
       if (P.overlap == 3 && !P.nr_on && !P.bem) P.overlap = 0;  // mode 3 runs k_near or the BEM SpMV
-      if (const char* f = std::getenv("KIFMM_NEAR_SPLIT")) P.nr_split = std::atof(f);
-      if (const char* f = std::getenv("KIFMM_NEAR_SPARE")) P.nr_spare = std::atoi(f);
       int lo_prio = 0, hi_prio = 0;
       cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
       if (P.overlap &&
@@ -644,7 +647,7 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
     info->nboxes = P.tree.nboxes; info->nleaves = P.tree.nleaves; info->nlevels = P.tree.nlevels;
     info->nU = P.lists.nU; info->nV = P.lists.nV; info->nW = P.lists.nW; info->nX = P.lists.nX;
     info->n_s2m = P.n_s2m; info->n_xnd = P.n_xnd; info->n_l2t = P.n_l2t; info->n_wnd = P.n_wnd;
-    info->m2l_tiles = P.g_m2l.ntiles; info->m2l_pairs = P.g_m2l.npairs;
+    info->m2l_tiles = P.g_m2l_sib.ntiles; info->m2l_pairs = P.nV_local;
     info->launches = P.launches;
     info->r0 = P.tree.r0;
     for (int d = 0; d < 3; ++d) info->lo_root[d] = P.tree.lo_root[d];

@@ -188,7 +188,7 @@ struct Plan {
   // (first point, m, chunk begin, chunk end), grouped by pass shape; chunks (first
   // source slot, n | nchk << 10 | ml << 20, mh, 0); source slots (point indices)
   bool nr_on = false;
-  int nr_table = 0;                        // k_near shape table (KIFMM_NEAR_TAB)
+  int nr_table = 0;                        // k_near shape table: 0 single layer, 3 double layer
   int n_tleaf_mut = 0;                     // target leaves with mutual segments
   int64_t n_mut_pairs = 0;                 // unordered point pairs of the mutual segments
   int64_t n_near_pairs = 0;               // directed near-field point pairs (k_near mode)
@@ -227,7 +227,7 @@ struct Plan {
   int n_l2t = 0, n_wnd = 0;
   std::vector<void*> allocations;              // everything cudaMalloc'ed for the plan
   // dense-algebra launches
-  GemmLaunch g_s2m, g_m2l, g_x, g_l2t, g_w;
+  GemmLaunch g_s2m, g_x, g_l2t, g_w;
   SibLaunch g_m2l_sib;
   double sib_min_density = 0.5;   // sibling groups at least this full go to k_m2l_sib
   std::vector<GemmLaunch> g_m2m;   // per child level (descending)

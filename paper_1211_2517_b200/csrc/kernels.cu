@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(KP * 4) k_ggs_sq(const GemmTile* __restrict__ 
 }
 
 // ----------------------------------------------------------------------------
-// k_m2l_sib: M2L grouped by sibling structure.  Every V pair (B, A) joins child a
+// k_m2l_sib16: M2L grouped by sibling structure.  Every V pair (B, A) joins child a
 // of P = parent(B) with child b of a colleague Q = P + delta of P, and
 // its operator is C_{2 delta + b - a}.  A column = (target B, source parent Q);
 // a tile = up to NT columns of one class (delta, a).  For each non-adjacent b the
@@ -235,136 +235,11 @@ __global__ void __launch_bounds__(KP * 4) k_ggs_sq(const GemmTile* __restrict__ 
 //   * the operator rows (A fragments) stream through registers in chunks of CH
 //     k-steps, chunk c+1 (or chunk 0 of the next step's operator) loaded while
 //     chunk c feeds the tensor pipe.
-// ----------------------------------------------------------------------------
-template <int KP, int NT, int MINB>
-__global__ void __launch_bounds__(KP * 4, MINB) k_m2l_sib(const int4* __restrict__ tiles, int ntiles,
-                                                  const int* __restrict__ cols, const int* __restrict__ classes,
-                                                  const double* __restrict__ C, int mvalid, const double* X, double* Y,
-                                                  int* __restrict__ counter) {
-  constexpr int NW = KP / 8;
-  constexpr int NTH = NW * 32;
-  constexpr int SB = KP + 4;
-  constexpr int KS = KP / 4;
-  constexpr int K2 = KP / 2;
-  constexpr int CW = 9;                        // column record: target, src[8]
-  constexpr int CH = (KS % 4 == 0) ? 4 : 2;    // k-steps per A chunk
-  constexpr int NCH = KS / CH;
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_meta[3][NT * CW];
-  __shared__ int s_tile[3];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int row = warp * 8 + g;
-  int ti = blockIdx.x;
-  if (ti >= ntiles) return;
-
-  auto fetch_meta = [&](int tid, int slot) {
-    const int4 tl = tiles[tid];
-    for (int e = threadIdx.x; e < NT * CW; e += NTH) {
-      const int c = e / CW;
-      s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
-    }
-  };
-  auto gather = [&](int slot, int b, int buf) {
-    double* Bd = sm + buf * NT * SB;
-    for (int p = warp; p < NT; p += NW) {
-      const int src = s_meta[slot][p * CW + 1 + b];
-      for (int c = lane; c < K2; c += 32) {
-        double* dst = Bd + p * SB + 2 * c;
-        if (src >= 0) cp_async16(dst, X + (size_t)src * KP + 2 * c);
-        else { dst[0] = 0.0; dst[1] = 0.0; }
-      }
-    }
-  };
-  auto op_rows = [&](int id) { return C + (size_t)id * KP * KP + (size_t)row * KP + t; };
-
-  int slot = 0;
-  fetch_meta(ti, 0);
-  if (threadIdx.x == 0) s_tile[1] = gridDim.x + atomicAdd(counter, 1);
-  __syncthreads();
-  const int* cls = classes + tiles[ti].x * 17;
-  gather(0, cls[1], 0);
-  cp_async_commit();
-  double a_cur[CH];
-  const double* Aop = op_rows(cls[9]);
-#pragma unroll
-  for (int s = 0; s < CH; ++s) a_cur[s] = __ldg(Aop + 4 * s);
-  int buf = 0;
-  double acc[NT / 8][2];
-#pragma unroll
-  for (int j = 0; j < NT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-
-  while (true) {
-    const int nv = cls[0];
-    const int nslot = slot == 2 ? 0 : slot + 1;
-    const int tnext = s_tile[nslot];
-    for (int jb = 0; jb < nv; ++jb) {
-      const bool last = jb + 1 == nv;
-      if (jb == 0 && tnext < ntiles) {  // one tile ahead: its metadata, and the id of the tile after it
-        fetch_meta(tnext, nslot);
-        if (threadIdx.x == 0) s_tile[nslot == 2 ? 0 : nslot + 1] = gridDim.x + atomicAdd(counter, 1);
-      }
-      cp_async_wait0();
-      __syncthreads();  // B panel of this step landed; next metadata visible
-      const double* Anext = nullptr;
-      if (!last) {
-        gather(slot, cls[2 + jb], buf ^ 1);
-        Anext = op_rows(cls[9 + jb + 1]);
-      } else if (tnext < ntiles) {
-        const int* ncls = classes + tiles[tnext].x * 17;
-        gather(nslot, ncls[1], buf ^ 1);
-        Anext = op_rows(ncls[9]);
-      }
-      cp_async_commit();
-      const double* B = sm + buf * NT * SB + g * SB + t;
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        double a_nxt[CH];
-        const double* src = c + 1 < NCH ? Aop + 4 * CH * (c + 1) : Anext;
-        if (src) {
-#pragma unroll
-          for (int s = 0; s < CH; ++s) a_nxt[s] = __ldg(src + 4 * s);
-        }
-#pragma unroll
-        for (int s = 0; s < CH; ++s) {
-          const double* bp = B + 4 * (c * CH + s);
-#pragma unroll
-          for (int j = 0; j < NT / 8; ++j) dmma_8x8x4(acc[j][0], acc[j][1], a_cur[s], bp[j * 8 * SB]);
-        }
-#pragma unroll
-        for (int s = 0; s < CH; ++s) a_cur[s] = a_nxt[s];
-      }
-      Aop = Anext;
-      buf ^= 1;
-      if (last) {
-        // D(g, 2t + c) of n-block j = output row `row` of column j*8 + 2t + c
-        if (row < mvalid) {
-#pragma unroll
-          for (int j = 0; j < NT / 8; ++j) {
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const int tg = s_meta[slot][(j * 8 + 2 * t + c) * CW];
-              if (tg >= 0) atomicAdd(Y + (size_t)tg * KP + row, acc[j][c]);
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < NT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-      }
-    }
-    if (tnext >= ntiles) break;
-    ti = tnext;
-    slot = nslot;
-    cls = classes + tiles[ti].x * 17;
-  }
-}
-
-// ----------------------------------------------------------------------------
-// k_m2l_sib16: k_m2l_sib with the m16n8k8 FP64 MMA (kp = 32, 64, 104): each B fragment
-// serves two 8-row halves, halving the shared-memory loads per DMMA.  RB = ceil(kp/16)
-// row blocks (kp = 104: 7 blocks, rows 104..111 zero — 7.7% padded M, K unpadded);
-// warp w owns rows 16 (w % RB) .. +16 and columns (w / RB) * NCW .. +NCW of a tile.
-// Same tile scheduler, metadata ring and cp.async B pipeline as k_m2l_sib.
+//
+// The m16n8k8 FP64 MMA (kp = 32, 64, 104; SASS DMMA.8x8x4): each B fragment serves two
+// 8-row halves, halving the shared-memory loads per DMMA.  RB = ceil(kp/16) row blocks
+// (kp = 104: 7 blocks, rows 104..111 zero — 7.7% padded M, K unpadded); warp w owns rows
+// 16 (w % RB) .. +16 and columns (w / RB) * NCW .. +NCW of a tile.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4], double b0, double b1) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
@@ -1302,25 +1177,6 @@ int launch_ggs(const GemmLaunch& g, const double* ops, int op_stride, int M, int
 
 }  // namespace
 
-template <int KP, int MINB>
-int launch_sib(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
-  constexpr int NT = sq_nt(KP);
-  const size_t smem = (size_t)NT * 2 * (KP + 4) * sizeof(double);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_sib<KP, NT, MINB>, KP * 4, smem);
-  const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
-  KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
-  k_m2l_sib<KP, NT, MINB><<<grid, KP * 4, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y,
-                                                      g.d_counter);
-  return 0;
-}
-
-// KIFMM_SIB_MINB (diagnostics): 2 = no register cap for the KP <= 64 kernels
-static int sib_minb() {
-  static int v = [] { const char* e = std::getenv("KIFMM_SIB_MINB"); return e ? std::atoi(e) : 3; }();
-  return v;
-}
-
 // ----------------------------------------------------------------------------
 // k_m2l_lr: the sibling-grouped M2L with the paper's stage-2 low-rank cores
 // (eq-lra): C_o ~= U^_o V^_o with rank r_o, so each operator step of a
@@ -1690,8 +1546,7 @@ int launch_lr2_cb(const SibLaunch& g, const LowRank& lr, int mvalid, const doubl
 
 template <int KP, int RP>
 int launch_lr2(const SibLaunch& g, const LowRank& lr, int mvalid, const double* X, double* Y, cudaStream_t st) {
-  static const int cb = [] { const char* e = std::getenv("KIFMM_LR2_CB"); return e ? std::atoi(e) : 1; }();
-  return cb == 1 ? launch_lr2_cb<KP, RP, 1>(g, lr, mvalid, X, Y, st) : launch_lr2_cb<KP, RP, 2>(g, lr, mvalid, X, Y, st);
+  return launch_lr2_cb<KP, RP, 1>(g, lr, mvalid, X, Y, st);  // (two column blocks per warp measured slower)
 }
 
 template <int KP, int RP>
@@ -1729,14 +1584,13 @@ int launch_m2l_lowrank(const SibLaunch& g, const LowRank& lr, int kp, int mvalid
   if (g.ntiles == 0) return 0;
   ++g_launches;
   int rc = 0;
-  static const int v2 = [] { const char* e = std::getenv("KIFMM_LR2"); return e ? std::atoi(e) : 1; }();
-  if (v2 && kp == 64 && (lr.rp == 16 || lr.rp == 32)) {
+  if (kp == 64 && (lr.rp == 16 || lr.rp == 32)) {
     rc = lr.rp == 16 ? launch_lr2<64, 16>(g, lr, mvalid, X, Y, st) : launch_lr2<64, 32>(g, lr, mvalid, X, Y, st);
     if (rc) return rc;
     KIFMM_CUDA(cudaGetLastError());
     return 0;
   }
-  if (v2 && kp == 32 && (lr.rp == 16 || lr.rp == 32)) {
+  if (kp == 32 && (lr.rp == 16 || lr.rp == 32)) {
     rc = lr.rp == 16 ? launch_lr2<32, 16>(g, lr, mvalid, X, Y, st) : launch_lr2<32, 32>(g, lr, mvalid, X, Y, st);
     if (rc) return rc;
     KIFMM_CUDA(cudaGetLastError());
@@ -1764,29 +1618,13 @@ int launch_sib16(const SibLaunch& g, const double* C, int mvalid, const double* 
   return 0;
 }
 
-static int sib16() {
-  static int v = [] { const char* e = std::getenv("KIFMM_SIB16"); return e ? std::atoi(e) : 1; }();
-  return v;
-}
-
 int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, const double* X, double* Y, cudaStream_t st) {
   if (g.ntiles == 0) return 0;
   ++g_launches;
-  if (sib16() && (kp == 32 || kp == 64 || (kp == 104 && sib16() != 2))) {
-    if (kp == 32) launch_sib16<32, 3>(g, C, mvalid, X, Y, st);
-    else if (kp == 104) launch_sib16<104, 3>(g, C, mvalid, X, Y, st);
-    else if (sib_minb() == 3) launch_sib16<64, 3>(g, C, mvalid, X, Y, st);
-    else launch_sib16<64, 2>(g, C, mvalid, X, Y, st);
-    KIFMM_CUDA(cudaGetLastError());
-    return 0;
-  }
-  if (kp == 32) { if (sib_minb() == 3) launch_sib<32, 3>(g, C, mvalid, X, Y, st); else launch_sib<32, 1>(g, C, mvalid, X, Y, st); }
-  else if (kp == 64) { if (sib_minb() == 3) launch_sib<64, 3>(g, C, mvalid, X, Y, st); else launch_sib<64, 1>(g, C, mvalid, X, Y, st); }
-  else {
-    static const int m104 = [] { const char* e = std::getenv("KIFMM_SIB104_MINB"); return e ? std::atoi(e) : 2; }();
-    if (m104 == 2) launch_sib<104, 2>(g, C, mvalid, X, Y, st);
-    else launch_sib<104, 1>(g, C, mvalid, X, Y, st);
-  }
+  if (kp == 32) launch_sib16<32, 3>(g, C, mvalid, X, Y, st);
+  else if (kp == 64) launch_sib16<64, 3>(g, C, mvalid, X, Y, st);
+  else if (kp == 104) launch_sib16<104, 3>(g, C, mvalid, X, Y, st);
+  else return -3;  // kp = round_up(k_eff, 8) with k_eff <= 100 at p <= 8: 32, 64 or 104 only
   KIFMM_CUDA(cudaGetLastError());
   return 0;
 }
@@ -1849,8 +1687,7 @@ int build_x_ops(Plan& P, cudaStream_t st) {
 }
 
 int sib_tile_width(int kp, bool lowrank) {
-  static const int v2 = [] { const char* e = std::getenv("KIFMM_LR2"); return e ? std::atoi(e) : 1; }();
-  return lowrank && v2 && kp <= 64 ? kLr2Cols : sq_nt(kp);
+  return lowrank && kp <= 64 ? kLr2Cols : sq_nt(kp);
 }
 
 int ggs_tile_width(int M, int K) {
@@ -1866,15 +1703,8 @@ int kernels_init() {
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs_sq<64, sq_nt(64)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs_sq<104, sq_nt(104)>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<32, sq_nt(32), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<64, sq_nt(64), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104), 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib<104, sq_nt(104), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<32, sq_nt(32), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<64, sq_nt(64), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_m2l_sib16<104, sq_nt(104), 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   KIFMM_CUDA(cudaFuncSetAttribute(k_ggs<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return 0;
@@ -1883,16 +1713,14 @@ int kernels_init() {
 
 // Evaluation work lists live in the plan; see build_schedules (schedule.cpp).
 // k_eval with 128 threads per target leaf (measured best of 128 / 256 threads and
-// a warp-per-leaf variant; KIFMM_EVAL_NT=256 selects the 256-thread kernel)
+// a warp-per-leaf variant)
 static void launch_eval(const Plan& P, EvalArgs a, int chk_self, cudaStream_t st, bool dl = false, int nitems = -1) {
-  static const int nt = [] { const char* e = std::getenv("KIFMM_EVAL_NT"); return e ? std::atoi(e) : 128; }();
   if (nitems < 0) {
     a.items = P.d_tleaf_items;
     nitems = P.n_tleaf;
   }
   if (nitems == 0) return;
   if (dl) k_eval<128, 256, true><<<nitems, 128, 0, st>>>(a, chk_self);
-  else if (nt == 256) k_eval<256, 512><<<nitems, 256, 0, st>>>(a, chk_self);
   else k_eval<128, 256><<<nitems, 128, 0, st>>>(a, chk_self);
 }
 
@@ -1917,14 +1745,8 @@ static int launch_near(const Plan& P, const EvalArgs& ea, cudaStream_t st) {
 static int launch_sym(const Plan& P, cudaStream_t st) {
   if (P.n_sym == 0) return 0;
   ++g_launches;
-  static const int minb = [] { const char* e = std::getenv("KIFMM_SYM_MINB"); return e ? std::atoi(e) : 5; }();
   const int grid = (P.n_sym + SYM_WARPS - 1) / SYM_WARPS;
-  if (minb == 8)
-    k_p2p_sym<8><<<grid, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts, P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
-  else if (minb == 5)
-    k_p2p_sym<5><<<grid, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts, P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
-  else
-    k_p2p_sym<6><<<grid, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts, P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
+  k_p2p_sym<5><<<grid, SYM_WARPS * 32, 0, st>>>(P.d_sym, P.n_sym, P.tree.d_pts, P.tree.d_pbeg, P.tree.d_pend, P.d_pot_near);
   KIFMM_CUDA(cudaGetLastError());
   return 0;
 }
@@ -2107,7 +1929,6 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       } else if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, sm2l)) {
         return -3;
       }
-      if (launch_ggs(P.g_m2l, P.d_C, kp * kp, kp, kp, k, P.d_qhat, kp, P.d_lhat, kp, true, sm2l)) return -3;
       if (P.overlap == 2) {
         KIFMM_CUDA(cudaEventRecord(P.ev_m2l, P.stream_m2l));
         KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));

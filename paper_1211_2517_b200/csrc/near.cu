@@ -443,23 +443,16 @@ int near_launch_sel(const NearArgs& a, int count, int spare, cudaStream_t st) {
 struct NearShapeDef {
   int tb, mq;
 };
-// pass shapes by capacity TB x MQ: table 0 favours TB (fewer reductions per pair),
-// table 1 small TB (fewer registers, more resident warps)
+// pass shapes by capacity TB x MQ (more targets per thread: fewer reductions per pair;
+// measured against a small-TB table with more resident warps, which was slower)
 const NearShapeDef kNearTab0[] = {{2, 4}, {3, 4}, {4, 4}, {5, 4}, {6, 4}, {4, 8}, {5, 8}, {6, 8}, {7, 8},
                                   {8, 8}, {5, 16}, {6, 16}, {7, 16}, {8, 16}, {5, 32}, {6, 32}, {7, 32}, {8, 32}};
-const NearShapeDef kNearTab1[] = {{2, 4}, {3, 4}, {2, 8}, {3, 8}, {2, 16}, {3, 16}, {2, 32}, {3, 32}, {4, 32},
-                                  {5, 32}, {6, 32}};
-
-const NearShapeDef kNearTab2[] = {{2, 4}, {4, 4}, {6, 4}, {8, 4}, {5, 8}, {6, 8}, {7, 8}, {8, 8},
-                                  {5, 16}, {6, 16}, {7, 16}, {8, 16}, {5, 32}, {6, 32}};
 
 const NearShapeDef* near_table(int tab, int* count) {
-  if (tab == 3) {  // double layer: table 0 up to 160 targets (static shared memory <= 48 KB)
+  if (tab == 3) {  // double layer: the shapes up to 160 targets (static shared memory <= 48 KB)
     *count = (int)(sizeof(kNearTab0) / sizeof(kNearTab0[0])) - 3;
     return kNearTab0;
   }
-  if (tab == 1) { *count = (int)(sizeof(kNearTab1) / sizeof(kNearTab1[0])); return kNearTab1; }
-  if (tab == 2) { *count = (int)(sizeof(kNearTab2) / sizeof(kNearTab2[0])); return kNearTab2; }
   *count = (int)(sizeof(kNearTab0) / sizeof(kNearTab0[0]));
   return kNearTab0;
 }
@@ -503,10 +496,10 @@ int near_launch(const Plan& P, double* out, cudaStream_t st, int part, int spare
     int rc = -3;
     switch (tab[g.x].tb * 64 + tab[g.x].mq) {
 #define KIFMM_NS(TBv, MQv) case TBv * 64 + MQv: rc = near_launch_sel<TBv, MQv>(a, count, spare, st); break;
-      KIFMM_NS(2, 4) KIFMM_NS(3, 4) KIFMM_NS(4, 4) KIFMM_NS(5, 4) KIFMM_NS(6, 4) KIFMM_NS(8, 4)
-      KIFMM_NS(2, 8) KIFMM_NS(3, 8) KIFMM_NS(4, 8) KIFMM_NS(5, 8) KIFMM_NS(6, 8) KIFMM_NS(7, 8) KIFMM_NS(8, 8)
-      KIFMM_NS(2, 16) KIFMM_NS(3, 16) KIFMM_NS(5, 16) KIFMM_NS(6, 16) KIFMM_NS(7, 16) KIFMM_NS(8, 16)
-      KIFMM_NS(2, 32) KIFMM_NS(3, 32) KIFMM_NS(4, 32) KIFMM_NS(5, 32) KIFMM_NS(6, 32) KIFMM_NS(7, 32) KIFMM_NS(8, 32)
+      KIFMM_NS(2, 4) KIFMM_NS(3, 4) KIFMM_NS(4, 4) KIFMM_NS(5, 4) KIFMM_NS(6, 4)
+      KIFMM_NS(4, 8) KIFMM_NS(5, 8) KIFMM_NS(6, 8) KIFMM_NS(7, 8) KIFMM_NS(8, 8)
+      KIFMM_NS(5, 16) KIFMM_NS(6, 16) KIFMM_NS(7, 16) KIFMM_NS(8, 16)
+      KIFMM_NS(5, 32) KIFMM_NS(6, 32) KIFMM_NS(7, 32) KIFMM_NS(8, 32)
 #undef KIFMM_NS
       default: break;
     }

@@ -75,24 +75,6 @@ int build_schedules(Plan& P, cudaStream_t st) {
   if (Ls.nW) KIFMM_CUDA(cudaMemcpyAsync(W.data(), Ls.d_W, sizeof(int4) * Ls.nW, cudaMemcpyDeviceToHost, st));
   if (Ls.nX) KIFMM_CUDA(cudaMemcpyAsync(X.data(), Ls.d_X, sizeof(int4) * Ls.nX, cudaMemcpyDeviceToHost, st));
   KIFMM_CUDA(cudaStreamSynchronize(st));
-  if (const char* dir = std::getenv("KIFMM_DUMP")) {  // debugging aid: raw tree + lists
-    auto dump = [&](const char* name, const void* p, size_t bytes) {
-      std::string path = std::string(dir) + "/" + name;
-      if (FILE* f = std::fopen(path.c_str(), "wb")) { std::fwrite(p, 1, bytes, f); std::fclose(f); }
-    };
-    dump("key.bin", T.key.data(), T.key.size() * 8);
-    dump("level.bin", T.level.data(), T.level.size() * 4);
-    dump("parent.bin", T.parent.data(), T.parent.size() * 4);
-    dump("pbeg.bin", T.pbeg.data(), T.pbeg.size() * 4);
-    dump("pend.bin", T.pend.data(), T.pend.size() * 4);
-    dump("leaf.bin", T.leaf.data(), T.leaf.size());
-    dump("child_begin.bin", T.child_begin.data(), T.child_begin.size() * 4);
-    dump("nchild.bin", T.nchild.data(), T.nchild.size() * 4);
-    dump("U.bin", U.data(), U.size() * 8);
-    dump("V.bin", V.data(), V.size() * 16);
-    dump("W.bin", W.data(), W.size() * 16);
-    dump("X.bin", X.data(), X.size() * 16);
-  }
   // validate the device lists before indexing host arrays with them
   auto bad = [&](int b) { return b < 0 || b >= nb; };
   for (auto& u : U)
@@ -174,7 +156,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     // (slot offsets are int32: past ~2e9 slots the one-sided k_eval path takes over)
     if (4.0 * (double)slots > budget || slots > 2000000000LL) mutual = false;
   }
-  static const double sym_r = [] { const char* e = std::getenv("KIFMM_SYM_R"); return e ? std::atof(e) : 1.4; }();
+  constexpr double sym_r = 1.4;  // padding-factor threshold of the warp-pair mode (measured scan 1.1-2.0)
   auto pass_slots = [](int m) { int full = m / 96, rem = m - 96 * full; return 96 * full + 32 * ((rem + 31) / 32); };
   auto pad_ratio = [&](int mt, int ms) {
     return (double)pass_slots(mt) / mt * (double)((ms + 15) / 16 * 16) / ms;
@@ -187,9 +169,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
     return r1 <= r2 ? 1 : 2;
   };
   // k_near pass shape of an m-point leaf (the least padding; passes of the largest beyond it)
-  static const int nr_tab_env = [] { const char* e = std::getenv("KIFMM_NEAR_TAB"); return e ? std::atoi(e) : 0; }();
   const bool dl = P.d_nrm != nullptr;
-  const int nr_tab = dl ? 3 : nr_tab_env;  // double layer: shapes up to 160 targets
+  const int nr_tab = dl ? 3 : 0;  // double layer: shapes up to 160 targets
   P.nr_table = nr_tab;
   const int kNearShapes = near_shape_count(nr_tab);
   auto nr_shape = [&](int m) {
@@ -202,12 +183,11 @@ int build_schedules(Plan& P, cudaStream_t st) {
     return (m + cap - 1) / cap * cap;
   };
   // target side of a mutual pair {a, b}, or -1 (not both owned)
-  static const bool mut_off = std::getenv("KIFMM_MUT_OFF") != nullptr;  // diagnostics: k_near one-sided only
   std::vector<int> leaf_slots(nb, 0);  // nr_slots of every owned leaf, once
   if (mutual)
     for (int i = 0; i < nt; ++i) leaf_slots[titems[i].x] = nr_slots(npts(titems[i].x));
   auto mut_target = [&](int a, int b) {
-    if (!mutual || mut_off || !inD(a) || !inD(b)) return -1;
+    if (!mutual || !inD(a) || !inD(b)) return -1;
     const int64_t ca = (int64_t)leaf_slots[a] * npts(b), cb = (int64_t)leaf_slots[b] * npts(a);
     if (ca != cb) return ca < cb ? a : b;
     return ((a ^ b) & 1) ? std::min(a, b) : std::max(a, b);
@@ -297,8 +277,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
   P.n_near_pairs = 0;
   P.nr_groups.clear();
   if (mutual && nt > 0) {
-    static const int kMinGroup = [] { const char* e = std::getenv("KIFMM_NEAR_MINGROUP"); return e ? std::atoi(e) : 2048; }();
-    static const int kUnitChunks = [] { const char* e = std::getenv("KIFMM_NEAR_UNIT"); return e ? std::atoi(e) : 4; }();
+    constexpr int kMinGroup = 2048;  // leaves per pass-shape launch (smaller groups fold into a neighbour)
+    constexpr int kUnitChunks = 4;   // chunks per work unit (C3 6.2 -> 5.3 ms against whole leaves)
     // pass shape per leaf: the least-padding shape, unless its group would have fewer than
     // kMinGroup leaves — then the next larger kept shape (more padding), or for the
     // largest leaves the largest kept smaller shape (more passes)
@@ -490,8 +470,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
   if (make_launch(P, P.g_s2m, sgroup, w_kn, st) || make_launch(P, P.g_x, xgroup, w_kn, st) ||
       make_launch(P, P.g_l2t, lgroups, w_nk, st) || make_launch(P, P.g_w, wgroups, w_nk, st))
     return -3;
-  // M2L.  Sibling groups (target B, source parent Q) at least sib_min_density full run
-  // in k_m2l_sib; the remaining pairs run offset-major in k_ggs_sq.
+  // M2L.  Every V pair runs in the sibling-class kernel: as a step of its sibling group's
+  // column (full or masked class), or as a one-operator pseudo-class column.
   {
     auto anchor = [&](int b, int out[3]) {
       uint64_t k = T.key[b];
@@ -513,7 +493,6 @@ int build_schedules(Plan& P, cudaStream_t st) {
       rec[0] = 1; rec[1] = 0; rec[9] = o;
       nvalid[kSib + o] = 1;
     }
-    static const bool sparse_in_sib = [] { const char* e = std::getenv("KIFMM_M2L_SPARSE_SIB"); return !e || std::atoi(e) != 0; }();
     for (int lin = 0; lin < 27; ++lin) {
       if (lin == 13) continue;
       const int didx = lin < 13 ? lin : lin - 1;
@@ -556,13 +535,10 @@ int build_schedules(Plan& P, cudaStream_t st) {
     // column) — when that (class, mask) gathers at least mask_min columns; the rest go by
     // the cost model below (the full class, absent children included, or one-operator
     // pseudo-classes per pair).
-    std::vector<PairGroup> groups(kNumOffsets);
-    for (int o = 0; o < kNumOffsets; ++o) groups[o] = PairGroup{o, 1.0, {}};
     const int NTs = sib_tile_width(kp, P.lr.on && P.lr.rp <= 32);  // (k_m2l_lr2 takes rp 16 / 32)
-    static const int mask_min_env = [] { const char* e = std::getenv("KIFMM_M2L_MASK_MIN"); return e ? std::atoi(e) : -1; }();
-    // 256 measured best of 16-2048 (tools/m2l_scale.py): C4 M2L 6.50 -> 5.61 ms, C5 29.0 ->
+    // 256 measured best of 16-2048 (round 1, a since-retired environment switch): C4 M2L 6.50 -> 5.61 ms, C5 29.0 ->
     // 28.0 ms; C3 neutral (below ~512 its sparse masks split into partly filled tiles)
-    const int mask_min = mask_min_env >= 0 ? mask_min_env : 256;
+    constexpr int mask_min = 256;
     struct SibGroup { int b, cls, mask, cnt; int src[8]; };
     std::vector<SibGroup> sgs;
     sgs.reserve(V.size() / 4 + 16);
@@ -637,8 +613,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
       // cost model (per column, FP64 peak 37 TF/s, fp64 L2 RED 5.2e11/s): the sibling
       // kernel spends nvalid GEMM columns + 1 RED row, offset-major cnt x (GEMM + RED row);
       // the RED weight 0.5 is the measured best of 0.25 / 0.5 / 1 / 2 over C3-C5
-      // (tools/m2l_scale.py: C4 M2L 6.49 ms at 0.5 vs 6.51 at 1; C5 29.0 vs 29.2)
-      static const double red_scale = [] { const char* e = std::getenv("KIFMM_M2L_RED_SCALE"); return e ? std::atof(e) : 0.5; }();
+      // (round 1: C4 M2L 6.49 ms at 0.5 vs 6.51 at 1; C5 29.0 vs 29.2)
+      constexpr double red_scale = 0.5;
       const double Gc = 2.0 * kp * kp / 37e12, Rr = red_scale * kp / 5.2e11;
       if (g.cnt * (Gc + Rr) >= nvalid[g.cls] * Gc + Rr) {
         add_col(g.cls, g);
@@ -648,19 +624,14 @@ int build_schedules(Plan& P, cudaStream_t st) {
           int o = -1;  // the pair's offset id: the class step of child j
           for (int t = 0; t < classes[g.cls * 17]; ++t)
             if (classes[g.cls * 17 + 1 + t] == j) o = classes[g.cls * 17 + 9 + t];
-          if (sparse_in_sib) {
-            auto& cc = cls_cols[kSib + o];
-            cc.push_back(g.b);
-            cc.push_back(g.src[j]);
-            for (int t = 1; t < 8; ++t) cc.push_back(-1);
-          } else {
-            groups[o].pairs.push_back(make_int2(g.src[j], g.b));
-          }
+          auto& cc = cls_cols[kSib + o];  // a one-operator pseudo-class column
+          cc.push_back(g.b);
+          cc.push_back(g.src[j]);
+          for (int t = 1; t < 8; ++t) cc.push_back(-1);
         }
       }
     }
     mark("m2l classes");
-    if (make_launch(P, P.g_m2l, groups, w_sq, st)) return -3;
     if (std::getenv("KIFMM_DEBUG_M2L")) {  // diagnostics: columns per class kind
       int64_t full = 0, masked = 0, pseudo = 0;
       for (size_t c = 0; c < cls_cols.size(); ++c) {
@@ -673,7 +644,6 @@ int build_schedules(Plan& P, cudaStream_t st) {
     P.m2l_exec_flops = 0;
     const int ncls = (int)cls_cols.size();
     for (int cls = 0; cls < ncls; ++cls) P.m2l_exec_flops += (double)nvalid[cls] * (cls_cols[cls].size() / 9) * 2.0 * P.k * P.k;
-    for (auto& g : groups) P.m2l_exec_flops += (double)g.pairs.size() * 2.0 * P.k * P.k;
     // sibling tiles: per class, columns in target order, NT columns per tile
     std::vector<int> cols;
     std::vector<int4> tiles;
@@ -685,13 +655,11 @@ int build_schedules(Plan& P, cudaStream_t st) {
       for (int c = 0; c < ncol; c += NTs) tiles.push_back(make_int4(cls, base + c, std::min(NTs, ncol - c), 0));
     }
     // longest tiles first (the kernel hands tiles out dynamically: LPT order balances the SMs;
-    // a Morton-window order for L2 locality measured no better on C2 / C3 / C5).  Stage 2
-    // with KIFMM_LR_ORDER=1: class-major (all SMs share one class's operator factors)
-    static const int lr_order = [] { const char* e = std::getenv("KIFMM_LR_ORDER"); return e ? std::atoi(e) : 0; }();
-    if (!(P.lr.on && lr_order == 1))
-      std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
-        return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
-      });
+    // a Morton-window order for L2 locality measured no better on C2 / C3 / C5; class-major
+    // order for stage 2 neither)
+    std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
+      return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
+    });
     mark("m2l tiles");
     P.g_m2l_sib.ntiles = (int)tiles.size();
     P.g_m2l_sib.ncols = (int)cols.size() / 9;

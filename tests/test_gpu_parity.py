@@ -220,15 +220,14 @@ def test_edge_cases():
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k", "torus50k"])
 @pytest.mark.parametrize("mode", ["1", "2", "3"])
-def test_overlapped_near_stream(case, mode, monkeypatch):
+def test_overlapped_near_stream(case, mode):
     # near field on a second stream joined before the output (mode 3: k_near split around
     # the M2L, beside the S2M / L2T GEMVs); repeated matvecs reuse the streams and events
-    monkeypatch.setenv("KIFMM_OVERLAP", mode)
     pts, q, p, k, s = CASES[case]()
     tb = tables(p, k)
     ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q)
     for lo in (0, 1):
-        gp = gpu_plan(pts, p, k, s, tb=tb, leaf_ops=lo)
+        gp = gpu_plan(pts, p, k, s, tb=tb, leaf_ops=lo, overlap=int(mode))
         for _ in range(2):
             out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
             assert par(out, ref) <= TOL
@@ -337,16 +336,15 @@ NEAR_CASES = {
 
 @pytest.mark.parametrize("case", list(NEAR_CASES))
 @pytest.mark.parametrize("mode", ["1", "2", "0"])
-def test_near_field_modes(case, mode, monkeypatch):
+def test_near_field_modes(case, mode):
     """Mutual leaf pairs (k_near, default), warp-pair symmetric (k_p2p_sym) and all
     one-sided (k_eval) give the oracle's result; fused and split passes."""
     pts, q, p, k, s = NEAR_CASES[case]()
     tb = tables(p, k)
     op = oracle.Plan(pts, s, tb["n"])
     ref, ph = op.matvec(tb, q, phases=True)
-    monkeypatch.setenv("KIFMM_SYM", mode)
     for split in (False, True):
-        gp = gpu_plan(pts, p, k, s, tb=tb, split_phases=split)
+        gp = gpu_plan(pts, p, k, s, tb=tb, split_phases=split, near_mode=int(mode))
         inf = gp.info
         if mode == "1":
             assert inf["near_mutual_leaves"] > 0 and inf["near_mutual_pairs"] > 0 and inf["near_sym_pairs"] == 0
@@ -360,7 +358,7 @@ def test_near_field_modes(case, mode, monkeypatch):
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "torus50k", "sphere20k_s400"])
 @pytest.mark.parametrize("mode", ["1", "0"])
-def test_double_layer_near_modes(case, mode, monkeypatch):
+def test_double_layer_near_modes(case, mode):
     """Double-layer sources with mutual leaf pairs (k_near, sign rule p_j -= (d . w_i) r^-3)
     and all one-sided (k_eval): the oracle's double-layer potential, fused and split."""
     pts, q, p, k, s = {**CASES, **NEAR_CASES}[case]()
@@ -369,9 +367,9 @@ def test_double_layer_near_modes(case, mode, monkeypatch):
     nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
     tb = tables(p, k)
     ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q, normals=nrm)
-    monkeypatch.setenv("KIFMM_SYM", mode)
     for split in (False, True):
-        gp = gpu_plan(pts, p, k, s, tb=tb, split_phases=split, normals=torch.from_numpy(nrm).cuda())
+        gp = gpu_plan(pts, p, k, s, tb=tb, split_phases=split, normals=torch.from_numpy(nrm).cuda(),
+                      near_mode=int(mode))
         assert (gp.info["near_mutual_leaves"] > 0) == (mode == "1")
         out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
         assert par(out, ref) <= TOL, (mode, split)
@@ -408,11 +406,7 @@ def test_depth_cap_duplicate_clusters():
     tb = tables(4, 24)
     ref = oracle.Plan(pts, 64, tb["n"]).matvec(tb, q)
     for mode in ("1", "0"):
-        os.environ["KIFMM_SYM"] = mode
-        try:
-            gp = gpu_plan(pts, 4, 24, 64, tb=tb)
-        finally:
-            del os.environ["KIFMM_SYM"]
+        gp = gpu_plan(pts, 4, 24, 64, tb=tb, near_mode=int(mode))
         out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
         assert par(out, ref) <= TOL, mode
 

@@ -1,5 +1,5 @@
-"""Near-field mode comparison on the GPU (diagnostics): one-sided (KIFMM_SYM=0),
-warp-pair symmetric (KIFMM_SYM=2) and mutual segments (default).
+"""Near-field mode comparison on the GPU (diagnostics): fmm_options.near_mode 0 (one-sided),
+2 (warp-pair symmetric) and 1 (mutual leaf pairs, the default).
 
     python tools/near_modes.py C2 [reps]
 """
@@ -23,8 +23,7 @@ P = torch.from_numpy(pts).to(dev)
 Q = torch.from_numpy(q).to(dev)
 res, outs = {}, {}
 for mode in modes:
-    os.environ["KIFMM_SYM"] = mode
-    plan = K.Plan(P, Q, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True)
+    plan = K.Plan(P, Q, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True, near_mode=int(mode))
     out = plan.matvec(Q)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
