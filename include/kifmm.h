@@ -159,6 +159,7 @@ typedef struct {
                                  mutual pair, 1 per one-sided pair (mutual mode; 0 otherwise) */
   double near_ms;             /* last profiled matvec: the near-field (P2P) launches alone, ms
                                  (CUDA events on the launching stream; -1 when not profiled) */
+  int64_t overlap;            /* the overlap mode the plan runs (fmm_options.overlap after defaults) */
 } fmm_info_t;
 
 /* fmm_options with every default filled in. */

@@ -56,7 +56,8 @@ class Info(ctypes.Structure):
                 ("m2l_rank_mean", ctypes.c_double), ("bem_near_bytes", ctypes.c_int64),
                 ("bem_extrusion", ctypes.c_double), ("near_mutual_leaves", ctypes.c_int64),
                 ("near_mutual_pairs", ctypes.c_int64), ("near_sym_pairs", ctypes.c_int64),
-                ("m2l_exec_flops", ctypes.c_double), ("near_pairs", ctypes.c_int64), ("near_ms", ctypes.c_double)]
+                ("m2l_exec_flops", ctypes.c_double), ("near_pairs", ctypes.c_int64), ("near_ms", ctypes.c_double),
+                ("overlap", ctypes.c_int64)]
 
 
 # phases of fmm_matvec (profile=True): the near field is evaluated in the "eval" pass together with

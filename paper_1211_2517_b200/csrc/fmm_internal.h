@@ -143,6 +143,15 @@ struct Exchange {
   double* d_recv = nullptr;
 };
 
+// bulk-copy streamed leaf-operator GEMV (stream.cu): items (first row, rows, first weight /
+// output point, output box) and per-CTA item ranges
+struct StreamPlan {
+  int4* d_items = nullptr;
+  int* d_cta = nullptr;
+  int nitems = 0, ncta = 0;
+  int64_t rows = 0;
+};
+
 struct Plan {
   int device = 0;
   int p = 0, k = 0, kp = 0, n = 0, leaf_size = 0, wx = 0;
@@ -221,6 +230,11 @@ struct Plan {
   int4* d_xt_items = nullptr;   // (target box, first row, end row, 0)
   double* d_s2m_mat = nullptr;
   double* d_l2t_mat = nullptr;
+  // slim path (overlap mode 3, one rank, every leaf operator built): S2M and X stream beside
+  // k_near part 1, L2T beside part 2, through the single-warp bulk-copy kernels of stream.cu
+  bool slim = false, slim_ready = false;
+  StreamPlan sw_s2m, sw_x, sw_l2t;
+  double* d_q_sorted = nullptr;  // N + 2 densities in sorted order (the streamed weights)
   int64_t leaf_op_bytes = 0;
   int n_s2m = 0; int4* d_s2m_items = nullptr; int* d_s2m_off = nullptr; int4* d_s2m_seg = nullptr;
   int n_xnd = 0; int4* d_x_items = nullptr;   int* d_x_off = nullptr;   int4* d_x_seg = nullptr;
@@ -310,6 +324,10 @@ extern int g_num_sms;
 extern int g_launches;
 int near_launch(const Plan& P, double* out, cudaStream_t st, int part = 0, int spare = 0);
 int build_schedules(Plan& P, cudaStream_t st);
+int stream_plan(Plan& P, StreamPlan& S, const std::vector<int4>& items, cudaStream_t st);
+int stream_s2m(const Plan& P, cudaStream_t st);
+int stream_x(const Plan& P, cudaStream_t st);
+int stream_l2t(const Plan& P, double* pot, cudaStream_t st);
 int upload_tables(Plan& P);
 int kernels_init();
 int ggs_tile_width(int M, int K);

@@ -1061,15 +1061,25 @@ __global__ void __launch_bounds__(L2T_WARPS * 32) k_l2t_leafop(const int4* __res
   }
 }
 
+// densities into the sorted points (and, slim plans, a contiguous sorted copy: the weights
+// the streamed S2M / X GEMVs bulk-copy)
 __global__ void k_set_density(double4* __restrict__ pts, const int32_t* __restrict__ perm, const double* __restrict__ q,
-                              int64_t N) {
+                              int64_t N, double* __restrict__ qs) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < N) pts[i].w = q[perm[i]];
+  if (i < N) {
+    const double v = q[perm[i]];
+    pts[i].w = v;
+    if (qs) qs[i] = v;
+  }
 }
 
-__global__ void k_set_density_owned(double4* __restrict__ pts, const double* __restrict__ q, int lo, int cnt) {
+__global__ void k_set_density_owned(double4* __restrict__ pts, const double* __restrict__ q, int lo, int cnt,
+                                    double* __restrict__ qs) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < cnt) pts[lo + i].w = q[i];
+  if (i < cnt) {
+    pts[lo + i].w = q[i];
+    if (qs) qs[lo + i] = q[i];
+  }
 }
 
 __global__ void k_gather_output(const double* __restrict__ pnear, const double* __restrict__ pfar,
@@ -1837,10 +1847,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       ++g_launches;
       if (owned) {
         const int cnt = Dp.own_hi - Dp.own_lo;
-        if (cnt > 0) k_set_density_owned<<<nblk(cnt), 256, 0, st>>>(T.d_pts, d_density, Dp.own_lo, cnt);
+        if (cnt > 0)
+          k_set_density_owned<<<nblk(cnt), 256, 0, st>>>(T.d_pts, d_density, Dp.own_lo, cnt,
+                                                         P.slim ? P.d_q_sorted : nullptr);
         if (pack(pts_w, 4, P.xd.d_send_idx, P.xd.nsend, 1, P.xd.d_send, st)) return -3;
       } else {
-        k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N);
+        k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N, P.slim ? P.d_q_sorted : nullptr);
       }
       KIFMM_CUDA(cudaGetLastError());
       return 0;
@@ -1869,10 +1881,20 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
           if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
         }
       }
+      if (P.slim) {  // mode 4: k_near part 1 from the fork, beside the streamed S2M and X
+        KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
+        KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, P.stream_near));
+        if (near_launch(P, P.d_pot_near, P.stream_near, 1, 0)) return -3;
+      }
       KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       mark(1);
-      if (P.leaf_s2m) {  // S2M as one GEMV per leaf with its precomputed operator
+      if (P.slim) {
+        // S2M stored into q^'; X added into l^ (zeroed above; the M2L adds with RED later)
+        KIFMM_CUDA(cudaMemsetAsync(P.d_pot_far, 0, sizeof(double) * N, st));
+        if (stream_s2m(P, st) || stream_x(P, st)) return -3;
+      } else if (P.leaf_s2m) {  // S2M as one GEMV per leaf with its precomputed operator
         if (P.n_s2m > 0) {
           ++g_launches;
           // 4 rows per lane in flight when a row is a power-of-two number of 32-byte lane
@@ -1914,6 +1936,22 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
       }
       mark(4);
+      if (P.slim) {  // mode 4: W (M2T) before the M2L — q_u = r_A U q^'_A, then the far pass
+        // adds its surfaces' fields to pot_far (zeroed in stage 1; the streamed L2T adds later)
+        if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
+        if (P.n_fitems > 0) {
+          EvalArgs a = ea;
+          a.accumulate = 1;
+          a.nrm = nullptr;  // far sources are equivalent surfaces: single layer
+          a.tri = nullptr;
+          a.items = P.d_fitems; a.seg_off = P.d_fitem_off; a.segs = P.d_fitem_seg;
+          a.out = P.d_pot_far;
+          a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
+          launch_eval(P, a, 0, st, false, P.n_fitems);
+          ++g_launches;
+          KIFMM_CUDA(cudaGetLastError());
+        }
+      }
       // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
       //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
       // overlap mode 2: M2L on the plan's high-priority stream (its persistent CTAs are
@@ -1943,8 +1981,10 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
       }
       mark(5);
-      // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
-      if (P.leaf_x && P.n_xt > 0) {
+      // X list (S2L): check potentials on DC of the target, then U^T projection (atomic);
+      // mode 4 streamed it in stage 1
+      if (P.slim) {
+      } else if (P.leaf_x && P.n_xt > 0) {
         ++g_launches;
         if (kp <= 64 && ((kp / 4) & (kp / 4 - 1)) == 0)
           k_x_gemv<4><<<(P.n_xt + 7) / 8, 256, 0, st>>>(P.d_xt_items, P.n_xt, P.d_x_seg, P.d_x_moff, T.d_pts, P.d_x_mat,
@@ -1970,6 +2010,13 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       // near field as its own pass (split_phases: phase exports; double layer: its own
       // kernel) unless it runs on the overlapped near stream
       const bool sep = P.split_phases || P.overlap || P.d_nrm || P.bem;
+      if (P.slim) {  // mode 4: k_near part 2 from here, beside the streamed L2T (adds to pot_far)
+        KIFMM_CUDA(cudaEventRecord(P.ev_m2l, st));
+        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_m2l, 0));
+        if (near_launch(P, P.d_pot_near, P.stream_near, 2, 0)) return -3;
+        KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
+        if (stream_l2t(P, P.d_pot_far, st)) return -3;
+      } else {
       if (P.bem) {  // BEM near field: the precomputed element-integral blocks
         if (P.overlap != 3) {  // (overlapped: launched on the near stream at the fork)
           ++g_launches;
@@ -2023,6 +2070,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaGetLastError());
       }
       if (!sep && launch_sym(P, st)) return -3;
+      }  // (not mode 4)
       if (sep && !P.split_phases) {  // [join the near stream,] then pot_near += pot_far on the owned points
         if (P.overlap) KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_join, 0));
         const int cnt = Dp.own_hi - Dp.own_lo;

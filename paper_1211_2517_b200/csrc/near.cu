@@ -427,6 +427,10 @@ template <int TB, int MQ, bool DL>
 int near_launch_one(const NearArgs& a, int count, int spare, cudaStream_t st) {
   static int per_sm = -1;
   if (per_sm < 0) {
+    // the largest shared-memory carveout: 5 CTAs of ~40 KB need more than the 168 KB the
+    // driver's default choice gives a kernel with static shared memory only
+    cudaFuncSetAttribute(k_near<TB, MQ, DL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_near<TB, MQ, DL>, NR_NT, 0) != cudaSuccess) per_sm = 1;
     per_sm = std::max(1, per_sm);
   }

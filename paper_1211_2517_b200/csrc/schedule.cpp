@@ -756,6 +756,33 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (build_leaf_ops(P, st)) return -3;
   }
   mark("leaf operators");
+  // ---- work lists of the bulk-copy streamed GEMVs (stream.cu; the slim overlap path): one
+  // rank (no ghost densities in the streamed weights), every leaf operator the matvec needs
+  P.slim_ready = false;
+  if (Dp.nranks == 1 && !P.bem && P.leaf_s2m && P.leaf_l2t && (xitems.empty() || P.leaf_x)) {
+    std::vector<int4> s2m, xw, l2t;
+    s2m.reserve(sitems.size());
+    for (const int4& it : sitems) {
+      const int b = it.x;
+      s2m.push_back(make_int4(T.pbeg[b] - Dp.own_lo, npts(b), T.pbeg[b], b));
+    }
+    std::sort(s2m.begin(), s2m.end(), [](const int4& a, const int4& b) { return a.x < b.x; });
+    int64_t xrow = 0;  // X operator rows: items in X-list order, grouped by target
+    for (size_t r = 0; r < xitems.size(); ++r) {
+      xw.push_back(make_int4((int)xrow, xsegs[r].w, xsegs[r].y, xitems[r].x));
+      xrow += xsegs[r].w;
+    }
+    for (const int4& ti : titems) {
+      const int b = ti.x;
+      if (T.level[b] >= 2) l2t.push_back(make_int4(T.pbeg[b] - Dp.own_lo, npts(b), T.pbeg[b], b));
+    }
+    std::sort(l2t.begin(), l2t.end(), [](const int4& a, const int4& b) { return a.x < b.x; });
+    if (xrow > INT32_MAX || stream_plan(P, P.sw_s2m, s2m, st) || stream_plan(P, P.sw_x, xw, st) ||
+        stream_plan(P, P.sw_l2t, l2t, st) || zalloc(&P.d_q_sorted, (size_t)T.N + 2))
+      return -3;
+    P.slim_ready = true;
+  }
+  mark("stream lists");
   KIFMM_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
