@@ -117,10 +117,11 @@ typedef struct {
                          0 = one-sided per target leaf (k_eval); 2 = warp-pair symmetric
                          (k_p2p_sym; single layer only, else 0).  Same result to rounding. */
   int overlap;        /* near field beside the far field on a second plan stream: -1 (default) =
-                         3 up to 8M owned points, else 0; 0 = serialised; 3 = k_near (or the BEM
-                         near-field SpMV) forked at the densities (NCCL plans: after the ghost
-                         exchange); 1 / 2 = the one-sided near field forked at the densities /
-                         beside a high-priority M2L stream.  Profiled and split-phase plans: 0. */
+                         3 up to 8M owned points, else 0; 0 = serialised; 3 = k_near (or the
+                         BEM near-field SpMV) forked at the densities (NCCL plans: after the
+                         ghost exchange); 1 / 2 = the one-sided near field forked at the
+                         densities / beside a high-priority M2L stream.  Profiled and
+                         split-phase plans: 0. */
 } fmm_options;
 
 typedef struct {

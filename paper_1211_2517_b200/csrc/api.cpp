@@ -59,6 +59,8 @@ void free_plan_memory(fmm_plan* h) {
   for (void* p : tp)
     if (p) cudaFree(p);
   for (auto e : P.ev_phase) cudaEventDestroy(e);
+  for (auto e : P.ev_trace) cudaEventDestroy(e);
+  P.ev_trace.clear();
   P.ev_phase.clear();
   if (P.ev_fork) cudaEventDestroy(P.ev_fork);
   if (P.ev_join) cudaEventDestroy(P.ev_join);
@@ -333,38 +335,23 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
       }
     }
     // Near field on a second stream (overlap modes, fmm_options.overlap):
-    //  4 (default when the streamed GEMVs are available: one rank, every leaf operator built):
-    //    k_near part 1 from the fork after the densities beside the single-warp bulk-copy
-    //    S2M and X GEMVs (stream.cu), part 2 after the L2L beside the streamed L2T; the W
-    //    far pass runs before the M2L.  The FP64-bound near field and the HBM-bound leaf
-    //    GEMVs share the SMs instead of taking turns.
-    //  3 (default otherwise, up to 8M owned points): all of k_near from the fork, beside the
-    //    full-occupancy S2M / M2M GEMVs, which wait for free SM slots (C2 -2.5%, C3 -10%;
-    //    C4 / C5 +-1%: their long launches leave little tail to fill).  NCCL plans fork
-    //    after the ghost exchange.
+    //  3 (default with the mutual near field, up to 8M owned points): all of k_near from the
+    //    fork after the densities on the near stream, beside the far field (the GEMVs take
+    //    SM slots as k_near's CTAs drain); results joined before the output (C2 -2.5%,
+    //    C3 -10%; C4 / C5 +-1%: their long launches leave little tail to fill).  NCCL plans
+    //    fork after the ghost exchange.
     //  1 / 2 (diagnostics, k_eval era): whole near field forked after the densities /
     //    beside a high-priority M2L stream.
     //  Off (0) in profiled and split-phase plans: per-phase events on one stream need the
     //  phases serialised.
+    //  (A mode running k_near in two parts beside single-warp bulk-copy GEMVs sized to fit
+    //  next to it was measured slower — C4 25.2 vs 21.8 ms: DESIGN.md §5.)
     {
       const int64_t owned = P.dist.own_hi - P.dist.own_lo;
-      const bool base_ok = (P.nr_on || P.bem) && !P.profile;
-      const int ovl_default = !base_ok ? 0 : (P.slim_ready && P.nr_on) ? 4 : owned <= (int64_t)8 << 20 ? 3 : 0;
-      P.overlap = !P.split_phases ? (opt->overlap >= 0 ? opt->overlap : ovl_default) : 0;
+      const bool ovl_default = (P.nr_on || P.bem) && !P.profile && owned <= (int64_t)8 << 20;
+      P.overlap = !P.split_phases ? (opt->overlap >= 0 ? opt->overlap : (ovl_default ? 3 : 0)) : 0;
       if (P.bem && P.overlap != 3) P.overlap = 0;         // BEM: only the SpMV fork (mode 3)
-      if (P.overlap == 4 && !(P.slim_ready && P.nr_on)) P.overlap = P.nr_on ? 3 : 0;
       if (P.overlap == 3 && !P.nr_on && !P.bem) P.overlap = 0;  // mode 3 runs k_near or the BEM SpMV
-      P.slim = P.overlap == 4;
-      if (P.slim) {
-        // share of every k_near group launched at the fork: enough near-field work to cover
-        // the streamed S2M + X (bytes at ~4 TB/s beside k_near) with 20% margin; the rest
-        // runs after the L2L beside the streamed L2T (k_near: ~11 T FP64 instr-lanes/s)
-        const double gemv_s = (double)(P.sw_s2m.rows + P.sw_x.rows) * P.kp * 8.0 / 4.0e12;
-        const double near_s = (13.0 * (double)P.n_mut_pairs + 12.0 * (double)(P.n_near_pairs - 2 * P.n_mut_pairs)) /
-                              1.1e13;
-        P.nr_split = near_s > 0 ? std::min(0.95, std::max(0.05, 1.2 * gemv_s / near_s)) : 0.5;
-        if (const char* e = std::getenv("KIFMM_NEAR_SPLIT")) P.nr_split = std::atof(e);  // TEMP (tuning)
-      }
       int lo_prio = 0, hi_prio = 0;
       cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
       if (P.overlap &&

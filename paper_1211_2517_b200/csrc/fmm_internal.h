@@ -230,9 +230,9 @@ struct Plan {
   int4* d_xt_items = nullptr;   // (target box, first row, end row, 0)
   double* d_s2m_mat = nullptr;
   double* d_l2t_mat = nullptr;
-  // slim path (overlap mode 3, one rank, every leaf operator built): S2M and X stream beside
-  // k_near part 1, L2T beside part 2, through the single-warp bulk-copy kernels of stream.cu
-  bool slim = false, slim_ready = false;
+  // the leaf-operator GEMVs (S2M, X, L2T) streamed by bulk copies (stream.cu): one rank,
+  // every leaf operator the matvec needs built
+  bool stream_ok = false;
   StreamPlan sw_s2m, sw_x, sw_l2t;
   double* d_q_sorted = nullptr;  // N + 2 densities in sorted order (the streamed weights)
   int64_t leaf_op_bytes = 0;
@@ -257,6 +257,7 @@ struct Plan {
   bool near_timed = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_phase;
+  std::vector<cudaEvent_t> ev_trace;  // KIFMM_TRACE=1 diagnostics (kernels.cu)
   bool profile = false;
   bool profiled = false;
   int launches = 0;       // kernels of this library launched by the last matvec

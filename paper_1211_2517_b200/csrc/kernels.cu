@@ -11,6 +11,7 @@
 //             rsqrt: near-field P2P (S2T), S2M / X check potentials,
 //             L2T / W potentials from equivalent densities.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include <nvtx3/nvToolsExt.h>
@@ -1807,6 +1808,47 @@ int unpack(double* dst, int ld, const int* idx, int nrows, int row, const double
 }
 }  // namespace
 
+// Diagnostics (KIFMM_TRACE=1, stderr only): events on both streams around the launches of
+// one matvec, printed relative to its start after the matvec completes — the only view of
+// the two-stream timeline without a tracing tool in this image.
+namespace {
+struct Trace {
+  Plan* P = nullptr;
+  int n = 0;
+  const char* names[32];
+  void begin(Plan& p) {
+    static const bool on = std::getenv("KIFMM_TRACE") != nullptr;
+    P = nullptr;
+    n = 0;
+    if (!on) return;
+    if (p.ev_trace.empty()) {
+      p.ev_trace.resize(32);
+      for (auto& e : p.ev_trace) cudaEventCreate(&e);
+    }
+    P = &p;
+  }
+  void mark(const char* name, cudaStream_t s) {
+    if (!P || n >= 32) return;
+    names[n] = name;
+    cudaEventRecord(P->ev_trace[n++], s);
+  }
+  void dump() {
+    if (!P || n == 0) return;
+    cudaDeviceSynchronize();
+    std::fprintf(stderr, "kifmm trace:");
+    for (int i = 0; i < n; ++i) {
+      float ms = -1;
+      cudaError_t e = cudaEventElapsedTime(&ms, P->ev_trace[0], P->ev_trace[i]);
+      std::fprintf(stderr, " %s=%.3f%s", names[i], ms, e == cudaSuccess ? "" : cudaGetErrorString(e));
+    }
+    std::fprintf(stderr, "\n");
+    (void)cudaGetLastError();
+    P = nullptr;
+  }
+};
+Trace g_trace;
+}  // namespace
+
 // Profile events (fmm_info.phase_ms): 0 density (+ghost densities) | 1 S2M | 2 M2M |
 // 3 exchange (straddlers + ghost q^') | 4 M2L | 5 X | 6 L2L | 7 evaluation (L2T, W, P2P) | 8 output
 int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st) {
@@ -1849,10 +1891,10 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         const int cnt = Dp.own_hi - Dp.own_lo;
         if (cnt > 0)
           k_set_density_owned<<<nblk(cnt), 256, 0, st>>>(T.d_pts, d_density, Dp.own_lo, cnt,
-                                                         P.slim ? P.d_q_sorted : nullptr);
+                                                         P.stream_ok ? P.d_q_sorted : nullptr);
         if (pack(pts_w, 4, P.xd.d_send_idx, P.xd.nsend, 1, P.xd.d_send, st)) return -3;
       } else {
-        k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N, P.slim ? P.d_q_sorted : nullptr);
+        k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N, P.stream_ok ? P.d_q_sorted : nullptr);
       }
       KIFMM_CUDA(cudaGetLastError());
       return 0;
@@ -1881,19 +1923,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
           if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
         }
       }
-      if (P.slim) {  // mode 4: k_near part 1 from the fork, beside the streamed S2M and X
-        KIFMM_CUDA(cudaEventRecord(P.ev_fork, st));
-        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
-        KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, P.stream_near));
-        if (near_launch(P, P.d_pot_near, P.stream_near, 1, 0)) return -3;
-      }
       KIFMM_CUDA(cudaMemsetAsync(P.d_qhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       KIFMM_CUDA(cudaMemsetAsync(P.d_lhat, 0, sizeof(double) * (size_t)T.nboxes * kp, st));
       mark(1);
-      if (P.slim) {
-        // S2M stored into q^'; X added into l^ (zeroed above; the M2L adds with RED later)
-        KIFMM_CUDA(cudaMemsetAsync(P.d_pot_far, 0, sizeof(double) * N, st));
-        if (stream_s2m(P, st) || stream_x(P, st)) return -3;
+      g_trace.mark("s2m_begin", st);
+      if (P.stream_ok) {  // S2M streamed by bulk copies (stream.cu), stored into q^'
+        if (stream_s2m(P, st)) return -3;
       } else if (P.leaf_s2m) {  // S2M as one GEMV per leaf with its precomputed operator
         if (P.n_s2m > 0) {
           ++g_launches;
@@ -1935,23 +1970,8 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaMemsetAsync(P.d_pot_near, 0, sizeof(double) * N, P.stream_near));
         if (near_launch(P, P.d_pot_near, P.stream_near, 1, P.nr_spare)) return -3;
       }
+      g_trace.mark("m2m_end", st);
       mark(4);
-      if (P.slim) {  // mode 4: W (M2T) before the M2L — q_u = r_A U q^'_A, then the far pass
-        // adds its surfaces' fields to pot_far (zeroed in stage 1; the streamed L2T adds later)
-        if (launch_ggs(P.g_w, P.d_Ue, 0, np, kp, n, P.d_qhat, kp, P.d_eqd_w, np, false, st)) return -3;
-        if (P.n_fitems > 0) {
-          EvalArgs a = ea;
-          a.accumulate = 1;
-          a.nrm = nullptr;  // far sources are equivalent surfaces: single layer
-          a.tri = nullptr;
-          a.items = P.d_fitems; a.seg_off = P.d_fitem_off; a.segs = P.d_fitem_seg;
-          a.out = P.d_pot_far;
-          a.eqd1 = P.d_eqd_l2t; a.eqd2 = P.d_eqd_w;
-          launch_eval(P, a, 0, st, false, P.n_fitems);
-          ++g_launches;
-          KIFMM_CUDA(cudaGetLastError());
-        }
-      }
       // M2L, all levels in one launch per kernel: l^_B += C_delta q^'_A
       //   dense sibling groups (one RED per (target, delta)), then the sparse remainder by offset
       // overlap mode 2: M2L on the plan's high-priority stream (its persistent CTAs are
@@ -1980,10 +2000,12 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         if (near_launch(P, P.d_pot_near, P.stream_near, 2, P.nr_spare)) return -3;
         KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
       }
+      g_trace.mark("m2l_end", st);
       mark(5);
-      // X list (S2L): check potentials on DC of the target, then U^T projection (atomic);
-      // mode 4 streamed it in stage 1
-      if (P.slim) {
+      // X list (S2L): check potentials on DC of the target, then U^T projection (atomic)
+      g_trace.mark("x_begin", st);
+      if (P.stream_ok) {  // streamed by bulk copies, added into l^ with RED
+        if (stream_x(P, st)) return -3;
       } else if (P.leaf_x && P.n_xt > 0) {
         ++g_launches;
         if (kp <= 64 && ((kp / 4) & (kp / 4 - 1)) == 0)
@@ -2010,13 +2032,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       // near field as its own pass (split_phases: phase exports; double layer: its own
       // kernel) unless it runs on the overlapped near stream
       const bool sep = P.split_phases || P.overlap || P.d_nrm || P.bem;
-      if (P.slim) {  // mode 4: k_near part 2 from here, beside the streamed L2T (adds to pot_far)
-        KIFMM_CUDA(cudaEventRecord(P.ev_m2l, st));
-        KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_m2l, 0));
-        if (near_launch(P, P.d_pot_near, P.stream_near, 2, 0)) return -3;
-        KIFMM_CUDA(cudaEventRecord(P.ev_join, P.stream_near));
-        if (stream_l2t(P, P.d_pot_far, st)) return -3;
-      } else {
+      g_trace.mark("l2l_end", st);
       if (P.bem) {  // BEM near field: the precomputed element-integral blocks
         if (P.overlap != 3) {  // (overlapped: launched on the near stream at the fork)
           ++g_launches;
@@ -2034,7 +2050,11 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       // overlapped on the near stream), else everything fused into pot_near
       double* far_out = sep ? P.d_pot_far : P.d_pot_near;
       // leaf-op mode: L2T as one GEMV per leaf, stored; the evaluation pass below adds to it
-      if (P.leaf_l2t && P.n_tleaf > 0) {
+      if (P.stream_ok) {  // streamed by bulk copies, added into the zeroed potentials
+        KIFMM_CUDA(cudaMemsetAsync(far_out, 0, sizeof(double) * N, st));
+        if (stream_l2t(P, far_out, st)) return -3;
+        g_trace.mark("l2t_end", st);
+      } else if (P.leaf_l2t && P.n_tleaf > 0) {
         ++g_launches;
         k_l2t_leafop<<<(P.n_tleaf + L2T_WARPS - 1) / L2T_WARPS, L2T_WARPS * 32, 0, st>>>(
             P.d_tleaf_items, P.n_tleaf, T.d_level, T.d_pbeg, T.d_pend, P.d_l2t_mat, P.d_lhat, kp, Dp.own_lo, far_out);
@@ -2070,7 +2090,6 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaGetLastError());
       }
       if (!sep && launch_sym(P, st)) return -3;
-      }  // (not mode 4)
       if (sep && !P.split_phases) {  // [join the near stream,] then pot_near += pot_far on the owned points
         if (P.overlap) KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_join, 0));
         const int cnt = Dp.own_hi - Dp.own_lo;
@@ -2080,6 +2099,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
           KIFMM_CUDA(cudaGetLastError());
         }
       }
+      g_trace.mark("joined", st);
       mark(8);
       if (owned) {
         const int cnt = Dp.own_hi - Dp.own_lo;
@@ -2109,6 +2129,11 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
 // One matvec of a single-GPU plan, or of one rank of an NCCL-connected plan.
 int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st) {
   const bool dist = P.nccl_comm != nullptr;
+  g_trace.begin(P);
+  g_trace.mark("start", st);
+  struct Dump {
+    ~Dump() { g_trace.dump(); }
+  } dump_at_exit;
   if (matvec_stage(P, 0, d_density, d_pot, owned, st)) return -3;
   if (dist && owned && nccl_exchange(P, P.xd, st)) return -5;
   if (matvec_stage(P, 1, d_density, d_pot, owned, st)) return -3;

@@ -756,9 +756,9 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (build_leaf_ops(P, st)) return -3;
   }
   mark("leaf operators");
-  // ---- work lists of the bulk-copy streamed GEMVs (stream.cu; the slim overlap path): one
-  // rank (no ghost densities in the streamed weights), every leaf operator the matvec needs
-  P.slim_ready = false;
+  // ---- work lists of the bulk-copy streamed GEMVs (stream.cu): one rank (the streamed
+  // weights are a sorted copy of the owned densities: no ghosts), every leaf operator built
+  P.stream_ok = false;
   if (Dp.nranks == 1 && !P.bem && P.leaf_s2m && P.leaf_l2t && (xitems.empty() || P.leaf_x)) {
     std::vector<int4> s2m, xw, l2t;
     s2m.reserve(sitems.size());
@@ -780,7 +780,7 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (xrow > INT32_MAX || stream_plan(P, P.sw_s2m, s2m, st) || stream_plan(P, P.sw_x, xw, st) ||
         stream_plan(P, P.sw_l2t, l2t, st) || zalloc(&P.d_q_sorted, (size_t)T.N + 2))
       return -3;
-    P.slim_ready = true;
+    P.stream_ok = true;
   }
   mark("stream lists");
   KIFMM_CUDA(cudaStreamSynchronize(st));

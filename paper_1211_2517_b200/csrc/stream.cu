@@ -1,25 +1,23 @@
-// Leaf-operator GEMVs (S2M, X, L2T) streamed through shared memory by bulk copies, one
-// warp per CTA — sized to run BESIDE the FP64-bound near field (k_near).
+// Leaf-operator GEMVs (S2M, X, L2T) streamed through shared memory by bulk copies.
 //
 // The three leaf-level translations with per-leaf operators (DESIGN.md §5 "leaf-op mode")
 // read kp doubles per point and per operator from HBM and do ~1 FMA per double: HBM-bound
-// (C4: 8.6 GB for S2M, 8.6 GB for L2T, 3.7 GB for X per matvec).  k_near is bound by the
-// FP64 pipe and reads little from HBM.  With full-occupancy GEMV kernels the two cannot
-// share an SM (k_near's CTAs hold the register file), so the matvec ran them one after the
-// other.  Here each GEMV is a persistent grid of single-warp CTAs (<= 64 registers, ~23 KB
-// of shared memory) that fits into what k_near leaves free: lane 0 issues
-// cp.async.bulk copies (SASS UBLKCP) of contiguous operator rows — plus the chunk's
-// densities (S2M, X) or the item's local expansion (L2T) — into an NS-stage ring, each stage
-// completing on its own mbarrier (expect_tx bytes); the warp consumes stage s while the
-// copies of the next NS - 1 stages are in flight, then refills s.  The waits are
-// mbarrier.try_wait (a suspended wait, not a spin that would steal issue slots from the
-// FP64 warps beside it).
+// (C4: 8.6 GB each for S2M and L2T, 3.7 GB for X per matvec).  Each is a persistent grid of
+// single-warp CTAs, kStreamCtaPerSm per SM: lane 0 issues cp.async.bulk copies (SASS
+// UBLKCP) of contiguous operator rows — plus the chunk's densities (S2M, X) or the item's
+// local expansion (L2T) — into an NS-stage shared-memory ring, each stage completing on its
+// own mbarrier (expect_tx bytes); the warp consumes stage s while the next NS - 1 stages are
+// in flight, then refills s.  ~200 KB in flight per SM keeps HBM busy with four warps per
+// SM (the register-path GEMVs needed 64 warps per SM in flight for 79-94% of the copy
+// bandwidth).  The waits are mbarrier.try_wait (suspended, not spinning).
 //
 // Work: an item = (first operator row, rows, first weight / output point, output box):
 //   S2M  q^'_B  = sum_j q_j S_B[j]   store      (MODE 0)
 //   X    l^_B  += sum_j q_j X_(B,A)[j]     (projection)       RED        (MODE 0)
 //   L2T  pot_j += T_B[j] . l^_B        add        (MODE 1)
 // Each CTA streams a contiguous range of items (host-balanced by rows, stream_plan below).
+// (Single-warp CTAs sized to run beside k_near instead — 1 per SM, ~23 KB — reached only
+// 1-2 TB/s and slowed k_near: measured slower overall.)
 #include <algorithm>
 #include <vector>
 
@@ -32,15 +30,19 @@ namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// rows per stage (the stage also holds up to max(KP, RS + 2) doubles of weights / vector)
+constexpr int kStreamCtaPerSm = 4;
+
+// rows per stage (the stage also holds up to max(KP, RS + 2) doubles of weights / vector);
+// 4 CTAs x NS stages x ~8.7 KB per SM
 template <int KP>
 struct StreamShape {
-  static constexpr int RS = KP <= 64 ? 14 : 8;
-  static constexpr int NS = 3;
+  static constexpr int RS = KP <= 64 ? 16 : 10;
+  static constexpr int NS = 6;
   static constexpr int EXTRA = (KP > RS + 2 ? KP : RS + 2);
   static constexpr int STAGE = (RS * KP + EXTRA) * 8;  // bytes (multiple of 16)
   static constexpr int T = (KP + 63) / 64;            // double2 column units per lane
   static_assert(STAGE % 16 == 0, "bulk copies move multiples of 16 bytes");
+  static_assert(RS <= 16, "the L2T reduce-scatter handles 16 rows per stage");
 };
 
 struct StreamArgs {
@@ -289,7 +291,7 @@ int stream_plan(Plan& P, StreamPlan& S, const std::vector<int4>& items, cudaStre
   if (items.empty()) return 0;
   int64_t total = 0;
   for (const int4& it : items) total += it.y;
-  const int ncta = std::max(1, std::min(g_num_sms, S.nitems));
+  const int ncta = std::max(1, std::min(kStreamCtaPerSm * g_num_sms, S.nitems));
   std::vector<int> cta(ncta + 1, S.nitems);
   cta[0] = 0;
   int64_t acc = 0;

@@ -219,18 +219,16 @@ def test_edge_cases():
 
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k", "torus50k"])
-@pytest.mark.parametrize("mode", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
 def test_overlapped_near_stream(case, mode):
     # near field on a second stream joined before the output (mode 3: all of k_near from the
-    # fork; mode 4: k_near split around the far field, beside the bulk-copy streamed S2M / X /
-    # L2T GEMVs); repeated matvecs reuse the streams and events
+    # fork, beside the S2M / M2M GEMVs); repeated matvecs reuse the streams and events
     pts, q, p, k, s = CASES[case]()
     tb = tables(p, k)
     ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q)
     for lo in (0, 1):
         gp = gpu_plan(pts, p, k, s, tb=tb, leaf_ops=lo, overlap=int(mode))
-        # mode 4 (streamed leaf GEMVs) needs the leaf operators; without them it falls back to 3
-        assert gp.info["overlap"] == (3 if mode == "4" and not lo else int(mode))
+        assert gp.info["overlap"] == int(mode)
         for _ in range(2):
             out = gp.matvec(torch.from_numpy(q).cuda()).cpu().numpy()
             assert par(out, ref) <= TOL
