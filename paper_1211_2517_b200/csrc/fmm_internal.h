@@ -230,10 +230,10 @@ struct Plan {
   int4* d_xt_items = nullptr;   // (target box, first row, end row, 0)
   double* d_s2m_mat = nullptr;
   double* d_l2t_mat = nullptr;
-  // the leaf-operator GEMVs (S2M, X, L2T) streamed by bulk copies (stream.cu): one rank,
-  // every leaf operator the matvec needs built
+  // the upward leaf-operator GEMVs (S2M, X) streamed by bulk copies (stream.cu): one rank,
+  // S2M (and X, if any) operators built
   bool stream_ok = false;
-  StreamPlan sw_s2m, sw_x, sw_l2t;
+  StreamPlan sw_s2m, sw_x;
   double* d_q_sorted = nullptr;  // N + 2 densities in sorted order (the streamed weights)
   int64_t leaf_op_bytes = 0;
   int n_s2m = 0; int4* d_s2m_items = nullptr; int* d_s2m_off = nullptr; int4* d_s2m_seg = nullptr;
@@ -328,7 +328,6 @@ int build_schedules(Plan& P, cudaStream_t st);
 int stream_plan(Plan& P, StreamPlan& S, const std::vector<int4>& items, cudaStream_t st);
 int stream_s2m(const Plan& P, cudaStream_t st);
 int stream_x(const Plan& P, cudaStream_t st);
-int stream_l2t(const Plan& P, double* pot, cudaStream_t st);
 int upload_tables(Plan& P);
 int kernels_init();
 int ggs_tile_width(int M, int K);

@@ -2050,11 +2050,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
       // overlapped on the near stream), else everything fused into pot_near
       double* far_out = sep ? P.d_pot_far : P.d_pot_near;
       // leaf-op mode: L2T as one GEMV per leaf, stored; the evaluation pass below adds to it
-      if (P.stream_ok) {  // streamed by bulk copies, added into the zeroed potentials
-        KIFMM_CUDA(cudaMemsetAsync(far_out, 0, sizeof(double) * N, st));
-        if (stream_l2t(P, far_out, st)) return -3;
-        g_trace.mark("l2t_end", st);
-      } else if (P.leaf_l2t && P.n_tleaf > 0) {
+      if (P.leaf_l2t && P.n_tleaf > 0) {
         ++g_launches;
         k_l2t_leafop<<<(P.n_tleaf + L2T_WARPS - 1) / L2T_WARPS, L2T_WARPS * 32, 0, st>>>(
             P.d_tleaf_items, P.n_tleaf, T.d_level, T.d_pbeg, T.d_pend, P.d_l2t_mat, P.d_lhat, kp, Dp.own_lo, far_out);

@@ -757,10 +757,10 @@ int build_schedules(Plan& P, cudaStream_t st) {
   }
   mark("leaf operators");
   // ---- work lists of the bulk-copy streamed GEMVs (stream.cu): one rank (the streamed
-  // weights are a sorted copy of the owned densities: no ghosts), every leaf operator built
+  // weights are a sorted copy of the owned densities: no ghosts), S2M / X operators built
   P.stream_ok = false;
-  if (Dp.nranks == 1 && !P.bem && P.leaf_s2m && P.leaf_l2t && (xitems.empty() || P.leaf_x)) {
-    std::vector<int4> s2m, xw, l2t;
+  if (Dp.nranks == 1 && !P.bem && P.leaf_s2m && (xitems.empty() || P.leaf_x)) {
+    std::vector<int4> s2m, xw;
     s2m.reserve(sitems.size());
     for (const int4& it : sitems) {
       const int b = it.x;
@@ -772,13 +772,8 @@ int build_schedules(Plan& P, cudaStream_t st) {
       xw.push_back(make_int4((int)xrow, xsegs[r].w, xsegs[r].y, xitems[r].x));
       xrow += xsegs[r].w;
     }
-    for (const int4& ti : titems) {
-      const int b = ti.x;
-      if (T.level[b] >= 2) l2t.push_back(make_int4(T.pbeg[b] - Dp.own_lo, npts(b), T.pbeg[b], b));
-    }
-    std::sort(l2t.begin(), l2t.end(), [](const int4& a, const int4& b) { return a.x < b.x; });
     if (xrow > INT32_MAX || stream_plan(P, P.sw_s2m, s2m, st) || stream_plan(P, P.sw_x, xw, st) ||
-        stream_plan(P, P.sw_l2t, l2t, st) || zalloc(&P.d_q_sorted, (size_t)T.N + 2))
+        zalloc(&P.d_q_sorted, (size_t)T.N + 2))
       return -3;
     P.stream_ok = true;
   }

@@ -1,23 +1,24 @@
-// Leaf-operator GEMVs (S2M, X, L2T) streamed through shared memory by bulk copies.
+// Leaf-operator GEMVs of the upward side (S2M, X) streamed through shared memory by bulk
+// copies.
 //
-// The three leaf-level translations with per-leaf operators (DESIGN.md §5 "leaf-op mode")
-// read kp doubles per point and per operator from HBM and do ~1 FMA per double: HBM-bound
-// (C4: 8.6 GB each for S2M and L2T, 3.7 GB for X per matvec).  Each is a persistent grid of
-// single-warp CTAs, kStreamCtaPerSm per SM: lane 0 issues cp.async.bulk copies (SASS
-// UBLKCP) of contiguous operator rows — plus the chunk's densities (S2M, X) or the item's
-// local expansion (L2T) — into an NS-stage shared-memory ring, each stage completing on its
+// Both leaf-level translations with per-leaf operators (DESIGN.md §5 "leaf-op mode") read
+// kp doubles per source point and do one FMA per double: HBM-bound (C4: 8.6 GB for S2M,
+// 3.7 GB for X per matvec).  Each is a persistent grid of single-warp CTAs, kStreamCtaPerSm
+// per SM: lane 0 issues cp.async.bulk copies (SASS UBLKCP) of contiguous operator rows plus
+// the chunk's densities into an NS-stage shared-memory ring, each stage completing on its
 // own mbarrier (expect_tx bytes); the warp consumes stage s while the next NS - 1 stages are
-// in flight, then refills s.  ~200 KB in flight per SM keeps HBM busy with four warps per
-// SM (the register-path GEMVs needed 64 warps per SM in flight for 79-94% of the copy
-// bandwidth).  The waits are mbarrier.try_wait (suspended, not spinning).
+// in flight, then refills s.  ~200 KB in flight per SM keeps HBM busy with four warps per SM
+// (C4 S2M 6.2 TB/s, 1.39 ms, against 5.1 TB/s for the register-path GEMV).  The waits are
+// mbarrier.try_wait (suspended, not spinning).
 //
-// Work: an item = (first operator row, rows, first weight / output point, output box):
-//   S2M  q^'_B  = sum_j q_j S_B[j]   store      (MODE 0)
-//   X    l^_B  += sum_j q_j X_(B,A)[j]     (projection)       RED        (MODE 0)
-//   L2T  pot_j += T_B[j] . l^_B        add        (MODE 1)
+// Work: an item = (first operator row, rows, first weight point, output box):
+//   S2M  q^'_B  = sum_j q_j S_B[j]   store
+//   X    l^_B  += sum_j q_j X_(B,A)[j]     (projection)       RED
 // Each CTA streams a contiguous range of items (host-balanced by rows, stream_plan below).
-// (Single-warp CTAs sized to run beside k_near instead — 1 per SM, ~23 KB — reached only
-// 1-2 TB/s and slowed k_near: measured slower overall.)
+// Measured and not kept: the L2T dot-product form (a reduce-scatter
+// over the warp per 16 rows) reached 4.3 TB/s against 6.4 for k_l2t_leafop; single-warp
+// CTAs sized to run BESIDE k_near (1 per SM, ~23 KB) reached only 1-2 TB/s and slowed
+// k_near (C4 25.2 vs 21.8 ms).
 #include <algorithm>
 #include <vector>
 
@@ -32,7 +33,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 
 constexpr int kStreamCtaPerSm = 4;
 
-// rows per stage (the stage also holds up to max(KP, RS + 2) doubles of weights / vector);
+// rows per stage (the stage also holds up to max(KP, RS + 2) doubles of weights);
 // 4 CTAs x NS stages x ~8.7 KB per SM
 template <int KP>
 struct StreamShape {
@@ -42,23 +43,21 @@ struct StreamShape {
   static constexpr int STAGE = (RS * KP + EXTRA) * 8;  // bytes (multiple of 16)
   static constexpr int T = (KP + 63) / 64;            // double2 column units per lane
   static_assert(STAGE % 16 == 0, "bulk copies move multiples of 16 bytes");
-  static_assert(RS <= 16, "the L2T reduce-scatter handles 16 rows per stage");
 };
 
 struct StreamArgs {
   const int4* items;     // (first row, rows, first weight / output point, output box)
   const int* cta_begin;  // CTA c streams items [cta_begin[c], cta_begin[c + 1])
   const double* mat;     // operator rows, KP doubles each
-  const double* q;       // MODE 0: densities in sorted order (contiguous copy of pts.w)
-  const double* vin;     // MODE 1: per-box vectors (l^), KP doubles per box
-  double* out;           // MODE 0: per-box rows (q^' or l^); MODE 1: potentials (sorted)
+  const double* q;       // densities in sorted order (contiguous copy of pts.w)
+  double* out;           // per-box rows (q^' or l^)
 };
 
 // lane's double2 unit t covers columns 2 lane + 64 t, + 1
 template <int KP>
 __device__ __forceinline__ bool col_ok(int lane, int t) { return 2 * lane + 64 * t < KP; }
 
-template <int KP, int MODE, bool ATOMIC>
+template <int KP, bool ATOMIC>
 __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
   using SS = StreamShape<KP>;
   constexpr int RS = SS::RS, NS = SS::NS, T = SS::T;
@@ -84,18 +83,10 @@ __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
     if (lane == 0) {
       const uint32_t bar = smem_u32(&full[s]);
       const uint32_t rbytes = (uint32_t)nr * KP * 8;
-      // extra: MODE 0 the chunk's densities (an aligned pair-superset), MODE 1 on an item's
-      // first chunk its box's vector
-      const double* xsrc = nullptr;
-      uint32_t xbytes = 0;
-      if (MODE == 0) {
-        const long w0 = (long)iss_rec.z + iss_r, a0 = w0 & ~1L, a1 = (w0 + nr + 1) & ~1L;
-        xsrc = A.q + a0;
-        xbytes = (uint32_t)(a1 - a0) * 8;
-      } else if (iss_r == 0) {
-        xsrc = A.vin + (size_t)iss_rec.w * KP;
-        xbytes = KP * 8;
-      }
+      // the chunk's densities (an aligned pair-superset: bulk copies move 16-byte units)
+      const long w0 = (long)iss_rec.z + iss_r, a0 = w0 & ~1L, a1 = (w0 + nr + 1) & ~1L;
+      const double* xsrc = A.q + a0;
+      const uint32_t xbytes = (uint32_t)(a1 - a0) * 8;
       // the ring slot was last read through the generic proxy: order those reads before
       // the async-proxy writes of the refill
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -106,8 +97,7 @@ __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
               smem_u32(st)),
           "l"(A.mat + ((size_t)iss_rec.x + iss_r) * KP), "r"(rbytes), "r"(bar)
           : "memory");
-      if (xbytes)
-        asm volatile(
+      asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(st + RS * KP * 8)),
             "l"(xsrc), "r"(xbytes), "r"(bar)
@@ -124,8 +114,7 @@ __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
   // ---- consumer
   int it = i0, r0 = 0;
   int4 rec = A.items[i0];
-  double acc[4][T][2];  // MODE 0: four row phases of accumulators
-  double vec[T][2];     // MODE 1: the item's vector
+  double acc[4][T][2];  // four row phases of accumulators
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -144,7 +133,7 @@ __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
     const int nr = min(RS, rec.y - r0);
     const double* rows = reinterpret_cast<const double*>(ring + (size_t)s * SS::STAGE);
     const double* extra = rows + RS * KP;
-    if (MODE == 0) {
+    {
       const double* w = extra + (((long)rec.z + r0) & 1);
 #pragma unroll 2
       for (int r = 0; r < nr; r += 4) {
@@ -162,44 +151,6 @@ __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
           }
         }
       }
-    } else {
-      if (r0 == 0) {
-#pragma unroll
-        for (int t = 0; t < T; ++t) {
-          const double2 v = col_ok<KP>(lane, t) ? *reinterpret_cast<const double2*>(extra + 2 * lane + 64 * t)
-                                                : make_double2(0.0, 0.0);
-          vec[t][0] = v.x;
-          vec[t][1] = v.y;
-        }
-      }
-      // partial dot products of the chunk's rows, then a butterfly reduce-scatter over the
-      // warp: 16 values -> lane l ends with the full sum of row (l >> 1) & 15
-      double d[16];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        d[r] = 0.0;
-        if (r < nr) {
-#pragma unroll
-          for (int t = 0; t < T; ++t)
-            if (col_ok<KP>(lane, t)) {
-              const double2 v = *reinterpret_cast<const double2*>(rows + r * KP + 2 * lane + 64 * t);
-              d[r] = fma(v.x, vec[t][0], fma(v.y, vec[t][1], d[r]));
-            }
-        }
-      }
-#pragma unroll
-      for (int h = 8; h >= 1; h >>= 1) {  // off = 2 h: keep half, send half
-        const bool up = lane & (2 * h);
-#pragma unroll
-        for (int i = 0; i < h; ++i) {
-          const double send = up ? d[i] : d[i + h];
-          const double keep = up ? d[i + h] : d[i];
-          d[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
-        }
-      }
-      d[0] += __shfl_xor_sync(0xffffffffu, d[0], 1);
-      const int row = (lane >> 1) & 15;
-      if (!(lane & 1) && row < nr) A.out[(size_t)rec.z + r0 + row] += d[0];
     }
     __syncwarp();  // every lane is done with stage s
     issue(seq + NS);
@@ -207,7 +158,7 @@ __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
     if (r0 >= rec.y) {  // item done
       const int nxt = it + 1;
       const int4 nrec = nxt < i1 ? A.items[nxt] : make_int4(0, 0, 0, -1);
-      if (MODE == 0 && nrec.w != rec.w) {  // output box done (X: consecutive items may share it)
+      if (nrec.w != rec.w) {  // output box done (X: consecutive items may share it)
 #pragma unroll
         for (int t = 0; t < T; ++t)
           if (col_ok<KP>(lane, t)) {
@@ -234,32 +185,30 @@ __global__ void __launch_bounds__(32, 1) k_stream(StreamArgs A) {
   }
 }
 
-template <int KP, int MODE, bool ATOMIC>
-int launch_one(const StreamPlan& S, const double* mat, const double* q, const double* vin, double* out,
-               cudaStream_t st) {
+template <int KP, bool ATOMIC>
+int launch_one(const StreamPlan& S, const double* mat, const double* q, double* out, cudaStream_t st) {
   if (S.nitems == 0) return 0;
   using SS = StreamShape<KP>;
   const int smem = SS::NS * SS::STAGE;
   static bool attr = false;
   if (!attr) {
-    KIFMM_CUDA(cudaFuncSetAttribute(k_stream<KP, MODE, ATOMIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    KIFMM_CUDA(cudaFuncSetAttribute(k_stream<KP, MODE, ATOMIC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    KIFMM_CUDA(cudaFuncSetAttribute(k_stream<KP, ATOMIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    KIFMM_CUDA(cudaFuncSetAttribute(k_stream<KP, ATOMIC>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     (int)cudaSharedmemCarveoutMaxShared));
     attr = true;
   }
-  StreamArgs a{S.d_items, S.d_cta, mat, q, vin, out};
-  k_stream<KP, MODE, ATOMIC><<<S.ncta, 32, smem, st>>>(a);
+  StreamArgs a{S.d_items, S.d_cta, mat, q, out};
+  k_stream<KP, ATOMIC><<<S.ncta, 32, smem, st>>>(a);
   KIFMM_CUDA(cudaGetLastError());
   return 0;
 }
 
-template <int MODE, bool ATOMIC>
-int launch_kp(int kp, const StreamPlan& S, const double* mat, const double* q, const double* vin, double* out,
-              cudaStream_t st) {
+template <bool ATOMIC>
+int launch_kp(int kp, const StreamPlan& S, const double* mat, const double* q, double* out, cudaStream_t st) {
   switch (kp) {
-    case 32: return launch_one<32, MODE, ATOMIC>(S, mat, q, vin, out, st);
-    case 64: return launch_one<64, MODE, ATOMIC>(S, mat, q, vin, out, st);
-    case 104: return launch_one<104, MODE, ATOMIC>(S, mat, q, vin, out, st);
+    case 32: return launch_one<32, ATOMIC>(S, mat, q, out, st);
+    case 64: return launch_one<64, ATOMIC>(S, mat, q, out, st);
+    case 104: return launch_one<104, ATOMIC>(S, mat, q, out, st);
   }
   set_error("stream GEMV: unsupported kp " + std::to_string(kp));
   return -3;
@@ -270,21 +219,16 @@ int launch_kp(int kp, const StreamPlan& S, const double* mat, const double* q, c
 int stream_s2m(const Plan& P, cudaStream_t st) {
   if (P.sw_s2m.nitems == 0) return 0;
   ++g_launches;
-  return launch_kp<0, false>(P.kp, P.sw_s2m, P.d_s2m_mat, P.d_q_sorted, nullptr, P.d_qhat, st);
+  return launch_kp<false>(P.kp, P.sw_s2m, P.d_s2m_mat, P.d_q_sorted, P.d_qhat, st);
 }
 int stream_x(const Plan& P, cudaStream_t st) {
   if (P.sw_x.nitems == 0) return 0;
   ++g_launches;
-  return launch_kp<0, true>(P.kp, P.sw_x, P.d_x_mat, P.d_q_sorted, nullptr, P.d_lhat, st);
-}
-int stream_l2t(const Plan& P, double* pot, cudaStream_t st) {
-  if (P.sw_l2t.nitems == 0) return 0;
-  ++g_launches;
-  return launch_kp<1, false>(P.kp, P.sw_l2t, P.d_l2t_mat, nullptr, P.d_lhat, pot, st);
+  return launch_kp<true>(P.kp, P.sw_x, P.d_x_mat, P.d_q_sorted, P.d_lhat, st);
 }
 
 // Host: items in streaming order, cut into ncta contiguous ranges of ~equal rows (a range
-// boundary never splits the items of one output box, so MODE 0 CTAs own their boxes).
+// boundary never splits the items of one output box, so a CTA owns its boxes).
 int stream_plan(Plan& P, StreamPlan& S, const std::vector<int4>& items, cudaStream_t st) {
   S.nitems = (int)items.size();
   S.ncta = 0;
