@@ -55,7 +55,7 @@ void free_plan_memory(fmm_plan* h) {
   P.allocations.clear();
   kifmm::Tree& T = P.tree;
   void* tp[] = {T.d_key, T.d_level, T.d_parent, T.d_pbeg, T.d_pend, T.d_child_begin, T.d_nchild, T.d_leaf, T.d_geom,
-                T.d_perm, T.d_pts, P.lists.d_U, P.lists.d_V, P.lists.d_W, P.lists.d_X, h->d_default_density};
+                T.d_perm, T.d_iperm, T.d_pts, P.lists.d_U, P.lists.d_V, P.lists.d_W, P.lists.d_X, h->d_default_density};
   for (void* p : tp)
     if (p) cudaFree(p);
   for (auto e : P.ev_phase) cudaEventDestroy(e);

@@ -85,6 +85,7 @@ struct Tree {
   uint8_t* d_leaf = nullptr;
   double4* d_geom = nullptr;          // (cx, cy, cz, r)
   int32_t* d_perm = nullptr;          // sorted -> caller
+  int32_t* d_iperm = nullptr;         // caller -> sorted
   double4* d_pts = nullptr;           // sorted points (x, y, z, q)
   // host mirrors (setup-time copies)
   std::vector<uint64_t> key;

@@ -1069,7 +1069,9 @@ __global__ void k_set_density(double4* __restrict__ pts, const int32_t* __restri
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < N) {
     const double v = q[perm[i]];
-    pts[i].w = v;
+    double4 p = pts[i];  // whole 32-byte points: full-sector stores, no partial writes
+    p.w = v;
+    pts[i] = p;
     if (qs) qs[i] = v;
   }
 }
@@ -1083,10 +1085,16 @@ __global__ void k_set_density_owned(double4* __restrict__ pts, const double* __r
   }
 }
 
+// potentials to caller order: pot[c] = near[iperm[c]] (+ far[iperm[c]]) — a gather, so the
+// stores are coalesced and the random accesses are 8-byte reads (a scatter of 8-byte
+// stores would make every 32-byte sector a partial write)
 __global__ void k_gather_output(const double* __restrict__ pnear, const double* __restrict__ pfar,
-                                const int32_t* __restrict__ perm, int64_t N, double* __restrict__ pot) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < N) pot[perm[i]] = pfar ? pnear[i] + pfar[i] : pnear[i];
+                                const int32_t* __restrict__ iperm, int64_t N, double* __restrict__ pot) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c < N) {
+    const int32_t i = iperm[c];
+    pot[c] = pfar ? pnear[i] + pfar[i] : pnear[i];
+  }
 }
 
 // owned output in sorted order: pot[i] = near[lo + i] (+ far[lo + i])
@@ -2111,7 +2119,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
     }
     case 4: {  // caller order (replicated mode; the owned ranges were allgathered into pot_near)
       if (owned) return 0;
-      k_gather_output<<<nblk(N), 256, 0, st>>>(P.d_pot_near, P.split_phases ? P.d_pot_far : nullptr, T.d_perm, N, d_pot);
+      k_gather_output<<<nblk(N), 256, 0, st>>>(P.d_pot_near, P.split_phases ? P.d_pot_far : nullptr, T.d_iperm, N, d_pot);
       ++g_launches;
       KIFMM_CUDA(cudaGetLastError());
       mark(9);

@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -38,7 +39,14 @@ NcclApi& api() {
   static NcclApi A;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    // KIFMM_NCCL_LIB: an explicit library path (test seam: tests/native/nccl_shim.cpp runs
+    // this transport with several processes on one GPU)
+    void* h = nullptr;
+    if (const char* p = std::getenv("KIFMM_NCCL_LIB")) {
+      h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+      if (!h) { A.err = std::string("dlopen(") + p + ") failed: " + dlerror(); return; }
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) { A.err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror(); return; }

@@ -65,6 +65,12 @@ __global__ void k_quantize(const double* __restrict__ pts, int64_t N, double lx,
   idx[i] = (int32_t)i;
 }
 
+// caller -> sorted index (the output permutation gathers with it: coalesced stores)
+__global__ void k_invert_perm(const int32_t* __restrict__ perm, int64_t N, int32_t* __restrict__ iperm) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < N) iperm[perm[i]] = (int32_t)i;
+}
+
 __global__ void k_gather_points(const double* __restrict__ pts, const int32_t* __restrict__ perm, int64_t N,
                                 double4* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -196,8 +202,9 @@ int build_tree_device(Plan& P, const double* d_points, cudaStream_t st) {
   cudaFree(d_tmp);
   cudaFree(d_key_in);
   cudaFree(d_idx);
-  if (dalloc(&T.d_pts, N)) return -3;
+  if (dalloc(&T.d_pts, N) || dalloc(&T.d_iperm, N)) return -3;
   k_gather_points<<<nblk(N), 256, 0, st>>>(d_points, T.d_perm, N, T.d_pts);
+  k_invert_perm<<<nblk(N), 256, 0, st>>>(T.d_perm, N, T.d_iperm);
   // K3 levels
   uint8_t *d_active, *d_head;
   int *d_nsel, *d_sel;

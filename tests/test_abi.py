@@ -94,3 +94,20 @@ def test_distributed_entry_points_validate_without_gpu():
     z = np.zeros(4, np.int32)
     assert L.fmm_partition_host(0, *([z.ctypes.data] * 5), 0, None, 0, None, 0, None, 0, None, 56, 25, 2, 0,
                                 ctypes.byref(out)) == K.FMM_EINVAL
+
+
+def test_nccl_shim_builds_and_exports_the_transport_symbols(tmp_path):
+    # the stand-in libnccl.so.2 of the multi-process transport test (test_gpu_nccl_shim.py)
+    # builds here and exports every entry point nccl_transport.cpp resolves with dlsym
+    import subprocess
+    so = str(tmp_path / "libnccl_shim.so")
+    subprocess.check_call(["g++", "-O2", "-shared", "-fPIC", "-I/usr/local/cuda/include",
+                           os.path.join(ROOT, "tests", "native", "nccl_shim.cpp"), "-o", so,
+                           "-L/usr/local/cuda/lib64/stubs", "-lcuda", "-lrt", "-lpthread"])
+    syms = subprocess.check_output(["nm", "-D", "--defined-only", so]).decode()
+    src = open(os.path.join(ROOT, "paper_1211_2517_b200", "csrc", "nccl_transport.cpp")).read()
+    import re
+    wanted = set(re.findall(r'sym\("(nccl\w+)"\)', src))
+    assert len(wanted) == 9
+    for w in wanted:
+        assert f" T {w}\n" in syms, w
