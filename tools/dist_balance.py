@@ -2,7 +2,9 @@
 (diagnostics; the ranks run one after another, so the per-rank phase events measure each
 rank's own kernels).  Default: the weak-scaling workload of bench.py (R tiled unit cubes
 of C2); with a config name, that one problem partitioned R ways (strong scaling).
-    python tools/dist_balance.py R [C4]"""
+    python tools/dist_balance.py R [C4]
+(compute-only strong-scaling efficiency = single_rank_ms / (R max_ms): the NCCL transfers
+of a real multi-GPU run are not in it)"""
 import json
 import os
 import sys
@@ -54,5 +56,6 @@ print(json.dumps(dict(config=name or f"C2 x {R} tiles", single_rank_ms=single, r
                       owned=[i["own_hi"] - i["own_lo"] for i in infos],
                       ghost_q_rows=[i["ghost_q_recv"] for i in infos], ghost_dens=[i["ghost_d_recv"] for i in infos],
                       straddling_boxes=infos[0]["n_straddle"],
+                      leaf_op_GB=[round(i["leaf_op_bytes"] / 1e9, 2) for i in infos],
                       ghost_MB_per_rank=[round((i["ghost_q_recv"] * i["kp"] + i["ghost_d_recv"]) * 8 / 1e6, 2)
                                          for i in infos])))
