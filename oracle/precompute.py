@@ -4,14 +4,15 @@ Plain numpy restatement of the precompute of arXiv 1211.2517 for the Laplace
 single-layer kernel, all operators at unit halfwidth r = 1 (homogeneous scaling,
 P:230-235; level normalisation reading Q15).  Library primitives used as single
 steps: numpy.linalg.pinv (truncated SVD, rcond relative to sigma_max) and
-numpy.linalg.eigh.  "P:n" = /root/reference/PAPER.md line n.
+numpy.linalg.svd.  "P:n" = /root/reference/PAPER.md line n.
 
   surfaces     P:109-113  UE, DC at (1+d) r;  UC, DE at (3-2d) r;  p points per edge
   E_u, E_d     P:126-154  equivalent-density solves (pinv, reading Q11)
   K_delta      P:136-144  K_ij = G(x_i, y_j): x = DC of the target at the origin,
                           y = UE of the source box centred at 2*delta
   K_fat SVD    P:172-203  one SVD suffices for the symmetric kernel:
-                          U = leading eigenvectors of K_fat K_fat^T = sum_d K_d K_d^T
+                          U = leading left singular vectors of K_fat = [K_0 ... K_315]
+                          (eq. fat: K_fat = U Sigma V^T)
   C_delta      P:216-223  K~ = U^T K R with R = U
   S', T'       P:341, P:351 (T~ = T U, typo reading Q16), fused with pinv (Q17)
   M~_o, L~_o
@@ -89,11 +90,8 @@ def build_tables(p: int, k: int, d: float = 0.1, rcond: float = 1e-10, k_exact: 
     Ei_u = np.linalg.pinv(E_u, rcond=rcond)
     Ei_d = np.linalg.pinv(E_d, rcond=rcond)
     K = m2l_matrices(p, d)                       # 316 x n x n
-    gram = sum(Kd @ Kd.T for Kd in K)           # K_fat K_fat^T
-    w, V = np.linalg.eigh(gram)
-    order = np.argsort(w)[::-1]
-    w, V = w[order], V[:, order]
-    sigma = np.sqrt(np.maximum(w, 0.0))
+    kfat = np.concatenate(list(K), axis=1)       # K_fat = [K_0 K_1 ... K_315]  (n x 316 n)
+    V, sigma, _ = np.linalg.svd(kfat, full_matrices=False)   # K_fat = U Sigma V^T, sigma descending
     keff = min(k, n) if k_exact else k_eff_gap(sigma, min(k, n))
     U = V[:, :keff].copy()
     for c in range(keff):                        # cosmetic sign convention (O6)
