@@ -131,7 +131,11 @@ ncclResult_t run_group(Comm* c, const std::vector<Pending>& ops) {
     const size_t bytes = p.count * type_size(p.type);
     if (d.bytes != bytes) { rc = ncclInvalidUsage; continue; }  // mismatched send / recv sizes
     CUdeviceptr src = 0;
-    if (bytes && (open_peer(c, d, &src) != ncclSuccess || cuMemcpyDtoD((CUdeviceptr)p.ptr, src, bytes) != CUDA_SUCCESS))
+    // on the receiver's stream, then waited for: a device-to-device cuMemcpy returns before
+    // the copy completes, and the sender may reuse its buffer after the next barrier
+    if (bytes && (open_peer(c, d, &src) != ncclSuccess ||
+                  cuMemcpyDtoDAsync((CUdeviceptr)p.ptr, src, bytes, p.stream) != CUDA_SUCCESS ||
+                  cuStreamSynchronize(p.stream) != CUDA_SUCCESS))
       rc = ncclUnhandledCudaError;
   }
   barrier(c);  // the senders' buffers are free again
@@ -257,7 +261,12 @@ ncclResult_t ncclAllReduce(const void* sendbuff, void* recvbuff, size_t count, n
     for (size_t i = 0; i < count; ++i) sum[i] += part[i];
   }
   barrier(c);  // every rank has read every buffer before any is overwritten
-  if (rc == ncclSuccess && bytes && cuMemcpyHtoD((CUdeviceptr)recvbuff, sum.data(), bytes) != CUDA_SUCCESS)
+  // on the caller's stream and waited for (a pageable host-to-device cuMemcpy may return
+  // before the DMA lands)
+  const CUstream s = reinterpret_cast<CUstream>(stream);
+  if (rc == ncclSuccess && bytes &&
+      (cuMemcpyHtoDAsync((CUdeviceptr)recvbuff, sum.data(), bytes, s) != CUDA_SUCCESS ||
+       cuStreamSynchronize(s) != CUDA_SUCCESS))
     rc = ncclUnhandledCudaError;
   return rc;
 }
