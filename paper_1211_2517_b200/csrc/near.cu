@@ -242,14 +242,11 @@ struct Cursor {
   int4 rec;  // this unit's record
 };
 
-// resident CTAs per SM the register allocation aims at: single-layer passes of up to 6
-// targets per thread fit 96 registers without spilling, so 5 CTAs (20 warps) hide more of
-// the FP64 dependency latency than 4 at 128 registers; 7-8 targets (or the double layer)
-// would spill at 96 and keep 4 (registers) or fewer (shared memory)
-__host__ __device__ constexpr int nr_minb(int tb, bool dl) { return !dl && tb <= 6 ? 5 : 1; }
-
+// (register targets measured on C4, ncu: 5 CTAs per SM at 96 registers for the 5-6 target
+// passes, or 2 CTAs at ~230 for 7-8, ran at the same speed as the compiler's default
+// 128 registers / 4 CTAs — more resident warps do not lift the FP64 pipe past ~70% here)
 template <int TB, int MQ, bool DL = false>
-__global__ void __launch_bounds__(NR_NT, nr_minb(TB, DL)) k_near(NearArgs A) {
+__global__ void __launch_bounds__(NR_NT) k_near(NearArgs A) {
   constexpr int NT = NR_NT, G = NT / MQ, CAP = TB * MQ, CH = near_ch(CAP, DL), NR_PER = CH / NT;
   static_assert(DL || TB * NT * sizeof(double) <= CH * sizeof(double4), "slice sums alias a source buffer");
   __shared__ __align__(16) double4 sbuf[2][CH];
