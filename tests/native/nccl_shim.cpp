@@ -119,7 +119,8 @@ ncclResult_t run_group(Comm* c, const std::vector<Pending>& ops) {
   RankSlot& me = c->sh->slot[c->rank];
   std::memset(&me, 0, sizeof(me));
   for (const Pending& p : ops) {
-    if (p.stream && cuStreamSynchronize(p.stream) != CUDA_SUCCESS) return ncclUnhandledCudaError;
+    // (stream 0 is the legacy default stream: synchronised like any other)
+    if (cuStreamSynchronize(p.stream) != CUDA_SUCCESS) return ncclUnhandledCudaError;
     if (p.send && describe(p.ptr, p.count * type_size(p.type), &me.to[p.peer]) != ncclSuccess)
       return ncclUnhandledCudaError;
   }
@@ -246,7 +247,7 @@ ncclResult_t ncclAllReduce(const void* sendbuff, void* recvbuff, size_t count, n
                            ncclComm_t comm, cudaStream_t stream) {
   if (type != ncclFloat64 || op != ncclSum) return ncclInvalidArgument;
   Comm* c = reinterpret_cast<Comm*>(comm);
-  if (stream && cuStreamSynchronize(reinterpret_cast<CUstream>(stream)) != CUDA_SUCCESS) return ncclUnhandledCudaError;
+  if (cuStreamSynchronize(reinterpret_cast<CUstream>(stream)) != CUDA_SUCCESS) return ncclUnhandledCudaError;
   const size_t bytes = count * 8;
   RankSlot& me = c->sh->slot[c->rank];
   std::memset(&me, 0, sizeof(me));

@@ -1,7 +1,7 @@
 """One rank of a multi-process matvec over the NCCL shim (test helper for
 tests/test_gpu_nccl_shim.py; run as a separate process per rank, all on cuda:0).
 
-    python tests/shim_rank.py <workdir> <rank> <nranks>
+    python tests/shim_rank.py <workdir> <rank> <nranks> [overlap]
 
 Reads workdir/case.npz (points, densities, operator tables, leaf size) and workdir/id.bin
 (the shim's unique id), builds the rank's plan with the production NCCL transport
@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1211_2517_b200 as K  # noqa: E402
 
 work, rank, nranks = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+overlap = int(sys.argv[4]) if len(sys.argv) > 4 else -1
 d = np.load(os.path.join(work, "case.npz"))
 uid = open(os.path.join(work, "id.bin"), "rb").read()
 tb = {k[3:]: d[k] for k in d.files if k.startswith("tb_")}
@@ -27,7 +28,7 @@ dev = torch.device("cuda:0")
 P = torch.from_numpy(d["pts"]).to(dev)
 q = d["q"]
 p, k, s = int(d["p"]), int(d["k"]), int(d["s"])
-plan = K.Plan(P, None, p=p, k=k, leaf_size=s, tables=tb, nranks=nranks, rank=rank, nccl_id=uid)
+plan = K.Plan(P, None, p=p, k=k, leaf_size=s, tables=tb, nranks=nranks, rank=rank, nccl_id=uid, overlap=overlap)
 assert plan.info["nranks"] == nranks
 rep = plan.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()   # REPLICATED: allgather inside
 lo, hi = plan.owned_range

@@ -59,7 +59,8 @@ CASES = {
 
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_nccl_transport_multiprocess(shim, tmp_path, case, nranks):
+@pytest.mark.parametrize("overlap", [0, 3])
+def test_nccl_transport_multiprocess(shim, tmp_path, case, nranks, overlap):
     pts, q, p, k, s = CASES[case]()
     tb = pc.build_tables(p, k)
     ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q)
@@ -68,7 +69,7 @@ def test_nccl_transport_multiprocess(shim, tmp_path, case, nranks):
     (tmp_path / "id.bin").write_bytes(unique_id(shim))
     env = dict(os.environ, KIFMM_NCCL_LIB=shim)
     procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "shim_rank.py"), str(tmp_path), str(r),
-                               str(nranks)], env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+                               str(nranks), str(overlap)], env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
              for r in range(nranks)]
     logs = []
     for pr in procs:
@@ -77,13 +78,16 @@ def test_nccl_transport_multiprocess(shim, tmp_path, case, nranks):
     assert all(pr.returncode == 0 for pr in procs), "\n".join(logs)
     res = [np.load(tmp_path / f"out_{r}.npz") for r in range(nranks)]
     perm = res[0]["perm"]
-    owned = np.empty(q.size)
-    for r in res:
-        assert par(r["rep"], ref) <= TOL  # REPLICATED: every rank holds the whole potential
+    owned, owned2 = np.empty(q.size), np.empty(q.size)
+    errs = {}
+    for i, r in enumerate(res):
         lo, hi = int(r["lo"]), int(r["hi"])
         owned[perm[lo:hi]] = r["own"]
-        assert np.array_equal(r["own"], r["own2"]) or par(r["own2"], r["own"]) <= 1e-14
-    assert par(owned, ref) <= TOL
+        owned2[perm[lo:hi]] = r["own2"]
+        errs[f"rep{i}"] = par(r["rep"], ref)  # REPLICATED: every rank holds the whole potential
+    errs["owned"] = par(owned, ref)
+    errs["owned_again"] = par(owned2, ref)  # the same plans, a second OWNED matvec
+    assert max(errs.values()) <= TOL, errs
     # the exchanges moved data: ghost multipole rows and straddling boxes on every rank
     assert all(int(r["ghost_q"]) > 0 for r in res)
     assert int(res[0]["straddle"]) > 0
