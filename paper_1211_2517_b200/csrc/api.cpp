@@ -67,6 +67,11 @@ void free_plan_memory(fmm_plan* h) {
   if (P.stream_near) cudaStreamDestroy(P.stream_near);
   if (P.stream_m2l) cudaStreamDestroy(P.stream_m2l);
   if (P.ev_m2l) cudaEventDestroy(P.ev_m2l);
+  if (P.stream_comm) cudaStreamDestroy(P.stream_comm);
+  if (P.ev_up) cudaEventDestroy(P.ev_up);
+  if (P.ev_comm) cudaEventDestroy(P.ev_comm);
+  P.stream_comm = nullptr;
+  P.ev_up = P.ev_comm = nullptr;
   for (auto& e : P.ev_near) {
     if (e) cudaEventDestroy(e);
     e = nullptr;
@@ -326,6 +331,12 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     if (opt->nccl_id) {  // (a one-rank communicator is allowed: it exercises the transport setup)
       if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("fmm_setup: CUDA error before NCCL init"); return fail(FMM_ECUDA); }
       if (kifmm::nccl_comm_init(P, opt->nccl_id)) return fail(FMM_ENCCL);
+      if (cudaStreamCreateWithFlags(&P.stream_comm, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&P.ev_up, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&P.ev_comm, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("fmm_setup: creating the communication stream failed");
+        return fail(FMM_ECUDA);
+      }
     }
     if (densities) {
       if (cudaMalloc(&h->d_default_density, sizeof(double) * N) != cudaSuccess ||
@@ -651,7 +662,7 @@ int fmm_info(const fmm_plan* h, fmm_info_t* info) {
     info->nboxes = P.tree.nboxes; info->nleaves = P.tree.nleaves; info->nlevels = P.tree.nlevels;
     info->nU = P.lists.nU; info->nV = P.lists.nV; info->nW = P.lists.nW; info->nX = P.lists.nX;
     info->n_s2m = P.n_s2m; info->n_xnd = P.n_xnd; info->n_l2t = P.n_l2t; info->n_wnd = P.n_wnd;
-    info->m2l_tiles = P.g_m2l_sib.ntiles; info->m2l_pairs = P.nV_local;
+    info->m2l_tiles = P.g_m2l_sib.ntiles + P.g_m2l_sib_ghost.ntiles; info->m2l_pairs = P.nV_local;
     info->launches = P.launches;
     info->r0 = P.tree.r0;
     for (int d = 0; d < 3; ++d) info->lo_root[d] = P.tree.lo_root[d];

@@ -243,7 +243,9 @@ struct Plan {
   std::vector<void*> allocations;              // everything cudaMalloc'ed for the plan
   // dense-algebra launches
   GemmLaunch g_s2m, g_x, g_l2t, g_w;
-  SibLaunch g_m2l_sib;
+  SibLaunch g_m2l_sib;        // M2L columns whose sources are complete on this rank (all, one rank)
+  SibLaunch g_m2l_sib_ghost;  // the rest: ghost / straddling sources (multi-rank plans)
+  bool m2l_local_done = false;  // this matvec already ran the local M2L tiles (overlapped exchange)
   double sib_min_density = 0.5;   // sibling groups at least this full go to k_m2l_sib
   std::vector<GemmLaunch> g_m2m;   // per child level (descending)
   std::vector<GemmLaunch> g_l2l;   // per parent level (ascending)
@@ -257,6 +259,10 @@ struct Plan {
   cudaEvent_t ev_near[2] = {nullptr, nullptr};  // profiled plans: around the near-field launches
   bool near_timed = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // NCCL plans: the straddler allreduce and the ghost exchange on their own stream, beside
+  // the M2L of the local sources (matvec_device)
+  cudaStream_t stream_comm = nullptr;
+  cudaEvent_t ev_up = nullptr, ev_comm = nullptr;
   std::vector<cudaEvent_t> ev_phase;
   std::vector<cudaEvent_t> ev_trace;  // KIFMM_TRACE=1 diagnostics (kernels.cu)
   bool profile = false;

@@ -1857,6 +1857,8 @@ struct Trace {
 Trace g_trace;
 }  // namespace
 
+int launch_m2l(const Plan& P, const SibLaunch& g, cudaStream_t st);
+
 // Profile events (fmm_info.phase_ms): 0 density (+ghost densities) | 1 S2M | 2 M2M |
 // 3 exchange (straddlers + ghost q^') | 4 M2L | 5 X | 6 L2L | 7 evaluation (L2T, W, P2P) | 8 output
 int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, bool owned, cudaStream_t st) {
@@ -1990,11 +1992,11 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         KIFMM_CUDA(cudaStreamWaitEvent(P.stream_m2l, P.ev_fork, 0));
         sm2l = P.stream_m2l;
       }
-      if (P.lr.on) {
-        if (launch_m2l_lowrank(P.g_m2l_sib, P.lr, kp, k, P.d_qhat, P.d_lhat, sm2l)) return -3;
-      } else if (launch_m2l_sib(P.g_m2l_sib, P.d_C, kp, k, P.d_qhat, P.d_lhat, sm2l)) {
-        return -3;
-      }
+      // the local-source tiles (unless matvec_device ran them beside the exchanges), then the
+      // tiles with ghost / straddling sources
+      if (!P.m2l_local_done && launch_m2l(P, P.g_m2l_sib, sm2l)) return -3;
+      P.m2l_local_done = false;
+      if (launch_m2l(P, P.g_m2l_sib_ghost, sm2l)) return -3;
       if (P.overlap == 2) {
         KIFMM_CUDA(cudaEventRecord(P.ev_m2l, P.stream_m2l));
         KIFMM_CUDA(cudaStreamWaitEvent(P.stream_near, P.ev_fork, 0));
@@ -2130,7 +2132,18 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
   return -1;
 }
 
-// One matvec of a single-GPU plan, or of one rank of an NCCL-connected plan.
+// M2L, all levels in one launch per kernel (the dense cores or the stage-2 factors)
+int launch_m2l(const Plan& P, const SibLaunch& g, cudaStream_t st) {
+  if (P.lr.on) return launch_m2l_lowrank(g, P.lr, P.kp, P.k, P.d_qhat, P.d_lhat, st);
+  return launch_m2l_sib(g, P.d_C, P.kp, P.k, P.d_qhat, P.d_lhat, st);
+}
+
+// One matvec of a single-GPU plan, or of one rank of an NCCL-connected plan.  NCCL plans
+// (not profiled) overlap the exchanges with compute: after the upward pass the straddler
+// allreduce, the ghost-q^' pack and the exchange run on the plan's comm stream while the
+// main stream runs the M2L tiles whose sources are complete locally (they touch neither
+// the straddling rows the allreduce rewrites nor the ghost rows still in flight); the
+// main stream then waits for the exchange and continues with the ghost-source tiles.
 int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, cudaStream_t st) {
   const bool dist = P.nccl_comm != nullptr;
   g_trace.begin(P);
@@ -2141,9 +2154,24 @@ int matvec_device(Plan& P, const double* d_density, double* d_pot, bool owned, c
   if (matvec_stage(P, 0, d_density, d_pot, owned, st)) return -3;
   if (dist && owned && nccl_exchange(P, P.xd, st)) return -5;
   if (matvec_stage(P, 1, d_density, d_pot, owned, st)) return -3;
-  if (dist && nccl_allreduce_sum(P, P.d_straddle_buf, (size_t)P.n_straddle * P.kp, st)) return -5;
-  if (matvec_stage(P, 2, d_density, d_pot, owned, st)) return -3;
-  if (dist && nccl_exchange(P, P.xq, st)) return -5;
+  if (dist && P.stream_comm && !P.profile) {
+    cudaStream_t sc = P.stream_comm;
+    KIFMM_CUDA(cudaEventRecord(P.ev_up, st));
+    KIFMM_CUDA(cudaStreamWaitEvent(sc, P.ev_up, 0));
+    if (nccl_allreduce_sum(P, P.d_straddle_buf, (size_t)P.n_straddle * P.kp, sc)) return -5;
+    if (matvec_stage(P, 2, d_density, d_pot, owned, sc)) return -3;
+    if (nccl_exchange(P, P.xq, sc)) return -5;
+    KIFMM_CUDA(cudaEventRecord(P.ev_comm, sc));
+    g_trace.mark("m2l_local_begin", st);
+    if (launch_m2l(P, P.g_m2l_sib, st)) return -3;
+    g_trace.mark("m2l_local_end", st);
+    P.m2l_local_done = true;
+    KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_comm, 0));
+  } else {
+    if (dist && nccl_allreduce_sum(P, P.d_straddle_buf, (size_t)P.n_straddle * P.kp, st)) return -5;
+    if (matvec_stage(P, 2, d_density, d_pot, owned, st)) return -3;
+    if (dist && nccl_exchange(P, P.xq, st)) return -5;
+  }
   if (matvec_stage(P, 3, d_density, d_pot, owned, st)) return -3;
   if (dist && !owned && nccl_allgather_ranges(P, P.d_pot_near, st)) return -5;
   return matvec_stage(P, 4, d_density, d_pot, owned, st);

@@ -644,28 +644,47 @@ int build_schedules(Plan& P, cudaStream_t st) {
     P.m2l_exec_flops = 0;
     const int ncls = (int)cls_cols.size();
     for (int cls = 0; cls < ncls; ++cls) P.m2l_exec_flops += (double)nvalid[cls] * (cls_cols[cls].size() / 9) * 2.0 * P.k * P.k;
-    // sibling tiles: per class, columns in target order, NT columns per tile
-    std::vector<int> cols;
-    std::vector<int4> tiles;
-    for (int cls = 0; cls < ncls; ++cls) {
-      const auto& cc = cls_cols[cls];
-      const int ncol = (int)cc.size() / 9;
-      const int base = (int)cols.size() / 9;
-      cols.insert(cols.end(), cc.begin(), cc.end());
-      for (int c = 0; c < ncol; c += NTs) tiles.push_back(make_int4(cls, base + c, std::min(NTs, ncol - c), 0));
-    }
-    // longest tiles first (the kernel hands tiles out dynamically: LPT order balances the SMs;
-    // a Morton-window order for L2 locality measured no better on C2 / C3 / C5; class-major
-    // order for stage 2 neither)
-    std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
-      return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
-    });
-    mark("m2l tiles");
-    P.g_m2l_sib.ntiles = (int)tiles.size();
-    P.g_m2l_sib.ncols = (int)cols.size() / 9;
-    if (upload(P, &P.g_m2l_sib.d_tiles, tiles, st) || upload(P, &P.g_m2l_sib.d_cols, cols, st) ||
-        upload(P, &P.g_m2l_sib.d_classes, classes, st) || upload(P, &P.g_m2l_sib.d_counter, std::vector<int>(1, 0), st))
+    // sibling tiles: per class, columns in target order, NT columns per tile.  Two launches:
+    // columns whose sources are all complete on this rank after its own M2M ("local": every
+    // present source box lies in the owned range) and the rest (ghost or straddling sources,
+    // complete only after the allreduce and the ghost exchange).  NCCL plans run the local
+    // tiles while the exchanges are in flight (matvec_device); one rank: all local.
+    auto build_tiles = [&](bool ghost, SibLaunch& L) -> int {
+      std::vector<int> cols;
+      std::vector<int4> tiles;
+      for (int cls = 0; cls < ncls; ++cls) {
+        const auto& cc = cls_cols[cls];
+        const int ncol = (int)cc.size() / 9;
+        const int base = (int)cols.size() / 9;
+        for (int c = 0; c < ncol; ++c) {
+          bool local = true;
+          for (int j = 1; j < 9; ++j) {
+            const int src = cc[(size_t)c * 9 + j];
+            if (src >= 0 && !Dp.full[src]) local = false;
+          }
+          if (local != ghost) cols.insert(cols.end(), cc.begin() + (size_t)c * 9, cc.begin() + (size_t)(c + 1) * 9);
+        }
+        const int nc = (int)cols.size() / 9 - base;
+        for (int c = 0; c < nc; c += NTs) tiles.push_back(make_int4(cls, base + c, std::min(NTs, nc - c), 0));
+      }
+      // longest tiles first (the kernel hands tiles out dynamically: LPT order balances the
+      // SMs; a Morton-window order for L2 locality measured no better on C2 / C3 / C5;
+      // class-major order for stage 2 neither)
+      std::stable_sort(tiles.begin(), tiles.end(), [&](const int4& a, const int4& b) {
+        return nvalid[a.x] * a.z > nvalid[b.x] * b.z;
+      });
+      L.ntiles = (int)tiles.size();
+      L.ncols = (int)cols.size() / 9;
+      if (upload(P, &L.d_tiles, tiles, st) || upload(P, &L.d_cols, cols, st) ||
+          upload(P, &L.d_counter, std::vector<int>(1, 0), st))
+        return -3;
+      return 0;
+    };
+    if (build_tiles(false, P.g_m2l_sib) || build_tiles(true, P.g_m2l_sib_ghost) ||
+        upload(P, &P.g_m2l_sib.d_classes, classes, st))
       return -3;
+    P.g_m2l_sib_ghost.d_classes = P.g_m2l_sib.d_classes;
+    mark("m2l tiles");
   }
   mark("m2l schedule");
   // M2M per child level (finest first) and L2L per parent level (coarsest first), by octant
