@@ -210,6 +210,7 @@ int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
 
 int bem_near_matvec(const Plan& P, cudaStream_t st) {
   if (P.n_tleaf == 0) return 0;
+  if (P.sw_bem.ncta > 0) return stream_bem_near(P, st);  // bulk-copy streamed (stream.cu)
   k_bem_near<<<P.n_tleaf, BN_NT, 0, st>>>(P.d_tleaf_items, P.tree.d_pbeg, P.tree.d_pend, P.d_near_off,
                                                   P.d_near_seg, P.d_bem_moff, P.tree.d_pts, P.d_bem_A, P.d_pot_near);
   KIFMM_CUDA(cudaGetLastError());

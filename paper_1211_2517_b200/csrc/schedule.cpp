@@ -422,6 +422,24 @@ int build_schedules(Plan& P, cudaStream_t st) {
     }
     if (upload(P, &P.d_near_seg, near_seg, st) || upload(P, &P.d_near_off, near_off, st)) return -3;
     if (int rc = bem_build_near(P, blocks, st)) return rc;
+    // the SpMV streamed by bulk copies (stream.cu) when every target leaf has <= 256
+    // elements (a lane holds 8 of a leaf's targets)
+    std::vector<int64_t> ent(nt, 0);
+    int mmax = 0;
+    for (int i = 0; i < nt; ++i) {
+      const int b = titems[i].x, mp = (npts(b) + 3) & ~3;
+      mmax = std::max(mmax, mp);
+      for (int s = near_off[i]; s < near_off[i + 1]; ++s) ent[i] += (int64_t)mp * near_seg[s].w;
+    }
+    if (mmax <= 256) {
+      auto zalloc_q = [&]() -> int {
+        KIFMM_CUDA(cudaMalloc(&P.d_q_sorted, sizeof(double) * ((size_t)T.N + 2)));
+        P.allocations.push_back(P.d_q_sorted);
+        KIFMM_CUDA(cudaMemsetAsync(P.d_q_sorted, 0, sizeof(double) * ((size_t)T.N + 2), st));
+        return 0;
+      };
+      if (zalloc_q() || stream_plan_bem(P, ent, st)) return -3;
+    }
   }
   P.n_far_seg = (int)far_seg.size();
   {  // the far pass over only the leaves with far segments (when it adds to stored results)
