@@ -273,7 +273,9 @@ __global__ void __launch_bounds__(32, 1) k_stream_bem(BemStreamArgs A) {
       }
     }
   };
-  auto cols_of = [&](const Cur& c) { return min(c.len - c.j, max(1, kBemStage / c.mp)); };
+  // columns per stage: <= kBemStage matrix doubles and <= 32 columns (their densities fit the
+  // stage's 36-double tail)
+  auto cols_of = [&](const Cur& c) { return min(c.len - c.j, max(1, min(32, kBemStage / c.mp))); };
   Cur iss{i0, 0, 0, 0, 0, 0};
   load_item(iss);
   advance(iss, 0);
