@@ -178,9 +178,14 @@ int bem_check_enclosure(Plan& P, cudaStream_t st) {
 
 // blocks: (target box first point, m, source first point, len) per near segment, aligned
 // with the near segment CSR; offsets into the matrix (int64)
-int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
+std::vector<int64_t> bem_block_offsets(const std::vector<int4>& blocks) {
   std::vector<int64_t> off(blocks.size() + 1, 0);  // columns of mp = 4 ceil(m / 4) rows: 32-byte aligned
   for (size_t i = 0; i < blocks.size(); ++i) off[i + 1] = off[i] + (int64_t)((blocks[i].y + 3) & ~3) * blocks[i].w;
+  return off;
+}
+
+int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
+  const std::vector<int64_t> off = bem_block_offsets(blocks);
   const int64_t entries = off.back();
   size_t fr = 0, tot = 0;
   KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));

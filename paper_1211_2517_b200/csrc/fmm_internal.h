@@ -337,7 +337,9 @@ int stream_plan(Plan& P, StreamPlan& S, const std::vector<int4>& items, cudaStre
 int stream_s2m(const Plan& P, cudaStream_t st);
 int stream_x(const Plan& P, cudaStream_t st);
 int stream_bem_near(const Plan& P, cudaStream_t st);
-int stream_plan_bem(Plan& P, const std::vector<int64_t>& item_entries, cudaStream_t st);
+int stream_plan_bem(Plan& P, const std::vector<int>& item_off, const std::vector<int4>& blocks,
+                    const std::vector<int64_t>& moff, cudaStream_t st);
+std::vector<int64_t> bem_block_offsets(const std::vector<int4>& blocks);
 int upload_tables(Plan& P);
 int kernels_init();
 int ggs_tile_width(int M, int K);

@@ -424,21 +424,12 @@ int build_schedules(Plan& P, cudaStream_t st) {
     if (int rc = bem_build_near(P, blocks, st)) return rc;
     // the SpMV streamed by bulk copies (stream.cu) when every target leaf has <= 256
     // elements (a lane holds 8 of a leaf's targets)
-    std::vector<int64_t> ent(nt, 0);
-    int mmax = 0;
-    for (int i = 0; i < nt; ++i) {
-      const int b = titems[i].x, mp = (npts(b) + 3) & ~3;
-      mmax = std::max(mmax, mp);
-      for (int s = near_off[i]; s < near_off[i + 1]; ++s) ent[i] += (int64_t)mp * near_seg[s].w;
-    }
-    if (mmax <= 256) {
-      auto zalloc_q = [&]() -> int {
-        KIFMM_CUDA(cudaMalloc(&P.d_q_sorted, sizeof(double) * ((size_t)T.N + 2)));
-        P.allocations.push_back(P.d_q_sorted);
-        KIFMM_CUDA(cudaMemsetAsync(P.d_q_sorted, 0, sizeof(double) * ((size_t)T.N + 2), st));
-        return 0;
-      };
-      if (zalloc_q() || stream_plan_bem(P, ent, st)) return -3;
+    const int rc = stream_plan_bem(P, near_off, blocks, bem_block_offsets(blocks), st);
+    if (rc < 0) return -3;
+    if (rc == 0 && P.sw_bem.ncta > 0) {
+      KIFMM_CUDA(cudaMalloc(&P.d_q_sorted, sizeof(double) * ((size_t)T.N + 2)));
+      P.allocations.push_back(P.d_q_sorted);
+      KIFMM_CUDA(cudaMemsetAsync(P.d_q_sorted, 0, sizeof(double) * ((size_t)T.N + 2), st));
     }
   }
   P.n_far_seg = (int)far_seg.size();
