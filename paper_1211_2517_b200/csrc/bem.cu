@@ -178,14 +178,9 @@ int bem_check_enclosure(Plan& P, cudaStream_t st) {
 
 // blocks: (target box first point, m, source first point, len) per near segment, aligned
 // with the near segment CSR; offsets into the matrix (int64)
-std::vector<int64_t> bem_block_offsets(const std::vector<int4>& blocks) {
+int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
   std::vector<int64_t> off(blocks.size() + 1, 0);  // columns of mp = 4 ceil(m / 4) rows: 32-byte aligned
   for (size_t i = 0; i < blocks.size(); ++i) off[i + 1] = off[i] + (int64_t)((blocks[i].y + 3) & ~3) * blocks[i].w;
-  return off;
-}
-
-int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
-  const std::vector<int64_t> off = bem_block_offsets(blocks);
   const int64_t entries = off.back();
   size_t fr = 0, tot = 0;
   KIFMM_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -215,7 +210,6 @@ int bem_build_near(Plan& P, const std::vector<int4>& blocks, cudaStream_t st) {
 
 int bem_near_matvec(const Plan& P, cudaStream_t st) {
   if (P.n_tleaf == 0) return 0;
-  if (P.sw_bem.ncta > 0) return stream_bem_near(P, st);  // bulk-copy streamed (stream.cu)
   k_bem_near<<<P.n_tleaf, BN_NT, 0, st>>>(P.d_tleaf_items, P.tree.d_pbeg, P.tree.d_pend, P.d_near_off,
                                                   P.d_near_seg, P.d_bem_moff, P.tree.d_pts, P.d_bem_A, P.d_pot_near);
   KIFMM_CUDA(cudaGetLastError());

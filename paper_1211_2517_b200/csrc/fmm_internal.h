@@ -235,7 +235,6 @@ struct Plan {
   // S2M (and X, if any) operators built
   bool stream_ok = false;
   StreamPlan sw_s2m, sw_x;
-  StreamPlan sw_bem;  // BEM near-field SpMV streamed (k_stream_bem; leaves of <= 256 points)
   double* d_q_sorted = nullptr;  // N + 2 densities in sorted order (the streamed weights)
   int64_t leaf_op_bytes = 0;
   int n_s2m = 0; int4* d_s2m_items = nullptr; int* d_s2m_off = nullptr; int4* d_s2m_seg = nullptr;
@@ -336,10 +335,6 @@ int build_schedules(Plan& P, cudaStream_t st);
 int stream_plan(Plan& P, StreamPlan& S, const std::vector<int4>& items, cudaStream_t st);
 int stream_s2m(const Plan& P, cudaStream_t st);
 int stream_x(const Plan& P, cudaStream_t st);
-int stream_bem_near(const Plan& P, cudaStream_t st);
-int stream_plan_bem(Plan& P, const std::vector<int>& item_off, const std::vector<int4>& blocks,
-                    const std::vector<int64_t>& moff, cudaStream_t st);
-std::vector<int64_t> bem_block_offsets(const std::vector<int4>& blocks);
 int upload_tables(Plan& P);
 int kernels_init();
 int ggs_tile_width(int M, int K);

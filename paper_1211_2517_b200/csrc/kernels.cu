@@ -1901,10 +1901,10 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
         const int cnt = Dp.own_hi - Dp.own_lo;
         if (cnt > 0)
           k_set_density_owned<<<nblk(cnt), 256, 0, st>>>(T.d_pts, d_density, Dp.own_lo, cnt,
-                                                         P.d_q_sorted);
+                                                         P.stream_ok ? P.d_q_sorted : nullptr);
         if (pack(pts_w, 4, P.xd.d_send_idx, P.xd.nsend, 1, P.xd.d_send, st)) return -3;
       } else {
-        k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N, P.d_q_sorted);
+        k_set_density<<<nblk(N), 256, 0, st>>>(T.d_pts, T.d_perm, d_density, N, P.stream_ok ? P.d_q_sorted : nullptr);
       }
       KIFMM_CUDA(cudaGetLastError());
       return 0;

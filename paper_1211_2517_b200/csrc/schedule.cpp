@@ -422,15 +422,6 @@ int build_schedules(Plan& P, cudaStream_t st) {
     }
     if (upload(P, &P.d_near_seg, near_seg, st) || upload(P, &P.d_near_off, near_off, st)) return -3;
     if (int rc = bem_build_near(P, blocks, st)) return rc;
-    // the SpMV streamed by bulk copies (stream.cu) when every target leaf has <= 256
-    // elements (a lane holds 8 of a leaf's targets)
-    const int rc = stream_plan_bem(P, near_off, blocks, bem_block_offsets(blocks), st);
-    if (rc < 0) return -3;
-    if (rc == 0 && P.sw_bem.ncta > 0) {
-      KIFMM_CUDA(cudaMalloc(&P.d_q_sorted, sizeof(double) * ((size_t)T.N + 2)));
-      P.allocations.push_back(P.d_q_sorted);
-      KIFMM_CUDA(cudaMemsetAsync(P.d_q_sorted, 0, sizeof(double) * ((size_t)T.N + 2), st));
-    }
   }
   P.n_far_seg = (int)far_seg.size();
   {  // the far pass over only the leaves with far segments (when it adds to stored results)

@@ -214,185 +214,7 @@ int launch_kp(int kp, const StreamPlan& S, const double* mat, const double* q, d
   return -3;
 }
 
-// ---- BEM near field (S2T by element integration): pot_B = sum_A M_(B,A) q_A over
-// the target leaf's near segments, M_(B,A) a column-major block of mp = 4 ceil(m_B / 4)
-// rows (bem.cu, bem_build_near).  The same single-warp bulk-copy ring over a host-built
-// chunk list: a chunk is <= 32 consecutive columns (<= 8 KB) of one block; its record
-// (matrix offset / 4, first density, nr | mp << 6 | m << 15 | last << 24, first target)
-// is staged into shared memory beside the copies, so the warp never waits on a dependent
-// metadata load.  Lane l accumulates the targets 2 l + 64 u (+1), u < 4 (leaves up to 256
-// points); a leaf's potentials are stored after its last chunk.
-constexpr int kBemStage = 1024;  // doubles of matrix per stage
-constexpr int kBemNS = 6;
-
-struct BemStreamArgs {
-  const int4* chunks;
-  const int* cta_begin;   // CTA c: chunks [cta_begin[c], cta_begin[c + 1])
-  const double* A;
-  const double* q;        // densities in sorted order
-  double* pot;
-};
-
-__global__ void __launch_bounds__(32, 1) k_stream_bem(BemStreamArgs A) {
-  constexpr int NS = kBemNS, STAGE = (kBemStage + 36) * 8;
-  extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ __align__(8) uint64_t full[NS];
-  __shared__ int4 srec[NS];
-  const int lane = threadIdx.x;
-  const int c0 = A.cta_begin[blockIdx.x], c1 = A.cta_begin[blockIdx.x + 1];
-  if (c0 >= c1) return;
-  if (lane == 0) {
-    for (int s = 0; s < NS; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  int4 pref = lane == 0 ? A.chunks[c0] : make_int4(0, 0, 0, 0);  // lane 0: the next record to issue
-  auto issue = [&](int seq) {
-    const int c = c0 + seq;
-    if (c >= c1 || lane != 0) return;
-    const int4 r = pref;
-    if (c + 1 < c1) pref = A.chunks[c + 1];  // in flight while the warp consumes a chunk
-    const int s = seq % NS;
-    unsigned char* st = ring + (size_t)s * STAGE;
-    const uint32_t bar = smem_u32(&full[s]);
-    const int nr = r.z & 63, mp = (r.z >> 6) & 511;
-    const uint32_t mbytes = (uint32_t)nr * mp * 8;  // mp % 4 == 0: 32-byte multiples
-    const long w0 = r.y, a0 = w0 & ~1L, a1 = (w0 + nr + 1) & ~1L;
-    const uint32_t wbytes = (uint32_t)(a1 - a0) * 8;
-    srec[s] = r;  // visible to the warp through the barrier's release / acquire
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(mbytes + wbytes) : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(st)),
-        "l"(A.A + (int64_t)r.x * 4), "r"(mbytes), "r"(bar)
-        : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(st + kBemStage * 8)),
-        "l"(A.q + a0), "r"(wbytes), "r"(bar)
-        : "memory");
-  };
-  for (int s = 0; s < NS; ++s) issue(s);
-  double acc[2][4][2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc[h][u][0] = acc[h][u][1] = 0.0;
-  for (int seq = 0; c0 + seq < c1; ++seq) {
-    const int s = seq % NS;
-    const uint32_t par = (uint32_t)(seq / NS) & 1u, bar = smem_u32(&full[s]);
-    uint32_t done = 0;
-    while (!done)
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-          : "=r"(done)
-          : "r"(bar), "r"(par)
-          : "memory");
-    const int4 r = srec[s];
-    const int nr = r.z & 63, mp = (r.z >> 6) & 511, m = (r.z >> 15) & 511;
-    const double* M = reinterpret_cast<const double*>(ring + (size_t)s * STAGE);
-    const double* w = M + kBemStage + (r.y & 1);
-    for (int c = 0; c < nr; c += 2) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (c + h < nr) {
-          const double wc = w[c + h];
-          const double* col = M + (size_t)(c + h) * mp + 2 * lane;
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (2 * lane + 64 * u < mp) {
-              const double2 v = *reinterpret_cast<const double2*>(col + 64 * u);
-              acc[h][u][0] = fma(wc, v.x, acc[h][u][0]);
-              acc[h][u][1] = fma(wc, v.y, acc[h][u][1]);
-            }
-        }
-      }
-    }
-    __syncwarp();
-    issue(seq + NS);
-    if (r.z >> 24) {  // the leaf's last chunk: store its potentials
-      const int tb = r.w;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int t = 2 * lane + 64 * u;
-        if (t < m) A.pot[tb + t] = acc[0][u][0] + acc[1][u][0];
-        if (t + 1 < m) A.pot[tb + t + 1] = acc[0][u][1] + acc[1][u][1];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) acc[h][u][0] = acc[h][u][1] = 0.0;
-      }
-    }
-  }
-}
-
 }  // namespace
-
-int stream_bem_near(const Plan& P, cudaStream_t st) {
-  if (P.sw_bem.ncta == 0) return 0;
-  constexpr int smem = kBemNS * (kBemStage + 36) * 8;
-  static bool attr = false;
-  if (!attr) {
-    KIFMM_CUDA(cudaFuncSetAttribute(k_stream_bem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    KIFMM_CUDA(cudaFuncSetAttribute(k_stream_bem, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    (int)cudaSharedmemCarveoutMaxShared));
-    attr = true;
-  }
-  BemStreamArgs a{P.sw_bem.d_items, P.sw_bem.d_cta, P.d_bem_A, P.d_q_sorted, P.d_pot_near};
-  k_stream_bem<<<P.sw_bem.ncta, 32, smem, st>>>(a);
-  KIFMM_CUDA(cudaGetLastError());
-  return 0;
-}
-
-// Host: the chunk list of the BEM near-field SpMV (target leaves in near-segment CSR
-// order; per leaf its blocks, per block chunks of <= min(32, 1024 / mp) columns) and the
-// CTA ranges over it (a range never splits a leaf: its CTA owns its potentials).
-// blocks[s] = (first target point, m, first source point, len); moff[s] the block offset.
-int stream_plan_bem(Plan& P, const std::vector<int>& item_off, const std::vector<int4>& blocks,
-                    const std::vector<int64_t>& moff, cudaStream_t st) {
-  StreamPlan& S = P.sw_bem;
-  S.nitems = 0;
-  S.ncta = 0;
-  const int nt = (int)item_off.size() - 1;
-  std::vector<int4> ch;
-  std::vector<int> leaf_end;  // chunk index after each leaf
-  for (int i = 0; i < nt; ++i) {
-    for (int s = item_off[i]; s < item_off[i + 1]; ++s) {
-      const int4 b = blocks[s];
-      const int mp = (b.y + 3) & ~3, per = std::max(1, std::min(32, 1024 / mp));
-      if (mp > 256 || moff[s] % 4 != 0 || moff[s] / 4 > INT32_MAX) return 1;  // not streamable
-      for (int j = 0; j < b.w; j += per) {
-        const int nr = std::min(per, b.w - j);
-        ch.push_back(make_int4((int)((moff[s] + (int64_t)j * mp) / 4), b.z + j, nr | (mp << 6) | (b.y << 15), b.x));
-      }
-    }
-    if (!ch.empty() && (leaf_end.empty() || (int)ch.size() > leaf_end.back())) {
-      ch.back().z |= 1 << 24;  // the leaf's last chunk
-      leaf_end.push_back((int)ch.size());
-    }
-  }
-  if (ch.empty()) return 0;
-  const int nch = (int)ch.size();
-  const int ncta = std::max(1, std::min(kStreamCtaPerSm * g_num_sms, (int)leaf_end.size()));
-  std::vector<int> cta(ncta + 1, nch);
-  cta[0] = 0;
-  int c = 1;
-  for (int e : leaf_end)  // cut after the leaf whose end reaches the next share of the chunks
-    if (c < ncta && (int64_t)e * ncta >= (int64_t)nch * c) cta[c++] = e;
-  for (; c < ncta; ++c) cta[c] = nch;
-  int4* dch = nullptr;
-  int* dc = nullptr;
-  KIFMM_CUDA(cudaMalloc(&dch, sizeof(int4) * ch.size()));
-  P.allocations.push_back(dch);
-  KIFMM_CUDA(cudaMalloc(&dc, sizeof(int) * cta.size()));
-  P.allocations.push_back(dc);
-  KIFMM_CUDA(cudaMemcpyAsync(dch, ch.data(), sizeof(int4) * ch.size(), cudaMemcpyHostToDevice, st));
-  KIFMM_CUDA(cudaMemcpyAsync(dc, cta.data(), sizeof(int) * cta.size(), cudaMemcpyHostToDevice, st));
-  KIFMM_CUDA(cudaStreamSynchronize(st));
-  S.d_items = dch;
-  S.d_cta = dc;
-  S.nitems = nch;
-  S.ncta = ncta;
-  return 0;
-}
 
 int stream_s2m(const Plan& P, cudaStream_t st) {
   if (P.sw_s2m.nitems == 0) return 0;
