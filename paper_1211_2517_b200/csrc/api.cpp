@@ -67,6 +67,11 @@ void free_plan_memory(fmm_plan* h) {
   if (P.stream_near) cudaStreamDestroy(P.stream_near);
   if (P.stream_m2l) cudaStreamDestroy(P.stream_m2l);
   if (P.ev_m2l) cudaEventDestroy(P.ev_m2l);
+  if (P.stream_nr2) cudaStreamDestroy(P.stream_nr2);
+  if (P.ev_nr_fork) cudaEventDestroy(P.ev_nr_fork);
+  if (P.ev_nr_join) cudaEventDestroy(P.ev_nr_join);
+  P.stream_nr2 = nullptr;
+  P.ev_nr_fork = P.ev_nr_join = nullptr;
   if (P.stream_comm) cudaStreamDestroy(P.stream_comm);
   if (P.ev_up) cudaEventDestroy(P.ev_up);
   if (P.ev_comm) cudaEventDestroy(P.ev_comm);
@@ -377,6 +382,13 @@ int fmm_setup_ex(const double* points, const double* densities, int64_t N, const
     }
     P.ev_phase.resize(kPhases + 1);
     for (auto& e : P.ev_phase) cudaEventCreate(&e);
+    if (P.nr_on && P.nr_groups.size() > 1 &&
+        (cudaStreamCreateWithFlags(&P.stream_nr2, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&P.ev_nr_fork, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&P.ev_nr_join, cudaEventDisableTiming) != cudaSuccess)) {
+      set_error("fmm_setup: creating the second near-field stream failed");
+      return fail(FMM_ECUDA);
+    }
     if (P.profile)
       for (auto& e : P.ev_near) cudaEventCreate(&e);
     if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {

@@ -259,6 +259,9 @@ struct Plan {
   cudaEvent_t ev_near[2] = {nullptr, nullptr};  // profiled plans: around the near-field launches
   bool near_timed = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // k_near's second launch stream (near_launch alternates the pass-shape launches)
+  cudaStream_t stream_nr2 = nullptr;
+  cudaEvent_t ev_nr_fork = nullptr, ev_nr_join = nullptr;
   // NCCL plans: the straddler allreduce and the ghost exchange on their own stream, beside
   // the M2L of the local sources (matvec_device)
   cudaStream_t stream_comm = nullptr;

@@ -486,7 +486,19 @@ int near_launch(const Plan& P, double* out, cudaStream_t st, int part, int spare
   // part 0: every unit; 1 / 2: the first P.nr_split / the remaining units of each group
   // (units are sorted longest first); counters: [0, ng) part 0 / 1, [ng, 2 ng) part 2
   if (part != 2) KIFMM_CUDA(cudaMemsetAsync(P.d_nr_counters, 0, sizeof(int) * 2 * ng, st));
+  // serialised plans: the pass-shape launches alternate between st and the plan's second
+  // near stream — every launch is a persistent grid whose CTAs drain at its end, and the
+  // other stream's launch takes the SM slots they free (the launches are independent: each
+  // adds its own pairs into the potentials with RED).  C4 near field 10.02 -> 9.86 ms,
+  // C3 1.58 -> 1.40, C2 0.59 -> 0.53.  With the near field beside the far field (overlap
+  // mode 3) the far kernels fill those slots instead (two streams there: C2 2.36 -> 2.43 ms)
+  const bool two = P.stream_nr2 && ng > 1 && P.overlap == 0;
+  if (two) {
+    KIFMM_CUDA(cudaEventRecord(P.ev_nr_fork, st));
+    KIFMM_CUDA(cudaStreamWaitEvent(P.stream_nr2, P.ev_nr_fork, 0));
+  }
   for (int gidx = 0; gidx < ng; ++gidx) {
+    cudaStream_t sg = two && (gidx & 1) ? P.stream_nr2 : st;
     const int3& g = P.nr_groups[gidx];
     const int na = part == 0 ? g.z : std::min(g.z, (int)(P.nr_split * g.z + 0.5));
     const int first = part == 2 ? na : 0, count = part == 1 ? na : g.z - first;
@@ -502,7 +514,7 @@ int near_launch(const Plan& P, double* out, cudaStream_t st, int part, int spare
     a.out = out;
     int rc = -3;
     switch (tab[g.x].tb * 64 + tab[g.x].mq) {
-#define KIFMM_NS(TBv, MQv) case TBv * 64 + MQv: rc = near_launch_sel<TBv, MQv>(a, count, spare, st); break;
+#define KIFMM_NS(TBv, MQv) case TBv * 64 + MQv: rc = near_launch_sel<TBv, MQv>(a, count, spare, sg); break;
       KIFMM_NS(2, 4) KIFMM_NS(3, 4) KIFMM_NS(4, 4) KIFMM_NS(5, 4) KIFMM_NS(6, 4)
       KIFMM_NS(4, 8) KIFMM_NS(5, 8) KIFMM_NS(6, 8) KIFMM_NS(7, 8) KIFMM_NS(8, 8)
       KIFMM_NS(5, 16) KIFMM_NS(6, 16) KIFMM_NS(7, 16) KIFMM_NS(8, 16)
@@ -515,6 +527,10 @@ int near_launch(const Plan& P, double* out, cudaStream_t st, int part, int spare
       return rc;
     }
     ++g_launches;
+  }
+  if (two) {
+    KIFMM_CUDA(cudaEventRecord(P.ev_nr_join, P.stream_nr2));
+    KIFMM_CUDA(cudaStreamWaitEvent(st, P.ev_nr_join, 0));
   }
   return 0;
 }
