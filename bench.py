@@ -143,6 +143,8 @@ def run_reference(args):
     pts, q, cfg = synth_inputs.make(args.config)
     sp, sq, what = oracle_sample(args.config, pts, q)
     ns = sp.shape[0]
+    import oracle
+    k_eff = int(oracle.precompute.build_tables(cfg["p"], cfg["k"])["k"])
     # warm-up and timed steps: each step one oracle matvec of the sample
     ts = oracle_matvec_timer(sp, sq, cfg, reps=args.warmup + args.steps)[args.warmup:]
     sec = float(np.mean(ts))
@@ -151,13 +153,20 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong" if not args.weak else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "N": cfg["N"], "p": cfg["p"], "k": cfg["k"], "leaf_size": cfg["leaf"],
-                   "kind": cfg["kind"]},
+        "config": workload_config(args, cfg, 1, k_eff),
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
                          "sample": f"{what}: {ns} points, one oracle matvec per step (oracle/ C++ -O2 OpenMP)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(args, cfg, ws: int, k_eff: int) -> dict:
+    """The workload a line measures (the same dict in both arms): no implementation details."""
+    wl = args.config if ws == 1 or not args.weak else f"{args.config} x{ws} (weak: {ws} tiled copies)"
+    return {"workload": wl, "N": cfg["N"], "N_per_gpu": cfg["N"] // ws, "p": cfg["p"], "k": cfg["k"], "k_eff": k_eff,
+            "leaf_size": cfg["leaf"], "kind": cfg["kind"],
+            "parallelism": "single" if ws == 1 else f"morton-partition{ws} (NCCL ghosts)"}
 
 
 def ncu_evidence(config: str):
@@ -336,22 +345,21 @@ def run_ours(args):
         cpu = {"value": sp.shape[0] / ts[0], "unit": "points/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"{what}: one oracle matvec of {sp.shape[0]} points, oracle/ C++ -O2 OpenMP, {ts[0]:.2f} s"}
     value = N / (ms * 1e-3)
-    wl = args.config if ws == 1 or not args.weak else f"{args.config} x{ws} (weak: {ws} tiled copies)"
-    config = {"workload": wl, "N": N,
-              "N_per_gpu": N // ws, "p": cfg["p"], "k": cfg["k"], "k_eff": k, "leaf_size": cfg["leaf"],
-              "kind": cfg["kind"], "parallelism": "single" if ws == 1 else f"morton-partition{ws} (NCCL ghosts)",
-              "l2": "flushed (256 MiB write) between timed steps",
+    config = workload_config(args, cfg, ws, k)
+    ovl = int(plan.get_info()["overlap"])  # the production plan's mode (the profiled twin runs serialised)
+    method = {"l2": "flushed (256 MiB write) between timed steps",
+              "overlap": ovl,
               "near_field": ("mutual leaf pairs (k_near) on a second stream beside the far field (overlap mode 3)"
-                             if (info["N"] if ws == 1 else N // ws) <= (8 << 20) else
-                             "mutual leaf pairs (k_near), serialised with the far field (> 8M owned points)")}
+                             if ovl == 3 else
+                             "mutual leaf pairs (k_near), serialised with the far field")}
     if ws > 1:
-        config.update(mode="owned", ghost_q_rows_rank0=info["ghost_q_recv"], ghost_dens_rank0=info["ghost_d_recv"],
+        method.update(mode="owned", ghost_q_rows_rank0=info["ghost_q_recv"], ghost_dens_rank0=info["ghost_d_recv"],
                       straddling_boxes=info["n_straddle"])
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak" if args.weak else "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config, "method": method,
         "roofline": roof,
         "kernels": {"m2l": m2l, "p2p": near},
         "phase_ms": phase,
