@@ -6,9 +6,9 @@
 // 3.7 GB for X per matvec).  Each is a persistent grid of single-warp CTAs, kStreamCtaPerSm
 // per SM: lane 0 issues cp.async.bulk copies (SASS UBLKCP) of contiguous operator rows plus
 // the chunk's densities into an NS-stage shared-memory ring, each stage completing on its
-// own mbarrier (expect_tx bytes); the warp consumes stage s while the next NS - 1 stages are
-// in flight, then refills s.  ~200 KB in flight per SM keeps HBM busy with four warps per SM
-// (C4 S2M 6.2 TB/s, 1.39 ms, against 5.1 TB/s for the register-path GEMV).  The waits are
+// own mbarrier (expect_tx bytes); the warp consumes stage s while the other stage is in
+// flight, then refills s.  ~200 KB in flight per SM keeps HBM busy with twelve warps per SM
+// (C4 S2M 6.3 TB/s, 1.36 ms, against 5.1 TB/s for the register-path GEMV).  The waits are
 // mbarrier.try_wait (suspended, not spinning).
 //
 // Work: an item = (first operator row, rows, first weight point, output box):
@@ -31,14 +31,17 @@ namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-constexpr int kStreamCtaPerSm = 4;
+// 12 single-warp CTAs per SM, 2 stages each (~200 KB in flight per SM): measured on C4
+// against 4 x 6 stages (S2M 1.40 / X 0.69 ms), 8 x 3 (1.37 / 0.60), 16 x 2 of 6 KB
+// (1.35 / 0.58); 12 x 2: 1.36 / 0.57 ms
+constexpr int kStreamCtaPerSm = 12;
 
 // rows per stage (the stage also holds up to max(KP, RS + 2) doubles of weights);
-// 4 CTAs x NS stages x ~8.7 KB per SM
+// kStreamCtaPerSm CTAs x NS stages x ~8.7 KB (kp <= 64) / 7.5 KB (kp = 104) per SM
 template <int KP>
 struct StreamShape {
-  static constexpr int RS = KP <= 64 ? 16 : 10;
-  static constexpr int NS = 6;
+  static constexpr int RS = KP <= 64 ? 16 : 8;
+  static constexpr int NS = 2;
   static constexpr int EXTRA = (KP > RS + 2 ? KP : RS + 2);
   static constexpr int STAGE = (RS * KP + EXTRA) * 8;  // bytes (multiple of 16)
   static constexpr int T = (KP + 63) / 64;            // double2 column units per lane
