@@ -258,7 +258,7 @@ struct Sib16Shape {
 template <int KP, int NT, int MINB>
 __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
     const int4* __restrict__ tiles, int ntiles, const int* __restrict__ cols, const int* __restrict__ classes,
-    const double* __restrict__ C, int mvalid, const double* X, double* Y, int* __restrict__ counter) {
+    const double* __restrict__ C, int mvalid, const double* X, double* Y, int* __restrict__ counter, int zero_row) {
   constexpr int RB = Sib16Shape<KP>::RB;
   constexpr int CS = Sib16Shape<KP>::CS;
   constexpr int NW = Sib16Shape<KP>::NW;
@@ -275,12 +275,19 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_meta[3][NT * CW];
   __shared__ int s_tile[3];
+  __shared__ __align__(8) uint64_t s_full[2];  // one mbarrier per B-panel buffer
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int r0 = (warp % RB) * 16;
   const int cbase = (warp / RB) * NCW;
   int ti = blockIdx.x;
   if (ti >= ntiles) return;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&s_full[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t phase[2] = {0u, 0u};  // parity of each buffer's next completion
 
   auto fetch_meta = [&](int tid, int slot) {
     const int4 tl = tiles[tid];
@@ -289,16 +296,39 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
       s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
     }
   };
+  // B panel of one step: every column's source row (KP doubles, contiguous) is one
+  // cp.async.bulk copy (SASS UBLKCP) issued by warp 0, completing on the buffer's mbarrier;
+  // absent sources read the zero row of q^' (row zero_row, never written)
   auto gather = [&](int slot, int b, int buf) {
-    double* Bd = sm + buf * NT * SB;
-    for (int p = warp; p < NT; p += NW) {
-      const int src = s_meta[slot][p * CW + 1 + b];
-      for (int c = lane; c < K2; c += 32) {
-        double* dst = Bd + p * SB + 2 * c;
-        if (src >= 0) cp_async16(dst, X + (size_t)src * KP + 2 * c);
-        else { dst[0] = 0.0; dst[1] = 0.0; }
-      }
+    if (warp != 0) return;
+    const uint32_t bar = (unsigned)__cvta_generic_to_shared(&s_full[buf]);
+    if (lane == 0) {
+      // the buffer was last read through the generic proxy (all warps passed the barrier)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(NT * KP * 8) : "memory");
     }
+    __syncwarp();
+    double* Bd = sm + buf * NT * SB;
+    for (int p = lane; p < NT; p += 32) {
+      const int src = s_meta[slot][p * CW + 1 + b];
+      const double* srow = X + (size_t)(src >= 0 ? src : zero_row) * KP;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              (unsigned)__cvta_generic_to_shared(Bd + p * SB)),
+          "l"(srow), "r"(KP * 8), "r"(bar)
+          : "memory");
+    }
+  };
+  auto wait_panel = [&](int buf) {
+    const uint32_t bar = (unsigned)__cvta_generic_to_shared(&s_full[buf]);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar), "r"(phase[buf])
+          : "memory");
+    phase[buf] ^= 1u;
   };
   // A fragment of k8-step ks: rows r0+g, r0+g+8; columns 8 ks + t, 8 ks + t + 4
   auto op_rows = [&](int id) { return C + (size_t)id * KP * KP + (size_t)(r0 + g) * KP + t; };
@@ -316,7 +346,6 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
   __syncthreads();
   const int* cls = classes + tiles[ti].x * 17;
   gather(0, cls[1], 0);
-  cp_async_commit();
   double a_cur[CH][4];
   const double* Aop = op_rows(cls[9]);
 #pragma unroll
@@ -336,8 +365,8 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
         fetch_meta(tnext, nslot);
         if (threadIdx.x == 0) s_tile[nslot == 2 ? 0 : nslot + 1] = gridDim.x + atomicAdd(counter, 1);
       }
-      cp_async_wait0();
-      __syncthreads();
+      wait_panel(buf);  // this step's B panel has landed
+      __syncthreads();  // every warp is done with the other buffer (and the new s_meta is visible)
       const double* Anext = nullptr;
       if (!last) {
         gather(slot, cls[2 + jb], buf ^ 1);
@@ -347,7 +376,6 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
         gather(nslot, ncls[1], buf ^ 1);
         Anext = op_rows(ncls[9]);
       }
-      cp_async_commit();
       // B fragment (k8-step ks, n-block j): b0 = B[8ks + t][col], b1 = B[8ks + t + 4][col], col = cbase + 8j + g
       const double* B = sm + buf * NT * SB + (size_t)(cbase + g) * SB + t;
 #pragma unroll
@@ -1624,7 +1652,8 @@ int launch_m2l_lowrank(const SibLaunch& g, const LowRank& lr, int kp, int mvalid
 }
 
 template <int KP, int MINB>
-int launch_sib16(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, cudaStream_t st) {
+int launch_sib16(const SibLaunch& g, const double* C, int mvalid, const double* X, double* Y, int zero_row,
+                 cudaStream_t st) {
   constexpr int NT = sq_nt(KP);
   constexpr int NTH = Sib16Shape<KP>::NW * 32;
   const size_t smem = (size_t)NT * 2 * (KP + 4) * sizeof(double);
@@ -1633,16 +1662,17 @@ int launch_sib16(const SibLaunch& g, const double* C, int mvalid, const double* 
   const int grid = std::min(g.ntiles, g_num_sms * std::max(1, per_sm));
   KIFMM_CUDA(cudaMemsetAsync(g.d_counter, 0, sizeof(int), st));
   k_m2l_sib16<KP, NT, MINB><<<grid, NTH, smem, st>>>(g.d_tiles, g.ntiles, g.d_cols, g.d_classes, C, mvalid, X, Y,
-                                                     g.d_counter);
+                                                     g.d_counter, zero_row);
   return 0;
 }
 
-int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, const double* X, double* Y, cudaStream_t st) {
+int launch_m2l_sib(const SibLaunch& g, const double* C, int kp, int mvalid, const double* X, double* Y, int zero_row,
+                   cudaStream_t st) {
   if (g.ntiles == 0) return 0;
   ++g_launches;
-  if (kp == 32) launch_sib16<32, 3>(g, C, mvalid, X, Y, st);
-  else if (kp == 64) launch_sib16<64, 3>(g, C, mvalid, X, Y, st);
-  else if (kp == 104) launch_sib16<104, 3>(g, C, mvalid, X, Y, st);
+  if (kp == 32) launch_sib16<32, 3>(g, C, mvalid, X, Y, zero_row, st);
+  else if (kp == 64) launch_sib16<64, 3>(g, C, mvalid, X, Y, zero_row, st);
+  else if (kp == 104) launch_sib16<104, 3>(g, C, mvalid, X, Y, zero_row, st);
   else return -3;  // kp = round_up(k_eff, 8) with k_eff <= 100 at p <= 8: 32, 64 or 104 only
   KIFMM_CUDA(cudaGetLastError());
   return 0;
@@ -2135,7 +2165,7 @@ int matvec_stage(Plan& P, int stage, const double* d_density, double* d_pot, boo
 // M2L, all levels in one launch per kernel (the dense cores or the stage-2 factors)
 int launch_m2l(const Plan& P, const SibLaunch& g, cudaStream_t st) {
   if (P.lr.on) return launch_m2l_lowrank(g, P.lr, P.kp, P.k, P.d_qhat, P.d_lhat, st);
-  return launch_m2l_sib(g, P.d_C, P.kp, P.k, P.d_qhat, P.d_lhat, st);
+  return launch_m2l_sib(g, P.d_C, P.kp, P.k, P.d_qhat, P.d_lhat, P.tree.nboxes, st);
 }
 
 // One matvec of a single-GPU plan, or of one rank of an NCCL-connected plan.  NCCL plans

@@ -713,7 +713,9 @@ int build_schedules(Plan& P, cudaStream_t st) {
     KIFMM_CUDA(cudaMemsetAsync(*p, 0, sizeof(double) * std::max<size_t>(cnt, 1), st));
     return 0;
   };
-  if (zalloc(&P.d_qhat, (size_t)nb * kp) || zalloc(&P.d_lhat, (size_t)nb * kp) ||
+  // q^' has one extra row, never written: the zero row absent sibling sources point at (the
+  // M2L gathers every column row with one bulk copy)
+  if (zalloc(&P.d_qhat, (size_t)(nb + 1) * kp) || zalloc(&P.d_lhat, (size_t)nb * kp) ||
       zalloc(&P.d_chk_s2m, P.leaf_s2m ? 1 : (size_t)P.n_s2m * np) || zalloc(&P.d_chk_x, P.leaf_x ? 1 : (size_t)P.n_xnd * np) ||
       zalloc(&P.d_eqd_l2t, (size_t)n_l2t * np) || zalloc(&P.d_eqd_w, (size_t)n_wnd * np) ||
       zalloc(&P.d_pot_near, T.N) || zalloc(&P.d_pot_far, T.N) || zalloc(&P.d_io, 2 * T.N))
