@@ -219,10 +219,11 @@ def test_edge_cases():
 
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k", "torus50k"])
-@pytest.mark.parametrize("mode", ["1", "2", "3"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
 def test_overlapped_near_stream(case, mode):
     # near field on a second stream joined before the output (mode 3: all of k_near from the
-    # fork, beside the S2M / M2M GEMVs); repeated matvecs reuse the streams and events
+    # fork, beside the S2M / M2M GEMVs); mode 0 serialised (k_near's pass-shape launches on
+    # two streams); repeated matvecs reuse the streams and events
     pts, q, p, k, s = CASES[case]()
     tb = tables(p, k)
     ref = oracle.Plan(pts, s, tb["n"]).matvec(tb, q)
