@@ -532,9 +532,9 @@ int build_schedules(Plan& P, cudaStream_t st) {
     // Sibling groups (target B, source parent Q) with only some of Q's V-children present
     // (surface trees) become columns of a *masked* class — the class's steps restricted to
     // the present children (same kernel, no absent-child GEMM steps, one RED row per
-    // column) — when that (class, mask) gathers at least mask_min columns; the rest go by
-    // the cost model below (the full class, absent children included, or one-operator
-    // pseudo-classes per pair).
+    // column) — when that (class, mask) gathers at least mask_min columns; the rest go in
+    // runs by the cost model below (the masked class of the run's union of masks, or
+    // one-operator pseudo-classes per pair).
     const int NTs = sib_tile_width(kp, P.lr.on && P.lr.rp <= 32);  // (k_m2l_lr2 takes rp 16 / 32)
     // 256 measured best of 16-2048 (round 1, a since-retired environment switch): C4 M2L 6.50 -> 5.61 ms, C5 29.0 ->
     // 28.0 ms; C3 neutral (below ~512 its sparse masks split into partly filled tiles)
@@ -591,43 +591,65 @@ int build_schedules(Plan& P, cudaStream_t st) {
       cc.push_back(g.b);
       for (int j = 0; j < 8; ++j) cc.push_back(g.src[j]);
     };
-    for (const SibGroup& g : sgs) {
-      if (g.mask == full_mask[g.cls]) { add_col(g.cls, g); continue; }
-      if (mcount[g.cls * 256 + g.mask] >= mask_min) {
-        int& id = vclass[g.cls * 256 + g.mask];
-        if (id < 0) {  // record: the full class's steps whose child is present
-          id = (int)cls_cols.size();
-          cls_cols.emplace_back();
-          std::vector<int> rec(17, -1);
-          const int* fr = &classes[g.cls * 17];
-          int nv = 0;
-          for (int j = 0; j < fr[0]; ++j)
-            if (g.mask >> fr[1 + j] & 1) { rec[1 + nv] = fr[1 + j]; rec[9 + nv] = fr[9 + j]; ++nv; }
-          rec[0] = nv;
-          classes.insert(classes.end(), rec.begin(), rec.end());
-          nvalid.push_back(nv);
-        }
-        add_col(id, g);
-        continue;
+    auto masked_class = [&](int cls, int mask) -> int {  // the full class's steps whose child is present
+      int& id = vclass[cls * 256 + mask];
+      if (id < 0) {
+        id = (int)cls_cols.size();
+        cls_cols.emplace_back();
+        std::vector<int> rec(17, -1);
+        const int* fr = &classes[cls * 17];
+        int nv = 0;
+        for (int j = 0; j < fr[0]; ++j)
+          if (mask >> fr[1 + j] & 1) { rec[1 + nv] = fr[1 + j]; rec[9 + nv] = fr[9 + j]; ++nv; }
+        rec[0] = nv;
+        classes.insert(classes.end(), rec.begin(), rec.end());
+        nvalid.push_back(nv);
       }
-      // cost model (per column, FP64 peak 37 TF/s, fp64 L2 RED 5.2e11/s): the sibling
-      // kernel spends nvalid GEMM columns + 1 RED row, offset-major cnt x (GEMM + RED row);
-      // the RED weight 0.5 is the measured best of 0.25 / 0.5 / 1 / 2 over C3-C5
-      // (round 1: C4 M2L 6.49 ms at 0.5 vs 6.51 at 1; C5 29.0 vs 29.2)
-      constexpr double red_scale = 0.5;
-      const double Gc = 2.0 * kp * kp / 37e12, Rr = red_scale * kp / 5.2e11;
-      if (g.cnt * (Gc + Rr) >= nvalid[g.cls] * Gc + Rr) {
-        add_col(g.cls, g);
-      } else {
-        for (int j = 0; j < 8; ++j) {
-          if (g.src[j] < 0) continue;
-          int o = -1;  // the pair's offset id: the class step of child j
-          for (int t = 0; t < classes[g.cls * 17]; ++t)
-            if (classes[g.cls * 17 + 1 + t] == j) o = classes[g.cls * 17 + 9 + t];
-          auto& cc = cls_cols[kSib + o];  // a one-operator pseudo-class column
-          cc.push_back(g.b);
-          cc.push_back(g.src[j]);
-          for (int t = 1; t < 8; ++t) cc.push_back(-1);
+      return id;
+    };
+    std::vector<std::vector<int>> sparse(kSib);  // per class: its remaining sparse groups
+    for (int i = 0; i < (int)sgs.size(); ++i) {
+      const SibGroup& g = sgs[i];
+      if (g.mask == full_mask[g.cls]) add_col(g.cls, g);
+      else if (mcount[g.cls * 256 + g.mask] >= mask_min) add_col(masked_class(g.cls, g.mask), g);
+      else sparse[g.cls].push_back(i);
+    }
+    // The sparse groups of a class, ordered by mask, in runs of one tile: a run becomes
+    // columns of the masked class of its masks' union (absent children inside the union
+    // are zero GEMM columns; one RED row per column) or one-operator pseudo-class columns
+    // (one RED row per pair), whichever the cost model prices lower.  Cost per column
+    // (FP64 peak 37 TF/s, fp64 L2 RED 5.2e11/s; the RED weight 0.5 is the measured best of
+    // 0.25 / 0.5 / 1 / 2 over C3-C5 in round 1).
+    // (round 2, with the runs: 0.25 / 0.5 / 1 / 2 / 4 / all-union: C3 M2L 1.966 / 1.976 /
+    // 2.009 / 2.049 / 2.093 / 2.152 ms, C4 5.42-5.48 — the union's zero columns cost more
+    // than the REDs they save)
+    constexpr double red_scale = 0.5;
+    const double Gc = 2.0 * kp * kp / 37e12, Rr = red_scale * kp / 5.2e11;
+    for (int c = 0; c < kSib; ++c) {
+      std::vector<int>& sp = sparse[c];
+      std::stable_sort(sp.begin(), sp.end(), [&](int x, int y) { return sgs[x].mask < sgs[y].mask; });
+      for (size_t r0 = 0; r0 < sp.size(); r0 += NTs) {
+        const size_t r1 = std::min(sp.size(), r0 + NTs);
+        int u = 0, pairs = 0;
+        for (size_t r = r0; r < r1; ++r) { u |= sgs[sp[r]].mask; pairs += sgs[sp[r]].cnt; }
+        const double cu = (double)(r1 - r0) * (__builtin_popcount(u) * Gc + Rr), cp = pairs * (Gc + Rr);
+        if (cu <= cp) {
+          const int id = u == full_mask[c] ? c : masked_class(c, u);
+          for (size_t r = r0; r < r1; ++r) add_col(id, sgs[sp[r]]);
+          continue;
+        }
+        for (size_t r = r0; r < r1; ++r) {
+          const SibGroup& g = sgs[sp[r]];
+          for (int j = 0; j < 8; ++j) {
+            if (g.src[j] < 0) continue;
+            int o = -1;  // the pair's offset id: the class step of child j
+            for (int t = 0; t < classes[g.cls * 17]; ++t)
+              if (classes[g.cls * 17 + 1 + t] == j) o = classes[g.cls * 17 + 9 + t];
+            auto& cc = cls_cols[kSib + o];  // a one-operator pseudo-class column
+            cc.push_back(g.b);
+            cc.push_back(g.src[j]);
+            for (int t = 1; t < 8; ++t) cc.push_back(-1);
+          }
         }
       }
     }
