@@ -1,6 +1,7 @@
 """Per-phase timing of one matvec config on the GPU (diagnostics, not the bench).
 
-    python tools/phase_timing.py C2 [C4 ...] [reps]  (profiled plans; near_ms = the k_near launches alone)
+    python tools/phase_timing.py C2 [C4 ...] [reps] [ovl=4]  (profiled plans; near_ms = the k_near
+    launches alone — in overlap mode 4 with the S2M / X streams they carry)
 """
 import json
 import os
@@ -14,7 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1211_2517_b200 as K  # noqa: E402
 import synth_inputs  # noqa: E402
 
-names = [a for a in sys.argv[1:] if not a.isdigit()] or ["C2"]
+ovl = int(([a[4:] for a in sys.argv[1:] if a.startswith("ovl=")] or [0])[0])
+names = [a for a in sys.argv[1:] if not a.isdigit() and not a.startswith("ovl=")] or ["C2"]
 reps = int(([a for a in sys.argv[1:] if a.isdigit()] or [5])[0])
 for name in names:
     pts, q, cfg = synth_inputs.make(name)
@@ -22,7 +24,7 @@ for name in names:
     P = torch.from_numpy(pts).to(dev)
     Q = torch.from_numpy(q).to(dev)
     t0 = time.time()
-    plan = K.Plan(P, Q, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True)
+    plan = K.Plan(P, Q, p=cfg["p"], k=cfg["k"], leaf_size=cfg["leaf"], profile=True, overlap=ovl)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     out = plan.matvec(Q)
