@@ -262,26 +262,27 @@ def run_ours(args):
     info = pplan.get_info()
     del pplan
     # ---- end to end through the C-ABI with host buffers (pinned), H2D + D2H inside the timing
+    # (the batched call pipelines the steps: step i + 1's density is copied in and step
+    # i - 1's potential copied out while step i computes; every step still copies its input
+    # from and its result to pinned host memory inside the timed region)
+    e2e_steps = max(5, args.steps // 2)
     if ws > 1:
         hq = torch.from_numpy(q[perm[lo:hi]].copy()).pin_memory()
-        hp = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
-        e2e_call = lambda: plan.matvec_owned_host(hq.numpy(), hp.numpy())
+        hp = [torch.empty(hi - lo, dtype=torch.float64).pin_memory() for _ in range(2)]
+        e2e_call = lambda k: plan.matvec_owned_host_batch([hq.numpy()] * k, [hp[i & 1].numpy() for i in range(k)])
         e2e_bytes = 8 * (hi - lo)
-        e2e_api = "fmm_matvec_owned_host (pinned host buffers, owned points)"
+        e2e_api = "fmm_matvec_owned_host_batch (pinned host buffers, owned points; copies overlapped with compute)"
     else:
         hq = torch.from_numpy(q).pin_memory()
-        hp = torch.empty(N, dtype=torch.float64).pin_memory()
-        e2e_call = lambda: plan.matvec_host(hq.numpy(), hp.numpy())
+        hp = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(2)]
+        e2e_call = lambda k: plan.matvec_host_batch([hq.numpy()] * k, [hp[i & 1].numpy() for i in range(k)])
         e2e_bytes = 8 * N
-        e2e_api = "fmm_matvec_host (pinned host buffers)"
-    for _ in range(3):
-        e2e_call()
+        e2e_api = "fmm_matvec_host_batch (pinned host buffers; copies overlapped with compute)"
+    e2e_call(3)
     if ws > 1:
         dist.barrier()
-    e2e_steps = max(5, args.steps // 2)
     te = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_call()
+    e2e_call(e2e_steps)
     e2e_s = (time.perf_counter() - te) / e2e_steps
     if ws > 1:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)

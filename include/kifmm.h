@@ -200,6 +200,19 @@ int fmm_matvec_owned(fmm_plan* plan, const double* density_owned, double* potent
 /* Same with HOST buffers (copies inside; returns after the stream synchronised). */
 int fmm_matvec_owned_host(fmm_plan* plan, const double* h_density_owned, double* h_potential_owned, void* stream);
 
+/* `count` matvecs with HOST buffers (pinned host memory for the copies to overlap):
+ * h_density[i] -> h_potential[i], each [N] in caller order (the _owned_ form: [own_hi -
+ * own_lo] in sorted order, as fmm_matvec_owned).  Same results as `count` calls of
+ * fmm_matvec_host, but pipelined: the density of matvec i + 1 is copied in (one copy
+ * stream) and the potential of matvec i - 1 copied out (another) while matvec i computes
+ * on `stream`, through two device staging pairs allocated on first use (2 N doubles).
+ * Buffers may repeat (the same density for every i).  Returns after all copies have
+ * landed.  FMM_EINVAL for a null buffer or count < 0. */
+int fmm_matvec_host_batch(fmm_plan* plan, const double* const* h_density, double* const* h_potential, int count,
+                          void* stream);
+int fmm_matvec_owned_host_batch(fmm_plan* plan, const double* const* h_density_owned,
+                                double* const* h_potential_owned, int count, void* stream);
+
 /* Solve A x = rhs with restarted GMRES(restart) (the paper's solver,
  * P:528, tolerance 1e-6 at P:539), A = the plan's matvec (single-GPU plans; with BEM
  * triangles, the collocation operator).  Device vectors in caller order; x holds the

@@ -73,7 +73,8 @@ EXPORTS = ("fmm_default_options", "fmm_setup", "fmm_setup_ex", "fmm_matvec", "fm
            "fmm_info", "fmm_export_tree", "fmm_export_lists", "fmm_export_phase", "fmm_tables_build",
            "fmm_tables_view_get", "fmm_tables_free", "fmm_last_error", "fmm_matvec_owned", "fmm_matvec_owned_host",
            "fmm_owned_range", "fmm_nccl_unique_id", "fmm_matvec_group", "fmm_partition_host", "fmm_partition_get",
-           "fmm_partition_free", "fmm_plan_partition", "fmm_gmres", "fmm_tables_save", "fmm_tables_load")
+           "fmm_partition_free", "fmm_plan_partition", "fmm_gmres", "fmm_tables_save", "fmm_tables_load",
+           "fmm_matvec_host_batch", "fmm_matvec_owned_host_batch")
 
 _lib = None
 
@@ -108,6 +109,8 @@ def lib():
         L.fmm_last_error.restype = ctypes.c_char_p
         L.fmm_matvec_owned.argtypes = [vp, vp, vp, vp]
         L.fmm_matvec_owned_host.argtypes = [vp, vp, vp, vp]
+        L.fmm_matvec_host_batch.argtypes = [vp, vp, vp, ci, vp]
+        L.fmm_matvec_owned_host_batch.argtypes = [vp, vp, vp, ci, vp]
         L.fmm_owned_range.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.fmm_nccl_unique_id.argtypes = [vp]
         L.fmm_matvec_group.argtypes = [ctypes.POINTER(vp), ci, ctypes.POINTER(vp), ctypes.POINTER(vp), ci, vp]
@@ -353,6 +356,36 @@ class Plan:
         _check(lib().fmm_matvec_owned_host(self._h, density_owned.ctypes.data, out.ctypes.data, _stream_ptr(stream)),
                "fmm_matvec_owned_host")
         return out
+
+    def _host_batch(self, fn, name, densities, outs, n, stream):
+        densities = [np.ascontiguousarray(d, dtype=np.float64) for d in densities]
+        if outs is None:
+            outs = [np.empty(n, dtype=np.float64) for _ in densities]
+        if len(outs) != len(densities):
+            raise ValueError("one output per density")
+        for d in densities:
+            if d.shape != (n,):
+                raise ValueError(f"every density must have shape ({n},)")
+        for o in outs:
+            if not (isinstance(o, np.ndarray) and o.dtype == np.float64 and o.shape == (n,)
+                    and o.flags.c_contiguous and o.flags.writeable):
+                raise TypeError(f"every out must be a writeable contiguous float64 array of shape ({n},)")
+        cnt = len(densities)
+        dp = (ctypes.c_void_p * max(cnt, 1))(*[d.ctypes.data for d in densities])
+        op = (ctypes.c_void_p * max(cnt, 1))(*[o.ctypes.data for o in outs])
+        _check(fn(self._h, ctypes.cast(dp, ctypes.c_void_p), ctypes.cast(op, ctypes.c_void_p), cnt,
+                  _stream_ptr(stream)), name)
+        return outs
+
+    def matvec_host_batch(self, densities, outs=None, stream=None):
+        """len(densities) matvecs with host buffers (pinned for overlap), H2D / D2H copies
+        overlapped with the neighbouring matvecs' compute (fmm_matvec_host_batch)."""
+        return self._host_batch(lib().fmm_matvec_host_batch, "fmm_matvec_host_batch", densities, outs, self.N, stream)
+
+    def matvec_owned_host_batch(self, densities_owned, outs=None, stream=None):
+        lo, hi = self.owned_range
+        return self._host_batch(lib().fmm_matvec_owned_host_batch, "fmm_matvec_owned_host_batch", densities_owned,
+                                outs, hi - lo, stream)
 
     def gmres(self, rhs, x0=None, restart: int = 50, maxit: int = 500, tol: float = 1e-6, stream=None):
         """Solve (this plan's operator) x = rhs by restarted GMRES on the device (fmm_gmres).

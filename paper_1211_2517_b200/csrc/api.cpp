@@ -1,6 +1,7 @@
 // C-ABI of the B200 KIFMM library (include/kifmm.h).
 #include "../../include/kifmm.h"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -81,6 +82,15 @@ void free_plan_memory(fmm_plan* h) {
     if (e) cudaEventDestroy(e);
     e = nullptr;
   }
+  for (auto& e : P.ev_io) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
+  if (P.stream_h2d) cudaStreamDestroy(P.stream_h2d);
+  if (P.stream_d2h) cudaStreamDestroy(P.stream_d2h);
+  P.stream_h2d = P.stream_d2h = nullptr;
+  if (P.d_io2) cudaFree(P.d_io2);
+  P.d_io2 = nullptr;
   P.ev_fork = P.ev_join = P.ev_m2l = nullptr;
   P.stream_near = P.stream_m2l = nullptr;
   kifmm::nccl_comm_destroy(P);
@@ -655,6 +665,99 @@ int fmm_matvec_host(fmm_plan* h, const double* h_density, double* h_potential, v
       return FMM_ECUDA;
     }
     return FMM_OK;
+  });
+}
+
+// Several matvecs with host buffers, copies overlapped with compute: matvec i reads
+// staging pair i % 2; its density's H2D runs on a copy stream while matvec i - 1 computes,
+// its potential's D2H on another copy stream while matvec i + 1 computes.  Events order
+// each staging buffer's reuse (H2D into a pair waits for the matvec two steps back to have
+// read it; that matvec's output waits for the D2H two steps back).
+static int matvec_host_batch(fmm_plan* h, const double* const* hq, double* const* hp, int count, bool owned,
+                             cudaStream_t st) {
+  kifmm::Plan& P = h->P;
+  const int64_t N = P.tree.N;
+  const int64_t cnt = owned ? P.dist.own_hi - P.dist.own_lo : N;
+  if (!P.d_io2 && cudaMalloc(&P.d_io2, sizeof(double) * 2 * std::max<int64_t>(N, 1)) != cudaSuccess) {
+    set_error("fmm_matvec_host_batch: staging buffers: out of device memory");
+    return FMM_ENOMEM;
+  }
+  if (!P.stream_h2d && (cudaStreamCreateWithFlags(&P.stream_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+                        cudaStreamCreateWithFlags(&P.stream_d2h, cudaStreamNonBlocking) != cudaSuccess)) {
+    set_error("fmm_matvec_host_batch: creating the copy streams failed");
+    return FMM_ECUDA;
+  }
+  for (auto& e : P.ev_io)
+    if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      set_error("fmm_matvec_host_batch: creating events failed");
+      return FMM_ECUDA;
+    }
+  cudaEvent_t* ev_in = P.ev_io;       // density staged
+  cudaEvent_t* ev_done = P.ev_io + 2; // matvec finished (input read, output written)
+  cudaEvent_t* ev_out = P.ev_io + 4;  // potential copied out
+  double* din[2] = {P.d_io, P.d_io2};
+  double* dout[2] = {P.d_io + N, P.d_io2 + N};
+  auto cuda = [&](cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return true;
+    set_error(std::string("fmm_matvec_host_batch: ") + what + ": " + cudaGetErrorString(e));
+    return false;
+  };
+  // the copy streams start after the work already queued on st (which may use d_io)
+  if (!cuda(cudaEventRecord(P.ev_io[6], st), "event") || !cuda(cudaStreamWaitEvent(P.stream_h2d, P.ev_io[6], 0), "wait") ||
+      !cuda(cudaStreamWaitEvent(P.stream_d2h, P.ev_io[6], 0), "wait"))
+    return FMM_ECUDA;
+  for (int i = 0; i < count; ++i) {
+    const int b = i & 1;
+    if (i >= 2 && !cuda(cudaStreamWaitEvent(P.stream_h2d, ev_done[b], 0), "wait")) return FMM_ECUDA;
+    if (cnt > 0 && !cuda(cudaMemcpyAsync(din[b], hq[i], sizeof(double) * cnt, cudaMemcpyHostToDevice, P.stream_h2d), "H2D copy"))
+      return FMM_ECUDA;
+    if (!cuda(cudaEventRecord(ev_in[b], P.stream_h2d), "event") || !cuda(cudaStreamWaitEvent(st, ev_in[b], 0), "wait"))
+      return FMM_ECUDA;
+    if (i >= 2 && !cuda(cudaStreamWaitEvent(st, ev_out[b], 0), "wait")) return FMM_ECUDA;
+    const int rc = kifmm::matvec_device(P, din[b], dout[b], owned, st);
+    if (rc) return rc == -5 ? FMM_ENCCL : FMM_ECUDA;
+    if (!cuda(cudaEventRecord(ev_done[b], st), "event") || !cuda(cudaStreamWaitEvent(P.stream_d2h, ev_done[b], 0), "wait"))
+      return FMM_ECUDA;
+    if (cnt > 0 && !cuda(cudaMemcpyAsync(hp[i], dout[b], sizeof(double) * cnt, cudaMemcpyDeviceToHost, P.stream_d2h), "D2H copy"))
+      return FMM_ECUDA;
+    if (!cuda(cudaEventRecord(ev_out[b], P.stream_d2h), "event")) return FMM_ECUDA;
+  }
+  // st is ordered after the last D2H (a later call may reuse the staging buffers)
+  if (!cuda(cudaEventRecord(P.ev_io[6], P.stream_d2h), "event") || !cuda(cudaStreamWaitEvent(st, P.ev_io[6], 0), "wait") ||
+      !cuda(cudaStreamSynchronize(st), "synchronize"))
+    return FMM_ECUDA;
+  return FMM_OK;
+}
+
+int fmm_matvec_host_batch(fmm_plan* h, const double* const* h_density, double* const* h_potential, int count,
+                          void* stream) {
+  return guard("fmm_matvec_host_batch", [&]() -> int {
+    if (!h || count < 0 || (count > 0 && (!h_density || !h_potential))) {
+      set_error("fmm_matvec_host_batch: null argument or negative count");
+      return FMM_EINVAL;
+    }
+    for (int i = 0; i < count; ++i)
+      if (!h_density[i] || !h_potential[i]) { set_error("fmm_matvec_host_batch: null buffer"); return FMM_EINVAL; }
+    if (h->P.dist.nranks > 1 && !h->P.nccl_comm) { set_error("fmm_matvec_host_batch: loopback plan, use fmm_matvec_group"); return FMM_EINVAL; }
+    return matvec_host_batch(h, h_density, h_potential, count, false, (cudaStream_t)stream);
+  });
+}
+
+int fmm_matvec_owned_host_batch(fmm_plan* h, const double* const* h_density_owned, double* const* h_potential_owned,
+                                int count, void* stream) {
+  return guard("fmm_matvec_owned_host_batch", [&]() -> int {
+    if (!h || count < 0 || (count > 0 && (!h_density_owned || !h_potential_owned))) {
+      set_error("fmm_matvec_owned_host_batch: null argument or negative count");
+      return FMM_EINVAL;
+    }
+    const kifmm::DistPlan& D = h->P.dist;
+    for (int i = 0; i < count; ++i)
+      if (D.own_hi > D.own_lo && (!h_density_owned[i] || !h_potential_owned[i])) {
+        set_error("fmm_matvec_owned_host_batch: null buffer");
+        return FMM_EINVAL;
+      }
+    if (D.nranks > 1 && !h->P.nccl_comm) { set_error("fmm_matvec_owned_host_batch: loopback plan, use fmm_matvec_group"); return FMM_EINVAL; }
+    return matvec_host_batch(h, h_density_owned, h_potential_owned, count, true, (cudaStream_t)stream);
   });
 }
 

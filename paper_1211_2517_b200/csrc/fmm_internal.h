@@ -189,6 +189,11 @@ struct Plan {
   double* d_pot_near = nullptr; // N (sorted)
   double* d_pot_far = nullptr;  // N (sorted)
   double* d_io = nullptr;       // N staging for host-buffer matvec
+  // batched host-buffer matvecs (fmm_matvec_host_batch): a second staging pair, copy
+  // streams and per-buffer events, created on first use
+  double* d_io2 = nullptr;
+  cudaStream_t stream_h2d = nullptr, stream_d2h = nullptr;
+  cudaEvent_t ev_io[7] = {};  // in[2], done[2], out[2], start
   // evaluation work lists (k_eval items: (box, out row, 0, 0); CSR of segments (kind, a, b, len))
   int np = 0;                                  // n rounded up to a multiple of 8
   int n_tleaf = 0; int4* d_tleaf_items = nullptr;

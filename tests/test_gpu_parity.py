@@ -212,10 +212,42 @@ def test_edge_cases():
     assert par(gp.matvec().cpu().numpy(), gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
     host = gp.matvec_host(q)
     assert par(host, gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()) < 1e-14
+    a_ref = gp.matvec(torch.from_numpy(q2).to(dev)).cpu().numpy()
+    host_ref = gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
+    check_host_batch(gp, q, q2, host_ref, a_ref)
     # exact 2x scaling (up to atomic reduction order)
     s1 = gpu_plan(pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
     s2 = gpu_plan(2 * pts, 4, 24, 64, tb=tb).matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
     assert par(s2, 0.5 * s1) < 1e-14
+
+
+def check_host_batch(gp, q, q2, ref_q, ref_q2):
+    """fmm_matvec_host_batch / fmm_matvec_owned_host_batch: pipelined host-buffer matvecs
+    (copies overlapped with compute) give the single matvecs' results; repeated buffers,
+    an odd count (both staging pairs, one reused) and count 0."""
+    hq = torch.from_numpy(q).pin_memory().numpy()
+    hq2 = torch.from_numpy(q2).pin_memory().numpy()
+    outs = gp.matvec_host_batch([hq, hq2, hq, hq2, hq])
+    for o, r in zip(outs, [ref_q, ref_q2, ref_q, ref_q2, ref_q]):
+        assert par(o, r) < 1e-14
+    assert gp.matvec_host_batch([]) == []
+    # owned form on a one-rank plan: sorted order, the whole range
+    lo, hi = gp.owned_range
+    perm = gp.export_tree()["perm"]
+    own = gp.matvec_owned_host_batch([q[perm[lo:hi]], q2[perm[lo:hi]], q[perm[lo:hi]]])
+    for o, r in zip(own, [ref_q, ref_q2, ref_q]):
+        assert par(o, r[perm[lo:hi]]) < 1e-14
+
+
+def test_host_batch_torus():
+    # a p = 6 plan with X / W lists and the streamed leaf operators, batch of 4
+    pts, q = synth_inputs.torus(50000)
+    gp = gpu_plan(pts, 6, 60, 128, tb=tables(6, 60))
+    dev = torch.device("cuda:0")
+    q2 = np.random.default_rng(6).uniform(-1, 1, q.size)
+    ref_q = gp.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()
+    ref_q2 = gp.matvec(torch.from_numpy(q2).to(dev)).cpu().numpy()
+    check_host_batch(gp, q, q2, ref_q, ref_q2)
 
 
 @pytest.mark.parametrize("case", ["sphere6k_s16", "octa_sphere32k", "torus50k"])

@@ -24,8 +24,11 @@ def raw(rep):
             except ValueError:
                 d[h] = v
                 continue
-            scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "usecond": 1e-3, "msecond": 1.0,
-                     "nsecond": 1e-6}.get(u, 1.0)
+            # times to ms, bytes to bytes (ncu picks the unit per value: a short kernel's
+            # duration comes in us, a long one's in ms)
+            scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+                     "B": 1.0, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6,
+                     "ns": 1e-6, "second": 1e3, "s": 1e3}.get(u, 1.0)
             d[h] = x * scale
         res.append(d)
     return res
