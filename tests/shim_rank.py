@@ -34,7 +34,8 @@ rep = plan.matvec(torch.from_numpy(q).to(dev)).cpu().numpy()   # REPLICATED: all
 lo, hi = plan.owned_range
 perm = plan.export_tree()["perm"]
 own = plan.matvec_owned(torch.from_numpy(q[perm[lo:hi]].copy()).to(dev)).cpu().numpy()
-own2 = plan.matvec_owned(torch.from_numpy(q[perm[lo:hi]].copy()).to(dev)).cpu().numpy()  # reuse
+# reuse, through the pipelined host-buffer batch (copy streams around the NCCL matvecs)
+own2 = plan.matvec_owned_host_batch([q[perm[lo:hi]].copy()] * 2)[1]
 np.savez(os.path.join(work, f"out_{rank}.npz"), rep=rep, own=own, own2=own2, lo=lo, hi=hi, perm=perm,
          overlap=plan.info["overlap"], ghost_q=plan.info["ghost_q_recv"], straddle=plan.info["n_straddle"])
 plan.free()

@@ -86,7 +86,7 @@ def test_nccl_transport_multiprocess(shim, tmp_path, case, nranks, overlap):
         owned2[perm[lo:hi]] = r["own2"]
         errs[f"rep{i}"] = par(r["rep"], ref)  # REPLICATED: every rank holds the whole potential
     errs["owned"] = par(owned, ref)
-    errs["owned_again"] = par(owned2, ref)  # the same plans, a second OWNED matvec
+    errs["owned_again"] = par(owned2, ref)  # the same plans, OWNED again through the host batch
     assert max(errs.values()) <= TOL, errs
     # the exchanges moved data: ghost multipole rows and straddling boxes on every rank
     assert all(int(r["ghost_q"]) > 0 for r in res)
