@@ -151,6 +151,90 @@ __global__ void __launch_bounds__(128) k_mut_part(double* out, const double4* __
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// VAR 6 (k_mut_lane): the transposed layout — every lane of a warp holds the SAME TB
+// targets (the warp's), the lanes take different sources (lane l: sources l, l + 32, ...),
+// so a source's reverse sum over the warp's targets is complete in one lane: no
+// reduce-scatter.  W warps hold W x TB targets; per 256-source chunk each warp stores its
+// per-source partials to shared memory, one barrier, then each thread sums the W partials
+// of 2 sources and adds them with RED (double-buffered partials).
+template <int TB, int W>
+__global__ void __launch_bounds__(W * 32) k_mut_lane(double* out, const double4* __restrict__ src, int ns, int reps,
+                                                     double* pot) {
+  constexpr int CHK = 256, NTH = W * 32;
+  __shared__ double4 sb[CHK];
+  __shared__ int sidx[CHK];
+  __shared__ double part[2][W][CHK];
+  for (int j = threadIdx.x; j < CHK; j += NTH) {
+    sb[j] = src[j];
+    sidx[j] = (int)(((unsigned)(j + 1) * 2654435761u + blockIdx.x * 40503u) & ((1u << 22) - 1));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double x[TB][3], q[TB], acc[TB];
+#pragma unroll
+  for (int u = 0; u < TB; ++u) {
+    x[u][0] = 0.5 + 1e-4 * (w + 7 * u); x[u][1] = 0.25 + 3e-6 * u + 1e-5 * w; x[u][2] = -0.125 * u + 1e-7 * w;
+    q[u] = 0.1 * u; acc[u] = 0;
+  }
+  int pb = 0;
+  for (int r = 0; r < reps * (ns / CHK); ++r) {
+    double* pw = &part[pb][w][0];
+#pragma unroll 2
+    for (int j = lane; j < CHK; j += 32) {
+      const double4 sv = sb[j];
+      double sj = 0.0;
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        const double dx = x[u][0] - sv.x, dy = x[u][1] - sv.y, dz = x[u][2] - sv.z;
+        const double g = rinv(fma(dz, dz, fma(dy, dy, dx * dx)));
+        acc[u] = fma(sv.w, g, acc[u]);
+        sj = fma(q[u], g, sj);
+      }
+      pw[j] = sj;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < CHK; j += NTH) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < W; ++t) s += part[pb][t][j];
+      atomicAdd(pot + sidx[j], s * 0.0795);
+    }
+    pb ^= 1;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < TB; ++u) s += acc[u];
+  out[blockIdx.x * NTH + threadIdx.x] = s;
+}
+
+template <int TB, int W>
+void run_lane(double* out, const double4* src, int ns, double* pot) {
+  const int reps = 40;
+  int per_sm = 0;
+  cudaFuncSetAttribute(k_mut_lane<TB, W>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mut_lane<TB, W>, W * 32, 0);
+  const int grid = 148 * per_sm;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  for (int i = 0; i < 4; ++i) {
+    cudaEventRecord(a);
+    k_mut_lane<TB, W><<<grid, W * 32>>>(out, src, ns, reps, pot);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (i && ms < best) best = ms;
+  }
+  const double pairs = (double)grid * W * TB * 256.0 * (ns / 256) * reps;  // unordered target-source pairs
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const double peak = 148.0 * 64 * clk * 1e3;
+  printf("{\"TB\": %d, \"W\": %d, \"var\": 6, \"ctas_per_sm\": %d, \"pairs_per_s\": %.4g, \"fp64_instr_frac\": %.3f}\n",
+         TB, W, per_sm, pairs / (best * 1e-3), pairs * 13.0 / (best * 1e-3) / peak);
+}
+
 template <int TB, int MQ = 8>
 void run_part(double* out, const double4* src, int ns, double* pot) {
   const int reps = 40;
@@ -239,6 +323,12 @@ int main() {
   run_part<6>(out, src, ns, pot);
   run_part<4>(out, src, ns, pot);
   run_part<5, 4>(out, src, ns, pot);
+  run_lane<5, 8>(out, src, ns, pot);
+  run_lane<8, 4>(out, src, ns, pot);
+  run_lane<8, 5>(out, src, ns, pot);
+  run_lane<7, 5>(out, src, ns, pot);
+  run_lane<6, 4>(out, src, ns, pot);
+  run_lane<4, 4>(out, src, ns, pot);
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
