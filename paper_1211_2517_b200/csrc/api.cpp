@@ -673,8 +673,20 @@ int fmm_matvec_host(fmm_plan* h, const double* h_density, double* h_potential, v
 // its potential's D2H on another copy stream while matvec i + 1 computes.  Events order
 // each staging buffer's reuse (H2D into a pair waits for the matvec two steps back to have
 // read it; that matvec's output waits for the D2H two steps back).
+static int matvec_host_batch_body(fmm_plan* h, const double* const* hq, double* const* hp, int count, bool owned,
+                                  cudaStream_t st);
 static int matvec_host_batch(fmm_plan* h, const double* const* hq, double* const* hp, int count, bool owned,
                              cudaStream_t st) {
+  const int rc = matvec_host_batch_body(h, hq, hp, count, owned, st);
+  if (rc != FMM_OK) {  // no copy may still touch the caller's host buffers after an error return
+    if (h->P.stream_h2d) cudaStreamSynchronize(h->P.stream_h2d);
+    if (h->P.stream_d2h) cudaStreamSynchronize(h->P.stream_d2h);
+  }
+  return rc;
+}
+
+static int matvec_host_batch_body(fmm_plan* h, const double* const* hq, double* const* hp, int count, bool owned,
+                                  cudaStream_t st) {
   kifmm::Plan& P = h->P;
   const int64_t N = P.tree.N;
   const int64_t cnt = owned ? P.dist.own_hi - P.dist.own_lo : N;
