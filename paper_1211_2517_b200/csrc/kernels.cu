@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
   static_assert(KS8 % CH == 0 && NB >= 1, "tile shape");
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_meta[3][NT * CW];
+  __shared__ int s_cls[3][17];  // each ring slot's class record (steps, children, offset ids)
   __shared__ int s_tile[3];
   __shared__ __align__(8) uint64_t s_full[2];  // one mbarrier per B-panel buffer
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -289,12 +290,15 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
   }
   uint32_t phase[2] = {0u, 0u};  // parity of each buffer's next completion
 
+  // a tile's column records and its class record into ring slot `slot` (read after the
+  // next CTA barrier: no dependent global load at the tile boundary)
   auto fetch_meta = [&](int tid, int slot) {
     const int4 tl = tiles[tid];
     for (int e = threadIdx.x; e < NT * CW; e += NTH) {
       const int c = e / CW;
       s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
     }
+    if (threadIdx.x < 17) s_cls[slot][threadIdx.x] = classes[tl.x * 17 + threadIdx.x];
   };
   // B panel of one step: every column's source row (KP doubles, contiguous) is one
   // cp.async.bulk copy (SASS UBLKCP) issued by warp 0, completing on the buffer's mbarrier;
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
   fetch_meta(ti, 0);
   if (threadIdx.x == 0) s_tile[1] = gridDim.x + atomicAdd(counter, 1);
   __syncthreads();
-  const int* cls = classes + tiles[ti].x * 17;
+  const int* cls = s_cls[0];
   gather(0, cls[1], 0);
   double a_cur[CH][4];
   const double* Aop = op_rows(cls[9]);
@@ -359,12 +363,17 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
     const int nv = cls[0];
     const int nslot = slot == 2 ? 0 : slot + 1;
     const int tnext = s_tile[nslot];
+    // thread 0 claims the tile after next at this tile's first step and publishes it just
+    // before its last step's barrier: on multi-step tiles the atomic's round trip runs under
+    // the MMAs instead of holding warp 0 (and so the CTA) at the first step's barrier
+    int claimed = 0;
     for (int jb = 0; jb < nv; ++jb) {
       const bool last = jb + 1 == nv;
       if (jb == 0 && tnext < ntiles) {
         fetch_meta(tnext, nslot);
-        if (threadIdx.x == 0) s_tile[nslot == 2 ? 0 : nslot + 1] = gridDim.x + atomicAdd(counter, 1);
+        if (threadIdx.x == 0) claimed = gridDim.x + atomicAdd(counter, 1);
       }
+      if (last && threadIdx.x == 0 && tnext < ntiles) s_tile[nslot == 2 ? 0 : nslot + 1] = claimed;
       wait_panel(buf);  // this step's B panel has landed
       __syncthreads();  // every warp is done with the other buffer (and the new s_meta is visible)
       const double* Anext = nullptr;
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
         gather(slot, cls[2 + jb], buf ^ 1);
         Anext = op_rows(cls[9 + jb + 1]);
       } else if (tnext < ntiles) {
-        const int* ncls = classes + tiles[tnext].x * 17;
+        const int* ncls = s_cls[nslot];
         gather(nslot, ncls[1], buf ^ 1);
         Anext = op_rows(ncls[9]);
       }
@@ -420,7 +429,7 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
     if (tnext >= ntiles) break;
     ti = tnext;
     slot = nslot;
-    cls = classes + tiles[ti].x * 17;
+    cls = s_cls[slot];
   }
 }
 
