@@ -292,13 +292,22 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
 
   // a tile's column records and its class record into ring slot `slot` (read after the
   // next CTA barrier: no dependent global load at the tile boundary)
+  // (4-byte cp.async: the warp does not wait for the records here; they are waited for
+  // before the barrier of the current tile's last step, where they are first read)
   auto fetch_meta = [&](int tid, int slot) {
     const int4 tl = tiles[tid];
     for (int e = threadIdx.x; e < NT * CW; e += NTH) {
       const int c = e / CW;
-      s_meta[slot][e] = c < tl.z ? cols[(size_t)tl.y * CW + e] : -1;
+      if (c < tl.z)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(&s_meta[slot][e])),
+                     "l"(cols + (size_t)tl.y * CW + e));
+      else
+        s_meta[slot][e] = -1;
     }
-    if (threadIdx.x < 17) s_cls[slot][threadIdx.x] = classes[tl.x * 17 + threadIdx.x];
+    if (threadIdx.x < 17)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(&s_cls[slot][threadIdx.x])),
+                   "l"(classes + tl.x * 17 + threadIdx.x));
+    asm volatile("cp.async.commit_group;\n" ::);
   };
   // B panel of one step: every column's source row (KP doubles, contiguous) is one
   // cp.async.bulk copy (SASS UBLKCP) issued by warp 0, completing on the buffer's mbarrier;
@@ -347,6 +356,7 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
   int slot = 0;
   fetch_meta(ti, 0);
   if (threadIdx.x == 0) s_tile[1] = gridDim.x + atomicAdd(counter, 1);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int* cls = s_cls[0];
   gather(0, cls[1], 0);
@@ -374,6 +384,7 @@ __global__ void __launch_bounds__(Sib16Shape<KP>::NW * 32, MINB) k_m2l_sib16(
         if (threadIdx.x == 0) claimed = gridDim.x + atomicAdd(counter, 1);
       }
       if (last && threadIdx.x == 0 && tnext < ntiles) s_tile[nslot == 2 ? 0 : nslot + 1] = claimed;
+      if (last) asm volatile("cp.async.wait_all;\n" ::: "memory");  // the next tile's records
       wait_panel(buf);  // this step's B panel has landed
       __syncthreads();  // every warp is done with the other buffer (and the new s_meta is visible)
       const double* Anext = nullptr;
