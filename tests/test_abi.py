@@ -86,6 +86,8 @@ def test_distributed_entry_points_validate_without_gpu():
         assert L.fmm_setup_ex(ctypes.c_void_p(8), None, 10, ctypes.byref(opt), None, ctypes.byref(out)) == K.FMM_EINVAL
     assert L.fmm_matvec_owned(None, None, None, None) == K.FMM_EINVAL
     assert L.fmm_matvec_owned_host(None, None, None, None) == K.FMM_EINVAL
+    assert L.fmm_matvec_host_batch(None, None, None, 1, None) == K.FMM_EINVAL
+    assert L.fmm_matvec_owned_host_batch(None, None, None, 1, None) == K.FMM_EINVAL
     assert L.fmm_matvec_group(None, 0, None, None, 1, None) == K.FMM_EINVAL
     b, e = ctypes.c_int64(), ctypes.c_int64()
     assert L.fmm_owned_range(None, ctypes.byref(b), ctypes.byref(e)) == K.FMM_EINVAL
